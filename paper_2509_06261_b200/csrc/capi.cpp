@@ -1,0 +1,842 @@
+// capi.cpp -- the extern "C" boundary (include/kvslab.h).
+//
+// Exceptions never cross this layer: each entry point catches the kvslab
+// error classes (named after slabsim's, common.hpp:31-59) and maps them to
+// ks_status, keeping the message in a thread-local for ks_last_error().
+#include "kvslab.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kvslab/slab_pool.hpp"
+#include "launch.hpp"
+
+using kvslab::BlockHandle;
+using kvslab::SlabPool;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+ks_status fail(ks_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+template <class F>
+ks_status guarded(F&& f) {
+  try {
+    return f();
+  } catch (const kvslab::InvalidConfigError& e) {
+    return fail(KS_INVALID_CONFIG, e.what());
+  } catch (const kvslab::InvalidKeyError& e) {
+    return fail(KS_INVALID_KEY, e.what());
+  } catch (const kvslab::PoolExhaustedError& e) {
+    return fail(KS_EXHAUSTED, e.what());
+  } catch (const kvslab::InvalidFreeError& e) {
+    return fail(KS_INVALID_FREE, e.what());
+  } catch (const kvslab::InvalidProfileError& e) {
+    return fail(KS_INVALID_PROFILE, e.what());
+  } catch (const std::out_of_range& e) {
+    return fail(KS_INVALID_ARGUMENT, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(KS_INTERNAL, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(KS_INTERNAL, e.what());
+  }
+}
+
+ks_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(KS_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+ks_block_handle to_c(const BlockHandle& h) {
+  ks_block_handle o;
+  o.slab_id = h.slab_id;
+  o.local_block_id = h.local_block_id;
+  o.global_block_id = h.global_block_id;
+  o.key = h.key;
+  return o;
+}
+BlockHandle from_c(const ks_block_handle& h) {
+  BlockHandle o;
+  o.slab_id = h.slab_id;
+  o.local_block_id = h.local_block_id;
+  o.global_block_id = h.global_block_id;
+  o.key = h.key;
+  return o;
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+constexpr size_t kStageWords = 1u << 20;  // 4 MiB of uint32 staging
+
+}  // namespace
+
+struct ks_pool {
+  // Pinned host -> device staging ring for small control uploads (table
+  // deltas, move lists).  A slot is reused only after the kernel that read it
+  // completed (its event), so calls on different streams never race.
+  static constexpr int kSlots = 8;
+  static constexpr size_t kSlotWords = kStageWords / kSlots;
+  struct Slot {
+    uint32_t* h = nullptr;
+    uint32_t* d = nullptr;
+  };
+
+  std::unique_ptr<SlabPool> pool;
+  int device = -1;
+  int num_sms = 0;
+  uint8_t* d_base = nullptr;
+  uint64_t d_bytes = 0;
+  void* d_slab_table = nullptr;
+  uint32_t* h_stage = nullptr;  // pinned, kStageWords
+  uint32_t* d_stage = nullptr;  // device, kStageWords
+  cudaEvent_t slot_ev[kSlots] = {};
+  bool slot_pending[kSlots] = {};
+  int next_slot = 0;
+  ks_op_log_fn log_fn = nullptr;
+  void* log_user = nullptr;
+  ks_clock_fn clock_fn = nullptr;
+  void* clock_user = nullptr;
+  std::vector<uint32_t> dirty;
+
+  ~ks_pool() {
+    if (device >= 0) {
+      DeviceGuard g(device);
+      for (int i = 0; i < kSlots; ++i)
+        if (slot_ev[i]) cudaEventSynchronize(slot_ev[i]), cudaEventDestroy(slot_ev[i]);
+      cudaFree(d_base);
+      cudaFree(d_slab_table);
+      cudaFree(d_stage);
+      cudaFreeHost(h_stage);
+    }
+  }
+  // Next staging slot, waiting for its previous consumer if still running.
+  cudaError_t acquire(int* idx, Slot* s) {
+    const int i = next_slot;
+    next_slot = (next_slot + 1) % kSlots;
+    if (slot_pending[i]) {
+      slot_pending[i] = false;
+      cudaError_t e = cudaEventSynchronize(slot_ev[i]);
+      if (e != cudaSuccess) return e;
+    }
+    *idx = i;
+    s->h = h_stage + i * kSlotWords;
+    s->d = d_stage + i * kSlotWords;
+    return cudaSuccess;
+  }
+  cudaError_t upload(const Slot& s, size_t words, cudaStream_t st) {
+    return cudaMemcpyAsync(s.d, s.h, words * 4, cudaMemcpyHostToDevice, st);
+  }
+  // Marks the slot busy until the work just enqueued on `st` finishes.
+  cudaError_t release(int i, cudaStream_t st) {
+    cudaError_t e = cudaEventRecord(slot_ev[i], st);
+    slot_pending[i] = e == cudaSuccess;
+    return e;
+  }
+};
+
+namespace {
+
+uint32_t fmt_bits(uint32_t dt) { return dt == KS_KV_FP16 ? 16 : (dt == KS_KV_INT4 ? 4 : 8); }
+
+struct FmtInfo {
+  uint64_t token_size, chunk, layer_bytes, key, natural_qp;
+};
+ks_status fmt_info(const ks_kv_format* f, FmtInfo* o) {
+  if (!f) return fail(KS_INVALID_ARGUMENT, "null format");
+  if (f->kv_dtype > KS_KV_INT4) return fail(KS_INVALID_ARGUMENT, "unknown kv_dtype");
+  if (f->num_kv_heads == 0 || f->head_dim == 0 || f->num_layers == 0 || f->tokens_per_block == 0)
+    return fail(KS_INVALID_ARGUMENT, "format counts must be positive");
+  if (f->num_q_heads == 0 || f->num_q_heads % f->num_kv_heads != 0)
+    return fail(KS_INVALID_ARGUMENT, "num_q_heads must be a positive multiple of num_kv_heads");
+  const uint64_t bits = fmt_bits(f->kv_dtype);
+  const uint64_t H = f->num_kv_heads, T = f->tokens_per_block;
+  o->token_size = H * f->head_dim * 2 * bits / 8;
+  o->chunk = T * f->head_dim * bits / 8;
+  o->layer_bytes = T * o->token_size + f->quant_param_bytes_per_block;
+  o->key = f->num_layers * o->layer_bytes;
+  switch (f->kv_dtype) {
+    case KS_KV_FP8_E4M3: o->natural_qp = 2 * H * 4; break;
+    case KS_KV_INT8: o->natural_qp = 2 * H * T * 2; break;
+    case KS_KV_INT4: o->natural_qp = 2 * H * T * 4; break;
+    default: o->natural_qp = 0;
+  }
+  const uint64_t qp = f->quant_param_bytes_per_block;
+  const bool qp_ok = qp == o->natural_qp || (f->kv_dtype == KS_KV_FP8_E4M3 && qp == 0);
+  if (!qp_ok)
+    return fail(KS_INVALID_ARGUMENT, "quant_param_bytes_per_block must be the format's natural size");
+  return KS_OK;
+}
+
+ks_status check_kernel_format(const ks_pool* pool, const ks_kv_format* f, FmtInfo* fi) {
+  ks_status s = fmt_info(f, fi);
+  if (s != KS_OK) return s;
+  if (f->head_dim != 128) return fail(KS_NOT_SUPPORTED, "kernels require head_dim == 128");
+  if (f->tokens_per_block != 16) return fail(KS_NOT_SUPPORTED, "kernels require tokens_per_block == 16");
+  if (f->num_q_heads / f->num_kv_heads > 16) return fail(KS_NOT_SUPPORTED, "GQA group > 16");
+  if (!pool) return fail(KS_INVALID_ARGUMENT, "null pool");
+  if (pool->device < 0 || !pool->d_base) return fail(KS_INVALID_ARGUMENT, "pool has no device tensor");
+  if (pool->pool->slab_size() % 16 != 0 || fi->key % 16 != 0 || fi->layer_bytes % 16 != 0)
+    return fail(KS_NOT_SUPPORTED, "slab size, key and layer stride must be multiples of 16 bytes");
+  pool->pool->blocks_per_slab(fi->key);  // throws InvalidKeyError when unregistered
+  return KS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t ks_abi_version(void) { return KS_ABI_VERSION; }
+const char* ks_last_error(void) { return g_err.c_str(); }
+uint64_t ks_launch_count(void) { return g_launches.load(); }
+
+const char* ks_status_name(ks_status s) {
+  switch (s) {
+    case KS_OK: return "KS_OK";
+    case KS_INVALID_CONFIG: return "KS_INVALID_CONFIG";
+    case KS_INVALID_KEY: return "KS_INVALID_KEY";
+    case KS_EXHAUSTED: return "KS_EXHAUSTED";
+    case KS_INVALID_FREE: return "KS_INVALID_FREE";
+    case KS_INVALID_PROFILE: return "KS_INVALID_PROFILE";
+    case KS_INVALID_ARGUMENT: return "KS_INVALID_ARGUMENT";
+    case KS_CUDA_ERROR: return "KS_CUDA_ERROR";
+    case KS_NOT_SUPPORTED: return "KS_NOT_SUPPORTED";
+    default: return "KS_INTERNAL";
+  }
+}
+
+// ------------------------------------------------------------- geometry
+static kvslab::KvGeometry to_geo(const ks_model_geometry* g) {
+  kvslab::KvGeometry o;
+  o.num_kv_heads = g->num_kv_heads;
+  o.head_dim = g->head_dim;
+  o.num_layers = g->num_layers;
+  o.tp_degree = g->tp_degree;
+  o.tokens_per_block = g->tokens_per_block;
+  o.quant_param_bytes_per_block = g->quant_param_bytes_per_block;
+  o.kv_bits = g->kv_bits;
+  return o;
+}
+ks_status ks_token_size(const ks_model_geometry* g, uint64_t* out) {
+  return guarded([&] {
+    if (!g || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *out = kvslab::token_size(to_geo(g));
+    return KS_OK;
+  });
+}
+ks_status ks_kv_block_size(const ks_model_geometry* g, uint64_t* out) {
+  return guarded([&] {
+    if (!g || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *out = kvslab::kv_block_size(to_geo(g));
+    return KS_OK;
+  });
+}
+
+// ------------------------------------------------------------- pool
+ks_status ks_pool_create(const ks_pool_config* cfg, int device, ks_pool** out) {
+  return guarded([&] {
+    if (!cfg || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    kvslab::SlabPoolConfig c;
+    c.capacity_bytes = cfg->capacity_bytes;
+    c.slab_size_bytes = cfg->slab_size_bytes;
+    if (cfg->num_keys && !cfg->block_size_keys) return fail(KS_INVALID_ARGUMENT, "null keys");
+    c.block_size_keys.assign(cfg->block_size_keys, cfg->block_size_keys + cfg->num_keys);
+    c.require_lcm_alignment = cfg->require_lcm_alignment != 0;
+    auto p = std::make_unique<ks_pool>();
+    p->pool = std::make_unique<SlabPool>(c);
+    if (device >= 0) {
+      DeviceGuard g(device);
+      if (!g.ok) return fail(KS_CUDA_ERROR, "cudaSetDevice failed");
+      p->device = device;
+      cudaError_t e = cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+      p->d_bytes = p->pool->usable_capacity_bytes();
+      e = cudaMalloc(&p->d_base, p->d_bytes);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(KV tensor)");
+      const size_t tbytes = static_cast<size_t>(p->pool->slab_count()) * 16;
+      e = cudaMalloc(&p->d_slab_table, tbytes);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(slab table)");
+      e = cudaMemset(p->d_slab_table, 0, tbytes);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(slab table)");
+      e = cudaMallocHost(&p->h_stage, kStageWords * 4);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMallocHost(staging)");
+      e = cudaMalloc(&p->d_stage, kStageWords * 4);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+      for (int i = 0; i < ks_pool::kSlots; ++i) {
+        e = cudaEventCreateWithFlags(&p->slot_ev[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+      }
+      e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
+    }
+    *out = p.release();
+    return KS_OK;
+  });
+}
+
+ks_status ks_pool_destroy(ks_pool* pool) {
+  delete pool;
+  return KS_OK;
+}
+
+ks_status ks_pool_get_info(const ks_pool* pool, ks_pool_info* out) {
+  if (!pool || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+  const SlabPool& p = *pool->pool;
+  out->slab_count = p.slab_count();
+  out->num_keys = static_cast<uint32_t>(p.config().block_size_keys.size());
+  out->slab_size_bytes = p.slab_size();
+  out->tail_remainder_bytes = p.tail_remainder_bytes();
+  out->usable_capacity_bytes = p.usable_capacity_bytes();
+  out->allocated_blocks = p.allocated_block_count();
+  out->device = pool->device;
+  out->require_lcm_alignment = p.config().require_lcm_alignment ? 1 : 0;
+  return KS_OK;
+}
+
+ks_status ks_pool_keys(const ks_pool* pool, uint64_t* keys_out, uint32_t capacity) {
+  if (!pool || (!keys_out && capacity)) return fail(KS_INVALID_ARGUMENT, "null argument");
+  const auto& k = pool->pool->config().block_size_keys;
+  if (capacity < k.size()) return fail(KS_INVALID_ARGUMENT, "capacity too small");
+  std::copy(k.begin(), k.end(), keys_out);
+  return KS_OK;
+}
+
+ks_status ks_alloc_block(ks_pool* pool, uint64_t key, ks_block_handle* out) {
+  return guarded([&] {
+    if (!pool || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *out = to_c(pool->pool->alloc_block(key));
+    return KS_OK;
+  });
+}
+
+ks_status ks_try_alloc_block(ks_pool* pool, uint64_t key, ks_block_handle* out, int32_t* ok) {
+  return guarded([&] {
+    if (!pool || !out || !ok) return fail(KS_INVALID_ARGUMENT, "null argument");
+    auto h = pool->pool->try_alloc_block(key);
+    *ok = h ? 1 : 0;
+    if (h) *out = to_c(*h);
+    return KS_OK;
+  });
+}
+
+ks_status ks_alloc_blocks(ks_pool* pool, uint64_t key, uint32_t n, ks_block_handle* out,
+                          uint32_t* n_done) {
+  return guarded([&] {
+    if (!pool || (!out && n) || !n_done) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *n_done = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      auto h = pool->pool->try_alloc_block(key);
+      if (!h) break;
+      out[i] = to_c(*h);
+      ++*n_done;
+    }
+    return KS_OK;
+  });
+}
+
+ks_status ks_free_block(ks_pool* pool, const ks_block_handle* h) {
+  return guarded([&] {
+    if (!pool || !h) return fail(KS_INVALID_ARGUMENT, "null argument");
+    pool->pool->free_block(from_c(*h));
+    return KS_OK;
+  });
+}
+
+ks_status ks_free_blocks(ks_pool* pool, const ks_block_handle* hs, uint32_t n) {
+  return guarded([&] {
+    if (!pool || (!hs && n)) return fail(KS_INVALID_ARGUMENT, "null argument");
+    for (uint32_t i = 0; i < n; ++i) pool->pool->free_block(from_c(hs[i]));
+    return KS_OK;
+  });
+}
+
+ks_status ks_blocks_per_slab(const ks_pool* pool, uint64_t key, uint64_t* out) {
+  return guarded([&] {
+    if (!pool || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *out = pool->pool->blocks_per_slab(key);
+    return KS_OK;
+  });
+}
+
+ks_status ks_snapshot_stats(const ks_pool* pool, ks_frag_stats* out) {
+  if (!pool || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+  const auto s = pool->pool->snapshot_stats();
+  out->allocated_bytes = s.allocated_bytes;
+  out->free_block_bytes = s.free_block_bytes;
+  out->slab_residue_bytes = s.slab_residue_bytes;
+  out->free_slab_bytes = s.free_slab_bytes;
+  return KS_OK;
+}
+
+ks_status ks_free_blocks_for_key(const ks_pool* pool, uint64_t key, uint64_t* out) {
+  return guarded([&] {
+    if (!pool || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *out = pool->pool->free_blocks_for_key(key);
+    return KS_OK;
+  });
+}
+
+ks_status ks_allocated_block_count(const ks_pool* pool, uint64_t key, uint64_t* out) {
+  return guarded([&] {
+    if (!pool || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *out = key == 0 ? pool->pool->allocated_block_count() : pool->pool->allocated_block_count(key);
+    return KS_OK;
+  });
+}
+
+ks_status ks_slab_state(const ks_pool* pool, uint32_t slab_id, int32_t* state, uint64_t* key) {
+  return guarded([&] {
+    if (!pool || !state || !key) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *state = static_cast<int32_t>(pool->pool->slab_state(slab_id));
+    *key = pool->pool->slab_key(slab_id);
+    return KS_OK;
+  });
+}
+
+ks_status ks_check_integrity(const ks_pool* pool, int32_t* ok) {
+  if (!pool || !ok) return fail(KS_INVALID_ARGUMENT, "null argument");
+  std::string why;
+  *ok = pool->pool->check_integrity(&why) ? 1 : 0;
+  if (!*ok) g_err = why;
+  return KS_OK;
+}
+
+ks_status ks_pool_equal(const ks_pool* a, const ks_pool* b, int32_t* equal) {
+  if (!a || !b || !equal) return fail(KS_INVALID_ARGUMENT, "null argument");
+  *equal = (*a->pool == *b->pool) ? 1 : 0;
+  return KS_OK;
+}
+
+ks_status ks_pool_clone_host(const ks_pool* pool, ks_pool** out) {
+  return guarded([&] {
+    if (!pool || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    auto p = std::make_unique<ks_pool>();
+    p->pool = std::make_unique<SlabPool>(*pool->pool);
+    p->pool->set_op_log(nullptr);
+    p->pool->set_clock(nullptr);
+    *out = p.release();
+    return KS_OK;
+  });
+}
+
+ks_status ks_set_op_log(ks_pool* pool, ks_op_log_fn fn, void* user) {
+  if (!pool) return fail(KS_INVALID_ARGUMENT, "null pool");
+  pool->log_fn = fn;
+  pool->log_user = user;
+  if (!fn) {
+    pool->pool->set_op_log(nullptr);
+    return KS_OK;
+  }
+  pool->pool->set_op_log([pool](const kvslab::OpLogRecord& r) {
+    ks_op_record c;
+    c.seq = r.seq;
+    c.time = r.time;
+    c.op = r.op;
+    c.key = r.key;
+    c.slab_id = r.slab_id;
+    c.local_block_id = r.local_block_id;
+    c.global_block_id = r.global_block_id;
+    pool->log_fn(&c, pool->log_user);
+  });
+  return KS_OK;
+}
+
+ks_status ks_set_clock(ks_pool* pool, ks_clock_fn fn, void* user) {
+  if (!pool) return fail(KS_INVALID_ARGUMENT, "null pool");
+  pool->clock_fn = fn;
+  pool->clock_user = user;
+  if (!fn) {
+    pool->pool->set_clock(nullptr);
+  } else {
+    pool->pool->set_clock([pool]() { return pool->clock_fn(pool->clock_user); });
+  }
+  return KS_OK;
+}
+
+ks_status ks_debug_flip_occupancy_bit(ks_pool* pool, uint32_t slab_id, uint32_t local) {
+  return guarded([&] {
+    if (!pool) return fail(KS_INVALID_ARGUMENT, "null pool");
+    pool->pool->debug_flip_occupancy_bit(slab_id, local);
+    return KS_OK;
+  });
+}
+
+uint64_t ks_global_block_id(uint32_t slab_id, uint32_t local_block_id, uint64_t bps) {
+  return SlabPool::global_block_id(slab_id, local_block_id, bps);
+}
+void ks_split_global_block_id(uint64_t gid, uint64_t bps, uint32_t* slab_id, uint32_t* local) {
+  const auto [s, l] = SlabPool::split_global_block_id(gid, bps);
+  if (slab_id) *slab_id = s;
+  if (local) *local = l;
+}
+ks_status ks_block_byte_offset(const ks_pool* pool, uint64_t key, uint64_t gid, uint64_t* out) {
+  return guarded([&] {
+    if (!pool || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *out = pool->pool->block_byte_offset(key, gid);
+    return KS_OK;
+  });
+}
+
+// ------------------------------------------------------------- formats
+ks_status ks_natural_qparams(const ks_kv_format* fmt, uint64_t* out) {
+  if (!fmt || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+  ks_kv_format f = *fmt;
+  FmtInfo fi;
+  // natural size does not depend on the declared qparams; probe with it
+  const uint64_t H = f.num_kv_heads, T = f.tokens_per_block;
+  switch (f.kv_dtype) {
+    case KS_KV_FP16: *out = 0; break;
+    case KS_KV_FP8_E4M3: *out = 2 * H * 4; break;
+    case KS_KV_INT8: *out = 2 * H * T * 2; break;
+    case KS_KV_INT4: *out = 2 * H * T * 4; break;
+    default: return fail(KS_INVALID_ARGUMENT, "unknown kv_dtype");
+  }
+  (void)fi;
+  return KS_OK;
+}
+
+ks_status ks_format_key(const ks_kv_format* fmt, uint64_t* out) {
+  if (!out) return fail(KS_INVALID_ARGUMENT, "null argument");
+  FmtInfo fi;
+  ks_status s = fmt_info(fmt, &fi);
+  if (s != KS_OK) return s;
+  *out = fi.key;
+  return KS_OK;
+}
+
+ks_status ks_validate_format(const ks_pool* pool, const ks_kv_format* fmt) {
+  return guarded([&] {
+    FmtInfo fi;
+    return check_kernel_format(pool, fmt, &fi);
+  });
+}
+
+// ------------------------------------------------------------- device
+ks_status ks_device_base(const ks_pool* pool, void** d_base, uint64_t* bytes) {
+  if (!pool || !d_base) return fail(KS_INVALID_ARGUMENT, "null argument");
+  *d_base = pool->d_base;
+  if (bytes) *bytes = pool->d_bytes;
+  return KS_OK;
+}
+
+ks_status ks_slab_table_device(const ks_pool* pool, const void** d_table) {
+  if (!pool || !d_table) return fail(KS_INVALID_ARGUMENT, "null argument");
+  *d_table = pool->d_slab_table;
+  return KS_OK;
+}
+
+ks_status ks_slab_table_sync(ks_pool* pool, void* stream) {
+  return guarded([&] {
+    if (!pool || pool->device < 0) return fail(KS_INVALID_ARGUMENT, "pool has no device tensor");
+    DeviceGuard g(pool->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    pool->pool->drain_dirty_slabs(&pool->dirty);
+    size_t i = 0;
+    while (i < pool->dirty.size()) {
+      const size_t n = std::min(pool->dirty.size() - i, ks_pool::kSlotWords / 5);
+      int si = 0;
+      ks_pool::Slot sl;
+      cudaError_t e = pool->acquire(&si, &sl);
+      if (e != cudaSuccess) return cuda_fail(e, "staging wait");
+      for (size_t j = 0; j < n; ++j) {
+        const uint32_t slab = pool->dirty[i + j];
+        const uint64_t key = pool->pool->slab_key(slab);
+        uint32_t* w = sl.h + 5 * j;
+        w[0] = slab;
+        w[1] = static_cast<uint32_t>(key);
+        w[2] = static_cast<uint32_t>(key >> 32);
+        w[3] = pool->pool->slab_blocks_total(slab);
+        w[4] = static_cast<uint32_t>(pool->pool->slab_state(slab));
+      }
+      e = pool->upload(sl, 5 * n, s);
+      if (e != cudaSuccess) return cuda_fail(e, "staging upload");
+      e = kvslab::launch_slab_table_scatter(pool->d_slab_table, sl.d, static_cast<uint32_t>(n), s);
+      if (e != cudaSuccess) return cuda_fail(e, "slab table scatter");
+      e = pool->release(si, s);
+      if (e != cudaSuccess) return cuda_fail(e, "staging release");
+      ++g_launches;
+      i += n;
+    }
+    return KS_OK;
+  });
+}
+
+ks_status ks_block_table_update(ks_pool* pool, int32_t* d_table, uint32_t row_stride,
+                                const int32_t* rows, const int32_t* cols, const int32_t* vals,
+                                uint32_t n, void* stream) {
+  return guarded([&] {
+    if (!pool || pool->device < 0) return fail(KS_INVALID_ARGUMENT, "pool has no device tensor");
+    if (n == 0) return KS_OK;
+    if (!d_table || !rows || !cols || !vals) return fail(KS_INVALID_ARGUMENT, "null argument");
+    DeviceGuard g(pool->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t i = 0;
+    while (i < n) {
+      const uint32_t m = static_cast<uint32_t>(std::min<size_t>(n - i, ks_pool::kSlotWords / 3));
+      int si = 0;
+      ks_pool::Slot sl;
+      cudaError_t e = pool->acquire(&si, &sl);
+      if (e != cudaSuccess) return cuda_fail(e, "staging wait");
+      for (uint32_t j = 0; j < m; ++j) {
+        sl.h[3 * j] = static_cast<uint32_t>(rows[i + j]);
+        sl.h[3 * j + 1] = static_cast<uint32_t>(cols[i + j]);
+        sl.h[3 * j + 2] = static_cast<uint32_t>(vals[i + j]);
+      }
+      e = pool->upload(sl, 3 * static_cast<size_t>(m), s);
+      if (e != cudaSuccess) return cuda_fail(e, "staging upload");
+      e = kvslab::launch_table_scatter(d_table, row_stride, reinterpret_cast<const int32_t*>(sl.d),
+                                       m, s);
+      if (e != cudaSuccess) return cuda_fail(e, "table scatter");
+      e = pool->release(si, s);
+      if (e != cudaSuccess) return cuda_fail(e, "staging release");
+      ++g_launches;
+      i += m;
+    }
+    return KS_OK;
+  });
+}
+
+ks_status ks_block_table_validate(ks_pool* pool, uint64_t key, const int32_t* d_table,
+                                  uint32_t row_stride, const int32_t* d_ctx_lens, uint32_t rows,
+                                  uint32_t tpb, void* stream, uint64_t* n_bad) {
+  return guarded([&] {
+    if (!pool || pool->device < 0 || !n_bad || tpb == 0)
+      return fail(KS_INVALID_ARGUMENT, "bad argument");
+    const uint64_t bps = pool->pool->blocks_per_slab(key);
+    DeviceGuard g(pool->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int si = 0;
+    ks_pool::Slot sl;
+    cudaError_t e = pool->acquire(&si, &sl);
+    if (e != cudaSuccess) return cuda_fail(e, "staging wait");
+    e = cudaMemsetAsync(sl.d, 0, 8, s);
+    if (e != cudaSuccess) return cuda_fail(e, "memset");
+    e = kvslab::launch_table_validate(d_table, row_stride, d_ctx_lens, rows, tpb,
+                                      pool->d_slab_table, pool->pool->slab_count(), key,
+                                      kvslab::dev::make_fastdiv(static_cast<uint32_t>(bps)),
+                                      reinterpret_cast<unsigned long long*>(sl.d), s);
+    if (e != cudaSuccess) return cuda_fail(e, "validate");
+    ++g_launches;
+    unsigned long long bad = 0;
+    e = cudaMemcpyAsync(&bad, sl.d, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "validate readback");
+    *n_bad = bad;
+    return KS_OK;
+  });
+}
+
+ks_status ks_kv_append(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_k,
+                       const void* d_v, uint32_t n_tokens, const int32_t* d_tok_seq,
+                       const int32_t* d_tok_pos, const int32_t* d_block_table, uint32_t bt_stride,
+                       const float* d_kv_scales, void* stream) {
+  return guarded([&] {
+    FmtInfo fi;
+    ks_status st = check_kernel_format(pool, fmt, &fi);
+    if (st != KS_OK) return st;
+    if (layer >= fmt->num_layers) return fail(KS_INVALID_ARGUMENT, "layer out of range");
+    if (n_tokens == 0) return KS_OK;
+    if (!d_k || !d_v || !d_tok_seq || !d_tok_pos || !d_block_table)
+      return fail(KS_INVALID_ARGUMENT, "null device pointer");
+    DeviceGuard g(pool->device);
+    kvslab::AppendParams p{};
+    p.pool = pool->d_base;
+    p.geom.slab_size = pool->pool->slab_size();
+    p.geom.key = fi.key;
+    p.geom.bps = kvslab::dev::make_fastdiv(static_cast<uint32_t>(pool->pool->blocks_per_slab(fi.key)));
+    p.layer_off = static_cast<uint64_t>(layer) * fi.layer_bytes;
+    p.H = fmt->num_kv_heads;
+    p.D = fmt->head_dim;
+    p.tpb = fmt->tokens_per_block;
+    p.chunk_bytes = static_cast<uint32_t>(fi.chunk);
+    p.params_off = static_cast<uint32_t>(2 * p.H * fi.chunk);
+    p.fp8_inblock = fmt->kv_dtype == KS_KV_FP8_E4M3 && fmt->quant_param_bytes_per_block > 0;
+    p.k = static_cast<const __half*>(d_k);
+    p.v = static_cast<const __half*>(d_v);
+    p.n_tokens = n_tokens;
+    p.tok_seq = d_tok_seq;
+    p.tok_pos = d_tok_pos;
+    p.block_table = d_block_table;
+    p.bt_stride = bt_stride;
+    p.kv_scales = d_kv_scales;
+    cudaError_t e = kvslab::launch_kv_append(p, static_cast<int>(fmt->kv_dtype),
+                                             static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "kv_append launch");
+    ++g_launches;
+    return KS_OK;
+  });
+}
+
+ks_status ks_paged_decode_workspace_size(const ks_pool* pool, const ks_kv_format* fmt,
+                                         uint32_t batch, size_t* bytes) {
+  if (!pool || !fmt || !bytes) return fail(KS_INVALID_ARGUMENT, "null argument");
+  const int sms = pool->num_sms > 0 ? pool->num_sms : 148;
+  const size_t part = kvslab::decode_partials_bytes(sms, static_cast<int>(fmt->num_q_heads / std::max(1u, fmt->num_kv_heads)));
+  *bytes = part + (static_cast<size_t>(batch) * fmt->num_kv_heads * 4 + 255) / 256 * 256;
+  return KS_OK;
+}
+
+ks_status ks_paged_decode(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
+                          void* d_out, float* d_lse, const int32_t* d_block_table,
+                          uint32_t bt_stride, const int32_t* d_ctx_lens, uint32_t batch,
+                          float sm_scale, const float* d_kv_scales, void* d_workspace,
+                          size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    FmtInfo fi;
+    ks_status st = check_kernel_format(pool, fmt, &fi);
+    if (st != KS_OK) return st;
+    if (layer >= fmt->num_layers) return fail(KS_INVALID_ARGUMENT, "layer out of range");
+    if (batch == 0) return KS_OK;
+    if (!d_q || !d_out || !d_block_table || !d_ctx_lens || !d_workspace)
+      return fail(KS_INVALID_ARGUMENT, "null device pointer");
+    size_t need = 0;
+    ks_paged_decode_workspace_size(pool, fmt, batch, &need);
+    if (workspace_bytes < need) return fail(KS_INVALID_ARGUMENT, "workspace too small");
+    if (batch > 8192) return fail(KS_NOT_SUPPORTED, "batch > 8192 per launch");
+    DeviceGuard g(pool->device);
+    kvslab::DecodeParams p{};
+    p.pool = pool->d_base;
+    p.geom.slab_size = pool->pool->slab_size();
+    p.geom.key = fi.key;
+    p.geom.bps = kvslab::dev::make_fastdiv(static_cast<uint32_t>(pool->pool->blocks_per_slab(fi.key)));
+    p.layer_off = static_cast<uint64_t>(layer) * fi.layer_bytes;
+    p.H = fmt->num_kv_heads;
+    p.G = fmt->num_q_heads / fmt->num_kv_heads;
+    p.q = static_cast<const __half*>(d_q);
+    p.out = static_cast<__half*>(d_out);
+    p.lse = d_lse;
+    p.block_table = d_block_table;
+    p.bt_stride = bt_stride;
+    p.ctx_lens = d_ctx_lens;
+    p.batch = batch;
+    const float scale = sm_scale > 0.f ? sm_scale : 1.0f / std::sqrt(static_cast<float>(fmt->head_dim));
+    p.sm_scale_log2 = scale * 1.4426950408889634f;
+    p.kv_scales = fmt->kv_dtype == KS_KV_FP8_E4M3 ? d_kv_scales : nullptr;
+    const size_t part = kvslab::decode_partials_bytes(pool->num_sms, static_cast<int>(p.G));
+    p.partials = static_cast<float*>(d_workspace);
+    p.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_workspace) + part);
+    p.max_ctas = 0;
+    cudaError_t e = kvslab::launch_paged_decode(p, static_cast<int>(fmt->kv_dtype), pool->num_sms,
+                                                static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "paged_decode launch");
+    ++g_launches;
+    return KS_OK;
+  });
+}
+
+ks_status ks_compact_plan(ks_pool* pool, uint64_t key, uint32_t max_moves, ks_block_move* moves,
+                          uint32_t* n_moves, uint32_t* slabs_freed) {
+  return guarded([&] {
+    if (!pool || !n_moves || (!moves && max_moves)) return fail(KS_INVALID_ARGUMENT, "null argument");
+    uint32_t freed = 0;
+    auto mv = pool->pool->plan_compaction(key, max_moves, &freed);
+    for (size_t i = 0; i < mv.size(); ++i) {
+      moves[i].src_global_block_id = mv[i].src.global_block_id;
+      moves[i].dst_global_block_id = mv[i].dst.global_block_id;
+    }
+    *n_moves = static_cast<uint32_t>(mv.size());
+    if (slabs_freed) *slabs_freed = freed;
+    return KS_OK;
+  });
+}
+
+ks_status ks_compact_apply(ks_pool* pool, uint64_t key, const ks_block_move* moves, uint32_t n,
+                           void* stream) {
+  return guarded([&] {
+    if (!pool || pool->device < 0) return fail(KS_INVALID_ARGUMENT, "pool has no device tensor");
+    if (n == 0) return KS_OK;
+    if (!moves) return fail(KS_INVALID_ARGUMENT, "null moves");
+    if (key % 16 != 0 || pool->pool->slab_size() % 16 != 0)
+      return fail(KS_NOT_SUPPORTED, "key and slab size must be multiples of 16 bytes");
+    const uint64_t bps = pool->pool->blocks_per_slab(key);
+    DeviceGuard g(pool->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t i = 0;
+    while (i < n) {
+      const uint32_t m = static_cast<uint32_t>(std::min<size_t>(n - i, ks_pool::kSlotWords / 2));
+      int si = 0;
+      ks_pool::Slot sl;
+      cudaError_t e = pool->acquire(&si, &sl);
+      if (e != cudaSuccess) return cuda_fail(e, "staging wait");
+      for (uint32_t j = 0; j < m; ++j) {
+        sl.h[j] = static_cast<uint32_t>(moves[i + j].src_global_block_id);
+        sl.h[m + j] = static_cast<uint32_t>(moves[i + j].dst_global_block_id);
+      }
+      e = pool->upload(sl, 2 * static_cast<size_t>(m), s);
+      if (e != cudaSuccess) return cuda_fail(e, "staging upload");
+      kvslab::CompactParams p{};
+      p.pool = pool->d_base;
+      p.geom.slab_size = pool->pool->slab_size();
+      p.geom.key = key;
+      p.geom.bps = kvslab::dev::make_fastdiv(static_cast<uint32_t>(bps));
+      p.src_gid = sl.d;
+      p.dst_gid = sl.d + m;
+      p.n_moves = m;
+      e = kvslab::launch_compact(p, pool->num_sms, s);
+      if (e != cudaSuccess) return cuda_fail(e, "compact launch");
+      e = pool->release(si, s);
+      if (e != cudaSuccess) return cuda_fail(e, "staging release");
+      ++g_launches;
+      i += m;
+    }
+    return KS_OK;
+  });
+}
+
+ks_status ks_block_table_remap(ks_pool* pool, int32_t* d_table, uint64_t n_entries,
+                               const ks_block_move* moves, uint32_t n, void* stream) {
+  return guarded([&] {
+    if (!pool || pool->device < 0) return fail(KS_INVALID_ARGUMENT, "pool has no device tensor");
+    if (n == 0 || n_entries == 0) return KS_OK;
+    if (!d_table || !moves) return fail(KS_INVALID_ARGUMENT, "null argument");
+    if (2ull * n > ks_pool::kSlotWords) return fail(KS_NOT_SUPPORTED, "too many moves for one remap");
+    std::vector<std::pair<uint32_t, uint32_t>> v(n);
+    for (uint32_t i = 0; i < n; ++i)
+      v[i] = {static_cast<uint32_t>(moves[i].src_global_block_id),
+              static_cast<uint32_t>(moves[i].dst_global_block_id)};
+    std::sort(v.begin(), v.end());
+    DeviceGuard g(pool->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int si = 0;
+    ks_pool::Slot sl;
+    cudaError_t e = pool->acquire(&si, &sl);
+    if (e != cudaSuccess) return cuda_fail(e, "staging wait");
+    for (uint32_t i = 0; i < n; ++i) {
+      sl.h[i] = v[i].first;
+      sl.h[n + i] = v[i].second;
+    }
+    e = pool->upload(sl, 2 * static_cast<size_t>(n), s);
+    if (e != cudaSuccess) return cuda_fail(e, "staging upload");
+    e = kvslab::launch_table_remap(d_table, n_entries, sl.d, sl.d + n, n, s);
+    if (e != cudaSuccess) return cuda_fail(e, "remap launch");
+    e = pool->release(si, s);
+    if (e != cudaSuccess) return cuda_fail(e, "staging release");
+    ++g_launches;
+    return KS_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,708 @@
+// decode.cu -- K2: slab-indexed paged decode attention for sm_100a.
+//
+// Replaces the reference's simulated attention cost (simulator.cpp:602-604,
+// "dur = gamma + delta*active + epsilon*sum(cached)") with the real read of
+// every cached K/V byte through the slab indirection.  Output matches
+// oracle/kvslab_oracle.c orc_paged_decode (fp64) within 1e-3 (FP16/FP8) or
+// 1e-2 (INT8/INT4) relative.
+//
+// Design:
+//  * Work = every (sequence, kv-head, block) of the batch, flattened
+//    seq-major; each warp of a persistent grid owns an equal contiguous range
+//    (stream-K style), so ragged contexts balance perfectly.  A unit (seq,
+//    kv-head) cut by a range boundary produces fp32 partials that the last
+//    finishing warp merges (per-unit counter; no second launch).
+//  * Each warp runs its own STAGES-deep ring: lane 0 issues 1-D
+//    cp.async.bulk copies (TMA engine) of the K chunk, V chunk, their
+//    quant params and -- at a unit start -- the G query rows, completing on a
+//    per-stage mbarrier.  Block-table entries are prefetched one block ahead.
+//  * QK^T and PV run on tensor cores as m16n8k16 tiles with the query group
+//    as N (8 or 16): S^T = K.Q^T (M = 16 tokens), O^T += V^T.P^T (M = dims).
+//    Quantised K/V enter the MMA as exact small integers (or e4m3 -> f16);
+//    per-token scales/zeros are applied to the 16x8 score tile and folded
+//    into P, so dequantisation costs no extra multiply per element.
+//  * The swizzled chunk layout plus the per-format fragment <-> dim/token
+//    permutations make every shared-memory fragment load conflict-free.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kvslab_device.cuh"
+#include "launch.hpp"
+
+namespace kvslab {
+namespace dev {
+
+constexpr int kD = 128;   // head dim
+constexpr int kTPB = 16;  // tokens per block
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int FMT>
+struct Geo {
+  static constexpr int kRow = kD * Fmt<FMT>::kBits / 8;  // bytes per token row
+  static constexpr int kChunk = kTPB * kRow;              // bytes per (K|V, head) chunk
+  static constexpr int kParam = FMT == kINT8 ? kTPB * 2 : (FMT == kINT4 ? kTPB * 4 : 0);
+};
+
+// ------------------------------------------------------------------ cursor
+// Walks the flattened (seq, head, block) space using the per-CTA prefix.
+struct Cursor {
+  uint32_t s, h, b, nblk;
+};
+__device__ __forceinline__ uint32_t nblk_of(const uint32_t* pre, uint32_t s, uint32_t H) {
+  return (pre[s + 1] - pre[s]) / H;
+}
+__device__ __forceinline__ void cursor_seek(Cursor& c, const uint32_t* pre, uint32_t batch,
+                                            uint32_t H, uint32_t idx) {
+  // largest s with pre[s] <= idx
+  uint32_t lo = 0, hi = batch;  // pre[batch] = total > idx
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (pre[mid] <= idx) lo = mid; else hi = mid;
+  }
+  c.s = lo;
+  c.nblk = nblk_of(pre, lo, H);
+  const uint32_t off = idx - pre[lo];
+  c.h = off / c.nblk;
+  c.b = off - c.h * c.nblk;
+}
+__device__ __forceinline__ void cursor_next(Cursor& c, const uint32_t* pre, uint32_t batch,
+                                            uint32_t H) {
+  if (++c.b < c.nblk) return;
+  c.b = 0;
+  if (++c.h < H) return;
+  c.h = 0;
+  do {
+    ++c.s;
+  } while (c.s < batch && pre[c.s + 1] == pre[c.s]);
+  if (c.s < batch) c.nblk = nblk_of(pre, c.s, H);
+}
+
+// ------------------------------------------------------ fragment loaders
+// K tile as the MMA A operand (rows = tokens g, g+8; k = dims permuted per
+// format, see header).  a[kk][0..3] for k-step kk.
+template <int FMT>
+__device__ __forceinline__ void load_k_frags(uint32_t sK, int g, int t, uint32_t (&a)[8][4]) {
+  if constexpr (FMT == kFP16) {
+    const int gt = (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}[t]
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int G = 8 * (c >> 1) + gt + 2 * (c & 1);
+      const uint4 lo = lds128(sK + swz(g * 256 + 16 * G));
+      const uint4 hi = lds128(sK + swz((g + 8) * 256 + 16 * G));
+      a[2 * c][0] = lo.x; a[2 * c][1] = hi.x; a[2 * c][2] = lo.y; a[2 * c][3] = hi.y;
+      a[2 * c + 1][0] = lo.z; a[2 * c + 1][1] = hi.z; a[2 * c + 1][2] = lo.w; a[2 * c + 1][3] = hi.w;
+    }
+  } else if constexpr (FMT == kFP8 || FMT == kINT8) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int G = 2 * t + c;
+      const uint4 lo = lds128(sK + swz(g * 128 + 16 * G));
+      const uint4 hi = lds128(sK + swz((g + 8) * 128 + 16 * G));
+      const uint32_t wl[4] = {lo.x, lo.y, lo.z, lo.w};
+      const uint32_t wh[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t* r = a[4 * c + e];
+        if constexpr (FMT == kFP8) {
+          r[0] = e4m3x2_to_f16x2(static_cast<uint16_t>(wl[e] & 0xffff));
+          r[2] = e4m3x2_to_f16x2(static_cast<uint16_t>(wl[e] >> 16));
+          r[1] = e4m3x2_to_f16x2(static_cast<uint16_t>(wh[e] & 0xffff));
+          r[3] = e4m3x2_to_f16x2(static_cast<uint16_t>(wh[e] >> 16));
+        } else {
+          const uint32_t xl = wl[e] ^ 0x80808080u, xh = wh[e] ^ 0x80808080u;
+          r[0] = hsub2_u32(__byte_perm(xl, 0x64646464u, 0x4140), 0x64806480u);
+          r[2] = hsub2_u32(__byte_perm(xl, 0x64646464u, 0x4342), 0x64806480u);
+          r[1] = hsub2_u32(__byte_perm(xh, 0x64646464u, 0x4140), 0x64806480u);
+          r[3] = hsub2_u32(__byte_perm(xh, 0x64646464u, 0x4342), 0x64806480u);
+        }
+      }
+    }
+  } else {  // INT4: one granule (32 dims) per row per thread
+    const uint4 lo = lds128(sK + swz(g * 64 + 16 * t));
+    const uint4 hi = lds128(sK + swz((g + 8) * 64 + 16 * t));
+    const uint32_t wl[4] = {lo.x, lo.y, lo.z, lo.w};
+    const uint32_t wh[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        uint32_t* r = a[2 * i + e];
+        r[0] = hsub2_u32(lop3_and_or(wl[i] >> (8 * e), 0x000F000Fu, 0x64006400u), 0x64006400u);
+        r[2] = hsub2_u32(lop3_and_or(wl[i] >> (8 * e + 4), 0x000F000Fu, 0x64006400u), 0x64006400u);
+        r[1] = hsub2_u32(lop3_and_or(wh[i] >> (8 * e), 0x000F000Fu, 0x64006400u), 0x64006400u);
+        r[3] = hsub2_u32(lop3_and_or(wh[i] >> (8 * e + 4), 0x000F000Fu, 0x64006400u), 0x64006400u);
+      }
+    }
+  }
+}
+
+// dims pi(kk, t, j) of the K permutation (used to gather Q into B fragments)
+template <int FMT>
+__device__ __forceinline__ int kdim(int kk, int t, int j) {
+  if constexpr (FMT == kFP16) {
+    const int gt = (t & 1) + ((t >> 1) << 2);
+    const int c = kk >> 1, e = kk & 1;
+    const int G = 8 * (c >> 1) + gt + 2 * (c & 1);
+    return 8 * G + 4 * e + j;
+  } else if constexpr (FMT == kFP8 || FMT == kINT8) {
+    return 32 * t + 4 * kk + j;
+  } else {
+    const int i = kk >> 1, e = kk & 1;
+    const int base = 32 * t + 8 * i + 2 * e;
+    return base + (j == 0 ? 0 : j == 1 ? 4 : j == 2 ? 1 : 5);
+  }
+}
+
+// token held in PV k-slot: slot 2t -> ta(t), 2t+1 -> tb(t), +8 for 2t+8/2t+9
+template <int FMT>
+__device__ __forceinline__ int tok_a(int t) {
+  if constexpr (FMT == kFP16) return t;
+  else if constexpr (FMT == kINT4) return (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}
+  else return 2 * t;
+}
+template <int FMT>
+__device__ __forceinline__ int tok_b(int t) {
+  if constexpr (FMT == kFP16) return t + 4;
+  else if constexpr (FMT == kINT4) return 2 + (t & 1) + ((t >> 1) << 2);  // {2,3,6,7}
+  else return 2 * t + 1;
+}
+
+// V tile as the MMA A operand of O^T = V^T P^T (rows = dims, k = tokens).
+// a[mt][0..3] for the 8 m-tiles; dim of (mt, row r8) given by vdim().
+template <int FMT>
+__device__ __forceinline__ void load_v_frags(uint32_t sV, int g, int t, uint32_t (&a)[8][4]) {
+  const int ta = tok_a<FMT>(t), tb = tok_b<FMT>(t);
+  if constexpr (FMT == kFP16) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int G = g + 8 * h;
+      const uint4 va = lds128(sV + swz(ta * 256 + 16 * G));
+      const uint4 vb = lds128(sV + swz(tb * 256 + 16 * G));
+      const uint4 vc = lds128(sV + swz((ta + 8) * 256 + 16 * G));
+      const uint4 vd = lds128(sV + swz((tb + 8) * 256 + 16 * G));
+      const uint32_t A[4] = {va.x, va.y, va.z, va.w}, B[4] = {vb.x, vb.y, vb.z, vb.w};
+      const uint32_t C[4] = {vc.x, vc.y, vc.z, vc.w}, Dd[4] = {vd.x, vd.y, vd.z, vd.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t* r = a[4 * h + i];
+        r[0] = __byte_perm(A[i], B[i], 0x5410);
+        r[1] = __byte_perm(A[i], B[i], 0x7632);
+        r[2] = __byte_perm(C[i], Dd[i], 0x5410);
+        r[3] = __byte_perm(C[i], Dd[i], 0x7632);
+      }
+    }
+  } else if constexpr (FMT == kFP8 || FMT == kINT8) {
+    const uint4 va = lds128(sV + swz(ta * 128 + 16 * g));
+    const uint4 vb = lds128(sV + swz(tb * 128 + 16 * g));
+    const uint4 vc = lds128(sV + swz((ta + 8) * 128 + 16 * g));
+    const uint4 vd = lds128(sV + swz((tb + 8) * 128 + 16 * g));
+    uint32_t A[4] = {va.x, va.y, va.z, va.w}, B[4] = {vb.x, vb.y, vb.z, vb.w};
+    uint32_t C[4] = {vc.x, vc.y, vc.z, vc.w}, Dd[4] = {vd.x, vd.y, vd.z, vd.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint32_t sel = e == 0 ? 0x5140u : 0x7362u;
+        uint32_t* r = a[2 * j + e];
+        if constexpr (FMT == kFP8) {
+          const uint32_t ab = __byte_perm(A[j], B[j], sel), cd = __byte_perm(C[j], Dd[j], sel);
+          r[0] = e4m3x2_to_f16x2(static_cast<uint16_t>(ab & 0xffff));
+          r[1] = e4m3x2_to_f16x2(static_cast<uint16_t>(ab >> 16));
+          r[2] = e4m3x2_to_f16x2(static_cast<uint16_t>(cd & 0xffff));
+          r[3] = e4m3x2_to_f16x2(static_cast<uint16_t>(cd >> 16));
+        } else {
+          const uint32_t ab = __byte_perm(A[j] ^ 0x80808080u, B[j] ^ 0x80808080u, sel);
+          const uint32_t cd = __byte_perm(C[j] ^ 0x80808080u, Dd[j] ^ 0x80808080u, sel);
+          r[0] = hsub2_u32(__byte_perm(ab, 0x64646464u, 0x4140), 0x64806480u);
+          r[1] = hsub2_u32(__byte_perm(ab, 0x64646464u, 0x4342), 0x64806480u);
+          r[2] = hsub2_u32(__byte_perm(cd, 0x64646464u, 0x4140), 0x64806480u);
+          r[3] = hsub2_u32(__byte_perm(cd, 0x64646464u, 0x4342), 0x64806480u);
+        }
+      }
+    }
+  } else {  // INT4: 8 bytes (16 dims) per token per thread
+    const uint32_t off = 8 * g;
+    const uint2 va = lds64(sV + swz(ta * 64 + off));
+    const uint2 vb = lds64(sV + swz(tb * 64 + off));
+    const uint2 vc = lds64(sV + swz((ta + 8) * 64 + off));
+    const uint2 vd = lds64(sV + swz((tb + 8) * 64 + off));
+    const uint32_t A[2] = {va.x, va.y}, B[2] = {vb.x, vb.y}, C[2] = {vc.x, vc.y},
+                   Dd[2] = {vd.x, vd.y};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int w = i >> 2, k = i & 3;
+      // bytes [A.k, A.k, B.k, B.k]: A.k in the low half, B.k in the high half
+      const uint32_t sel = k | (k << 4) | ((4 + k) << 8) | ((4 + k) << 12);
+      const uint32_t ab = __byte_perm(A[w], B[w], sel);
+      const uint32_t cd = __byte_perm(C[w], Dd[w], sel);
+      uint32_t* r = a[i];
+      r[0] = hsub2_u32(lop3_and_or(ab, 0x000F000Fu, 0x64006400u), 0x64006400u);
+      r[1] = hsub2_u32(lop3_and_or(ab >> 4, 0x000F000Fu, 0x64006400u), 0x64006400u);
+      r[2] = hsub2_u32(lop3_and_or(cd, 0x000F000Fu, 0x64006400u), 0x64006400u);
+      r[3] = hsub2_u32(lop3_and_or(cd >> 4, 0x000F000Fu, 0x64006400u), 0x64006400u);
+    }
+  }
+}
+// output dim of V m-tile mt, row half r8 (0: row g, 1: row g+8)
+template <int FMT>
+__device__ __forceinline__ int vdim(int mt, int g, int r8) {
+  if constexpr (FMT == kFP16) return 64 * (mt >> 2) + 8 * g + 2 * (mt & 3) + r8;
+  else return 16 * g + 2 * mt + r8;
+}
+
+// ------------------------------------------------------------------ kernel
+template <int FMT, int NT, int STAGES>
+__global__ void __launch_bounds__(kDecodeWarps * 32)
+paged_decode_kernel(const DecodeParams p) {
+  using Gm = Geo<FMT>;
+  constexpr int kNQ = NT * 8;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  // ---- per-CTA prefix of blocks over sequences (x H) ----
+  uint32_t* pre = reinterpret_cast<uint32_t*>(smem + p.prefix_offset);
+  {
+    const uint32_t nthr = blockDim.x, per = (p.batch + nthr - 1) / nthr;
+    const uint32_t b0 = min(p.batch, threadIdx.x * per), b1 = min(p.batch, b0 + per);
+    uint32_t sum = 0;
+    for (uint32_t s = b0; s < b1; ++s) {
+      const int c = p.ctx_lens[s];
+      sum += c > 0 ? (static_cast<uint32_t>(c) + kTPB - 1) / kTPB : 0;
+    }
+    __shared__ uint32_t wsum[kDecodeWarps];
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    uint32_t wbase = 0;
+    for (int w = 0; w < warp; ++w) wbase += wsum[w];
+    uint32_t run = wbase + incl - sum;
+    for (uint32_t s = b0; s < b1; ++s) {
+      pre[s] = run * p.H;
+      const int c = p.ctx_lens[s];
+      run += c > 0 ? (static_cast<uint32_t>(c) + kTPB - 1) / kTPB : 0;
+    }
+    if (threadIdx.x == nthr - 1) pre[p.batch] = run * p.H;
+    __syncthreads();
+  }
+  const uint32_t total = pre[p.batch];
+
+  // CTA 0 writes empty outputs for sequences with no context.
+  if (blockIdx.x == 0) {
+    for (uint32_t s = threadIdx.x; s < p.batch; s += blockDim.x) {
+      if (pre[s + 1] != pre[s]) continue;
+      for (uint32_t i = 0; i < p.H * p.G * kD; ++i)
+        p.out[(static_cast<uint64_t>(s) * p.H * p.G) * kD + i] = __float2half(0.f);
+      if (p.lse)
+        for (uint32_t i = 0; i < p.H * p.G; ++i) p.lse[s * p.H * p.G + i] = -INFINITY;
+    }
+  }
+
+  const uint32_t W = gridDim.x * kDecodeWarps;
+  const uint32_t wid = blockIdx.x * kDecodeWarps + warp;
+  const uint32_t start = static_cast<uint32_t>((static_cast<uint64_t>(wid) * total) / W);
+  const uint32_t end = static_cast<uint32_t>((static_cast<uint64_t>(wid + 1) * total) / W);
+  if (start >= end) return;
+  const uint32_t n = end - start;
+
+  uint8_t* wbuf = smem + static_cast<size_t>(warp) * STAGES * p.stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_offset) + warp * STAGES;
+  const uint32_t q_off = 2 * Gm::kChunk + 2 * Gm::kParam;
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < STAGES; ++i) mbar_init(&bars[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const uint64_t pol = policy_evict_first();
+  const uint32_t Hq = p.H * p.G;
+  const uint32_t stage_tx_kv = 2 * Gm::kChunk + 2 * Gm::kParam;
+
+  // ---- producer (lane 0 issues; all lanes track the cursor) ----
+  // Block-table entries are fetched 32 at a time (lane j holds the entry of
+  // block base+j), double-buffered one window ahead of the issue point.
+  auto load_window = [&](uint32_t base) -> int32_t {
+    int32_t e = 0;
+    if (base + lane < n) {
+      Cursor c;
+      cursor_seek(c, pre, p.batch, p.H, start + base + lane);
+      e = __ldg(p.block_table + static_cast<uint64_t>(c.s) * p.bt_stride + c.b);
+    }
+    return e;
+  };
+  int32_t win0 = load_window(0);
+  int32_t win1 = n > 32 ? load_window(32) : 0;
+  Cursor pc;  // cursor of the next block to issue
+  cursor_seek(pc, pre, p.batch, p.H, start);
+  uint32_t issued = 0;
+
+  auto issue = [&](uint32_t i) {
+    const uint32_t st = i % STAGES;
+    uint8_t* sb = wbuf + st * p.stage_bytes;
+    const bool need_q = (i == 0) || (pc.b == 0);
+    if ((i & 31) == 0 && i > 0 && i + 32 < n) {
+      if ((i >> 5) & 1) win0 = load_window(i + 32);
+      else win1 = load_window(i + 32);
+    }
+    const int32_t ent = __shfl_sync(0xffffffffu, ((i >> 5) & 1) ? win1 : win0, i & 31);
+    if (lane == 0) {
+      const uint64_t boff = block_offset(p.geom, static_cast<uint32_t>(ent)) + p.layer_off;
+      const uint8_t* blk = p.pool + boff;
+      const uint32_t tx = stage_tx_kv + (need_q ? p.G * kD * 2 : 0);
+      mbar_expect_tx(&bars[st], tx);
+      bulk_g2s(sb, blk + static_cast<uint64_t>(pc.h) * Gm::kChunk, Gm::kChunk, &bars[st], pol);
+      bulk_g2s(sb + Gm::kChunk, blk + static_cast<uint64_t>(p.H + pc.h) * Gm::kChunk, Gm::kChunk,
+               &bars[st], pol);
+      if constexpr (Gm::kParam > 0) {
+        const uint8_t* prm = blk + 2ull * p.H * Gm::kChunk;
+        bulk_g2s(sb + 2 * Gm::kChunk, prm + static_cast<uint64_t>(pc.h) * Gm::kParam, Gm::kParam,
+                 &bars[st], pol);
+        bulk_g2s(sb + 2 * Gm::kChunk + Gm::kParam,
+                 prm + static_cast<uint64_t>(p.H + pc.h) * Gm::kParam, Gm::kParam, &bars[st], pol);
+      }
+      if (need_q) {
+        bulk_g2s(sb + q_off, p.q + (static_cast<uint64_t>(pc.s) * Hq + pc.h * p.G) * kD,
+                 p.G * kD * 2, &bars[st], pol);
+      }
+    }
+    cursor_next(pc, pre, p.batch, p.H);
+  };
+  const uint32_t prologue = n < STAGES ? n : STAGES;
+  for (uint32_t i = 0; i < prologue; ++i) issue(i);
+  issued = prologue;
+
+  // ---- consumer state ----
+  Cursor cc;
+  cursor_seek(cc, pre, p.batch, p.H, start);
+  uint32_t qf[NT][8][2];
+  float acc[8][NT][4];
+  float m_run[NT][2], l_run[NT][2], z_run[NT][2], qsum[NT][2];
+  float kscale = 1.f, vscale = 1.f;
+  uint32_t seg_b0 = cc.b;
+  int ctx_cur = 0;
+
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t st = i % STAGES;
+    const uint8_t* sb = wbuf + st * p.stage_bytes;
+    const uint32_t sK = smem_u32(sb), sV = sK + Gm::kChunk;
+    const uint32_t sKp = sK + 2 * Gm::kChunk, sVp = sKp + Gm::kParam;
+    mbar_wait(&bars[st], (i / STAGES) & 1);
+
+    const bool first = (i == 0) || (cc.b == 0);
+    if (first) {
+      seg_b0 = cc.b;
+      ctx_cur = p.ctx_lens[cc.s];
+      // Q rows of this unit -> B fragments (query g of each n-tile, permuted dims)
+      const uint32_t sQ = sK + q_off;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int qrow = nt * 8 + g;
+        float qs = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          uint32_t b0 = 0, b1 = 0;
+          if (qrow < static_cast<int>(p.G)) {
+            const uint32_t rowa = sQ + qrow * kD * 2;
+            const int d0 = kdim<FMT>(kk, t, 0), d1 = kdim<FMT>(kk, t, 1);
+            const int d2 = kdim<FMT>(kk, t, 2), d3 = kdim<FMT>(kk, t, 3);
+            b0 = static_cast<uint32_t>(lds16(rowa + 2 * d0)) |
+                 (static_cast<uint32_t>(lds16(rowa + 2 * d1)) << 16);
+            b1 = static_cast<uint32_t>(lds16(rowa + 2 * d2)) |
+                 (static_cast<uint32_t>(lds16(rowa + 2 * d3)) << 16);
+          }
+          qf[nt][kk][0] = b0;
+          qf[nt][kk][1] = b1;
+          if constexpr (FMT == kINT4) {
+            const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&b0));
+            const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&b1));
+            qs += (f0.x + f0.y) + (f1.x + f1.y);
+          }
+        }
+        if constexpr (FMT == kINT4) {
+          qs += __shfl_xor_sync(0xffffffffu, qs, 1);
+          qs += __shfl_xor_sync(0xffffffffu, qs, 2);
+          // C-fragment columns are queries 2t, 2t+1 of this n-tile
+          qsum[nt][0] = __shfl_sync(0xffffffffu, qs, (2 * t) * 4);
+          qsum[nt][1] = __shfl_sync(0xffffffffu, qs, (2 * t + 1) * 4);
+        }
+        m_run[nt][0] = m_run[nt][1] = -INFINITY;
+        l_run[nt][0] = l_run[nt][1] = 0.f;
+        z_run[nt][0] = z_run[nt][1] = 0.f;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
+      }
+      if constexpr (FMT == kFP8) {
+        if (p.kv_scales) {
+          kscale = p.kv_scales[cc.h];
+          vscale = p.kv_scales[p.H + cc.h];
+        }
+      }
+    }
+
+    // ---- S^T = K . Q^T ----
+    uint32_t ka[8][4];
+    load_k_frags<FMT>(sK, g, t, ka);
+    float sacc[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma16816(sacc[nt], ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
+    }
+
+    // per-token K/V scale (and zero) for tokens g, g+8
+    float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f}, sv[2] = {1.f, 1.f}, zv[2] = {0.f, 0.f};
+    if constexpr (FMT == kINT8) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
+        sv[r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
+      }
+    } else if constexpr (FMT == kINT4) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
+        sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
+        zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
+        sv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
+        zv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
+      }
+    }
+    const int valid = min(kTPB, ctx_cur - static_cast<int>(cc.b) * kTPB);
+
+    uint32_t pb[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float sc[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = e >> 1, tok = g + 8 * r;
+        float x = sacc[nt][e] * sk[r];
+        if constexpr (FMT == kINT4) x += zk[r] * qsum[nt][e & 1];
+        x *= p.sm_scale_log2;
+        sc[e] = tok < valid ? x : -INFINITY;
+      }
+      float mx[2] = {fmaxf(sc[0], sc[2]), fmaxf(sc[1], sc[3])};
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
+        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
+        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
+      }
+      float alpha[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const float mn = fmaxf(m_run[nt][c], mx[c]);
+        alpha[c] = ex2(m_run[nt][c] - mn);
+        m_run[nt][c] = mn;
+      }
+      float pr[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[e] - m_run[nt][e & 1]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        l_run[nt][c] = l_run[nt][c] * alpha[c] + pr[c] + pr[c + 2];
+        if constexpr (FMT == kINT4)
+          z_run[nt][c] = z_run[nt][c] * alpha[c] + pr[c] * zv[0] + pr[c + 2] * zv[1];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        acc[mt][nt][0] *= alpha[0];
+        acc[mt][nt][1] *= alpha[1];
+        acc[mt][nt][2] *= alpha[0];
+        acc[mt][nt][3] *= alpha[1];
+      }
+      // fold V scales into P, pack, and move into B-fragment layout
+      const uint32_t plo = pack_h2(pr[0] * sv[0], pr[1] * sv[0]);
+      const uint32_t phi = pack_h2(pr[2] * sv[1], pr[3] * sv[1]);
+      const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
+      const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
+      const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
+      const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
+      pb[nt][0] = __byte_perm(xa, xb, sel);
+      pb[nt][1] = __byte_perm(ya, yb, sel);
+    }
+
+    // ---- O^T += V^T . P^T ----
+    uint32_t va[8][4];
+    load_v_frags<FMT>(sV, g, t, va);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        mma16816(acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[nt][0], pb[nt][1]);
+
+    // ---- end of a unit segment ----
+    const bool last = (i == n - 1) || (cc.b == cc.nblk - 1);
+    if (last) {
+      const uint32_t unit = cc.s * p.H + cc.h;
+      const bool whole = (seg_b0 == 0) && (cc.b == cc.nblk - 1);
+      float lf[NT][2], zf[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float l = l_run[nt][c], z = z_run[nt][c];
+          l += __shfl_xor_sync(0xffffffffu, l, 4);
+          l += __shfl_xor_sync(0xffffffffu, l, 8);
+          l += __shfl_xor_sync(0xffffffffu, l, 16);
+          if constexpr (FMT == kINT4) {
+            z += __shfl_xor_sync(0xffffffffu, z, 4);
+            z += __shfl_xor_sync(0xffffffffu, z, 8);
+            z += __shfl_xor_sync(0xffffffffu, z, 16);
+          }
+          lf[nt][c] = l;
+          zf[nt][c] = z;
+        }
+      if (whole) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int q = nt * 8 + 2 * t + c;
+            if (q >= static_cast<int>(p.G)) continue;
+            const float inv = 1.f / lf[nt][c];
+            __half* orow = p.out + (static_cast<uint64_t>(cc.s) * Hq + cc.h * p.G + q) * kD;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+              const int d0 = vdim<FMT>(mt, g, 0);
+              const float o0 = (acc[mt][nt][c] * vscale + zf[nt][c]) * inv;
+              const float o1 = (acc[mt][nt][2 + c] * vscale + zf[nt][c]) * inv;
+              *reinterpret_cast<__half2*>(orow + d0) = __floats2half2_rn(o0, o1);
+            }
+            if (p.lse && g == 0)
+              p.lse[static_cast<uint64_t>(cc.s) * Hq + cc.h * p.G + q] =
+                  (m_run[nt][c] + __log2f(lf[nt][c])) * 0.69314718055994531f;
+          }
+      } else {
+        // partial slot: 2*wid (first segment of this warp) or 2*wid+1 (last)
+        const uint32_t slot = 2 * wid + (i + 1 == cc.b - seg_b0 + 1 ? 0 : 1);
+        float* ps = p.partials + static_cast<uint64_t>(slot) * kNQ * (kD + 2);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int q = nt * 8 + 2 * t + c;
+            if (g == 0) {
+              ps[q] = m_run[nt][c];
+              ps[kNQ + q] = lf[nt][c];
+            }
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+              const int d0 = vdim<FMT>(mt, g, 0);
+              float2 v;
+              v.x = acc[mt][nt][c] * vscale + zf[nt][c];
+              v.y = acc[mt][nt][2 + c] * vscale + zf[nt][c];
+              *reinterpret_cast<float2*>(ps + 2 * kNQ + q * kD + d0) = v;
+            }
+          }
+        __threadfence();
+        __syncwarp();
+        uint32_t old = 0;
+        const uint32_t nseg = cc.b - seg_b0 + 1;
+        if (lane == 0) old = atomicAdd(p.counters + unit, nseg);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old + nseg == cc.nblk) {
+          // last contributor: merge every partial of this unit
+          __threadfence();
+          const uint64_t U0 = pre[cc.s] + static_cast<uint64_t>(cc.h) * cc.nblk;
+          const uint64_t U1 = U0 + cc.nblk;
+          const uint32_t wa = static_cast<uint32_t>(((U0 + 1) * W + total - 1) / total - 1);
+          const uint32_t wb = static_cast<uint32_t>((U1 * W + total - 1) / total - 1);
+          for (int q = 0; q < static_cast<int>(p.G); ++q) {
+            float M = -INFINITY;
+            for (uint32_t w = wa; w <= wb; ++w) {
+              const uint32_t ws = static_cast<uint32_t>((static_cast<uint64_t>(w) * total) / W);
+              const uint32_t we = static_cast<uint32_t>((static_cast<uint64_t>(w + 1) * total) / W);
+              if (ws >= we) continue;
+              const uint32_t sl = 2 * w + (ws < U0 ? 1 : 0);
+              M = fmaxf(M, __ldcg(p.partials + static_cast<uint64_t>(sl) * kNQ * (kD + 2) + q));
+            }
+            float L = 0.f;
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (uint32_t w = wa; w <= wb; ++w) {
+              const uint32_t ws = static_cast<uint32_t>((static_cast<uint64_t>(w) * total) / W);
+              const uint32_t we = static_cast<uint32_t>((static_cast<uint64_t>(w + 1) * total) / W);
+              if (ws >= we) continue;
+              const uint32_t sl = 2 * w + (ws < U0 ? 1 : 0);
+              const float* pp = p.partials + static_cast<uint64_t>(sl) * kNQ * (kD + 2);
+              const float f = ex2(__ldcg(pp + q) - M);
+              L += f * __ldcg(pp + kNQ + q);
+              const float4 a4 = __ldcg(reinterpret_cast<const float4*>(pp + 2 * kNQ + q * kD) + lane);
+              o.x += f * a4.x; o.y += f * a4.y; o.z += f * a4.z; o.w += f * a4.w;
+            }
+            const float inv = 1.f / L;
+            __half* orow = p.out + (static_cast<uint64_t>(cc.s) * Hq + cc.h * p.G + q) * kD;
+            *reinterpret_cast<__half2*>(orow + 4 * lane) = __floats2half2_rn(o.x * inv, o.y * inv);
+            *reinterpret_cast<__half2*>(orow + 4 * lane + 2) = __floats2half2_rn(o.z * inv, o.w * inv);
+            if (p.lse && lane == 0)
+              p.lse[static_cast<uint64_t>(cc.s) * Hq + cc.h * p.G + q] = (M + __log2f(L)) * 0.69314718055994531f;
+          }
+          if (lane == 0) p.counters[unit] = 0;
+        }
+      }
+    }
+
+    __syncwarp();
+    if (issued < n) {
+      issue(issued);
+      ++issued;
+    }
+    cursor_next(cc, pre, p.batch, p.H);
+  }
+}
+
+template <int FMT, int NT>
+static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t stream) {
+  constexpr int kStages = 4;
+  using Gm = Geo<FMT>;
+  DecodeParams p = p0;
+  p.stage_bytes = (2 * Gm::kChunk + 2 * Gm::kParam + p.G * kD * 2 + 127) / 128 * 128;
+  const size_t ring = static_cast<size_t>(kDecodeWarps) * kStages * p.stage_bytes;
+  p.bar_offset = static_cast<uint32_t>(ring);
+  p.prefix_offset = p.bar_offset + kDecodeWarps * kStages * 8;
+  const size_t smem = p.prefix_offset + (p.batch + 1) * 4;
+  auto kern = paged_decode_kernel<FMT, NT, kStages>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecodeWarps * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int grid = per_sm * num_sms;
+  if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;
+  kern<<<grid, kDecodeWarps * 32, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace dev
+
+cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms,
+                                cudaStream_t stream) {
+  using namespace dev;
+  const bool two = p.G > 8;
+  switch (kv_dtype) {
+    case kFP16: return two ? launch_fmt<kFP16, 2>(p, num_sms, stream) : launch_fmt<kFP16, 1>(p, num_sms, stream);
+    case kFP8: return two ? launch_fmt<kFP8, 2>(p, num_sms, stream) : launch_fmt<kFP8, 1>(p, num_sms, stream);
+    case kINT8: return two ? launch_fmt<kINT8, 2>(p, num_sms, stream) : launch_fmt<kINT8, 1>(p, num_sms, stream);
+    case kINT4: return two ? launch_fmt<kINT4, 2>(p, num_sms, stream) : launch_fmt<kINT4, 1>(p, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+size_t decode_partials_bytes(int num_sms, int G) {
+  // upper bound of warps in a persistent launch x 2 slots x 16 queries
+  (void)G;
+  const size_t warps = static_cast<size_t>(num_sms) * 64;  // <= 64 warps/SM resident
+  return warps * 2 * 16 * (dev::kD + 2) * sizeof(float);
+}
+
+}  // namespace kvslab

@@ -1,0 +1,78 @@
+// launch.hpp -- kernel parameter blocks and host-side launchers (internal).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "kvslab_geom.hpp"
+
+namespace kvslab {
+
+constexpr int kDecodeWarps = 4;
+
+struct DecodeParams {
+  const uint8_t* pool;
+  dev::SlabGeom geom;
+  uint64_t layer_off;  // layer * layer_bytes
+  uint32_t H, G;       // kv heads, query heads per kv head
+  const __half* q;
+  __half* out;
+  float* lse;
+  const int32_t* block_table;
+  uint32_t bt_stride;
+  const int32_t* ctx_lens;
+  uint32_t batch;
+  float sm_scale_log2;
+  const float* kv_scales;  // FP8 [2][H]
+  float* partials;
+  uint32_t* counters;
+  // filled by the launcher
+  uint32_t stage_bytes, bar_offset, prefix_offset;
+  int max_ctas;  // 0 = persistent full machine
+};
+
+struct AppendParams {
+  uint8_t* pool;
+  dev::SlabGeom geom;
+  uint64_t layer_off;
+  uint32_t H, D, tpb;
+  uint32_t chunk_bytes, params_off;
+  bool fp8_inblock;
+  const __half* k;
+  const __half* v;
+  uint32_t n_tokens;
+  const int32_t* tok_seq;
+  const int32_t* tok_pos;
+  const int32_t* block_table;
+  uint32_t bt_stride;
+  const float* kv_scales;
+};
+
+struct CompactParams {
+  uint8_t* pool;
+  dev::SlabGeom geom;
+  const uint32_t* src_gid;
+  const uint32_t* dst_gid;
+  uint32_t n_moves;
+};
+
+cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms,
+                                cudaStream_t stream);
+size_t decode_partials_bytes(int num_sms, int G);
+cudaError_t launch_kv_append(const AppendParams& p, int kv_dtype, cudaStream_t stream);
+cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream);
+cudaError_t launch_table_scatter(int32_t* table, uint32_t row_stride, const int32_t* triples,
+                                 uint32_t n, cudaStream_t stream);
+cudaError_t launch_table_remap(int32_t* table, uint64_t n_entries, const uint32_t* src_sorted,
+                               const uint32_t* dst_sorted, uint32_t n, cudaStream_t stream);
+cudaError_t launch_table_validate(const int32_t* table, uint32_t row_stride,
+                                  const int32_t* ctx_lens, uint32_t rows, uint32_t tpb,
+                                  const void* slab_table, uint32_t slab_count, uint64_t key,
+                                  dev::FastDiv bps, unsigned long long* n_bad,
+                                  cudaStream_t stream);
+cudaError_t launch_slab_table_scatter(void* table, const void* entries, uint32_t n,
+                                      cudaStream_t stream);
+
+}  // namespace kvslab

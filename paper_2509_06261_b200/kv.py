@@ -1,0 +1,240 @@
+"""Device data path: KV formats, K1 append, K2 paged decode, K3 compaction.
+
+Thin host wrappers over libkvslab.so.  Tensors are torch CUDA tensors (used
+only as device buffers and streams); the arguments cross the C ABI as raw
+pointers.  There is no CPU fallback: every function requires the pool's
+device tensor and calls a CUDA kernel.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib as L
+from .slab_pool import KvSlabError, SlabPool, check
+
+
+class KvDtype(enum.IntEnum):
+    FP16 = 0
+    FP8_E4M3 = 1
+    INT8 = 2
+    INT4 = 3
+
+
+_BITS = {KvDtype.FP16: 16, KvDtype.FP8_E4M3: 8, KvDtype.INT8: 8, KvDtype.INT4: 4}
+
+
+@dataclass(frozen=True)
+class KvFormat:
+    """Per-model KV format (ks_kv_format).  quant_param_bytes_per_block=None
+    selects the format's natural per-layer quant-param size."""
+    kv_dtype: KvDtype
+    num_kv_heads: int
+    num_q_heads: int
+    head_dim: int = 128
+    num_layers: int = 1
+    tokens_per_block: int = 16
+    quant_param_bytes_per_block: Optional[int] = None
+
+    @property
+    def qparams(self) -> int:
+        if self.quant_param_bytes_per_block is not None:
+            return self.quant_param_bytes_per_block
+        H, T = self.num_kv_heads, self.tokens_per_block
+        return {KvDtype.FP16: 0, KvDtype.FP8_E4M3: 2 * H * 4, KvDtype.INT8: 2 * H * T * 2,
+                KvDtype.INT4: 2 * H * T * 4}[KvDtype(self.kv_dtype)]
+
+    @property
+    def bits(self) -> int:
+        return _BITS[KvDtype(self.kv_dtype)]
+
+    @property
+    def token_size(self) -> int:  # per layer, K+V, precision.cpp:76-89
+        return self.num_kv_heads * self.head_dim * 2 * self.bits // 8
+
+    @property
+    def chunk_bytes(self) -> int:
+        return self.tokens_per_block * self.head_dim * self.bits // 8
+
+    @property
+    def layer_bytes(self) -> int:
+        return self.tokens_per_block * self.token_size + self.qparams
+
+    @property
+    def key(self) -> int:  # == kv_block_size(profile), precision.cpp:91-99
+        return self.num_layers * self.layer_bytes
+
+    @property
+    def group(self) -> int:
+        return self.num_q_heads // self.num_kv_heads
+
+    def to_c(self) -> L.ks_kv_format:
+        return L.ks_kv_format(int(self.kv_dtype), self.num_kv_heads, self.num_q_heads,
+                              self.head_dim, self.num_layers, self.tokens_per_block, self.qparams)
+
+    def decode_bytes(self, ctx_lens: Sequence[int]) -> int:
+        """Algorithmic bytes of one K2 launch: every cached K/V
+        byte + quant params + the block-table entries + Q + O, each once."""
+        T = self.tokens_per_block
+        total = 0
+        for c in ctx_lens:
+            nb = (c + T - 1) // T if c > 0 else 0
+            total += c * self.token_size + nb * self.qparams + nb * 4
+        total += 2 * len(ctx_lens) * self.num_q_heads * self.head_dim * 2
+        return total
+
+    def append_bytes(self, n_tokens: int) -> int:
+        """Algorithmic bytes of one K1 launch: fp16 K,V in + quantised bytes out
+        + quant params written + token metadata/table lookups."""
+        H, T = self.num_kv_heads, self.tokens_per_block
+        per_tok_params = {KvDtype.FP16: 0, KvDtype.FP8_E4M3: 0, KvDtype.INT8: 2 * H * 2,
+                          KvDtype.INT4: 2 * H * 4}[KvDtype(self.kv_dtype)]
+        return n_tokens * (2 * H * self.head_dim * 2 + self.token_size + per_tok_params + 12)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class _CAI:
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3}
+
+
+def kv_tensor(pool: SlabPool) -> torch.Tensor:
+    """Zero-copy uint8 view of the pool's single KV tensor."""
+    base, nbytes = C.c_void_p(), C.c_uint64()
+    check(L.lib.ks_device_base(pool.handle, C.byref(base), C.byref(nbytes)))
+    if not base.value:
+        raise KvSlabError("pool has no device tensor")
+    return torch.as_tensor(_CAI(base.value, nbytes.value), device=f"cuda:{pool.device}")
+
+
+def validate_format(pool: SlabPool, fmt: KvFormat) -> None:
+    f = fmt.to_c()
+    check(L.lib.ks_validate_format(pool.handle, C.byref(f)))
+
+
+def slab_table_sync(pool: SlabPool, stream=None) -> None:
+    check(L.lib.ks_slab_table_sync(pool.handle, _stream(stream)))
+
+
+def slab_table_tensor(pool: SlabPool) -> torch.Tensor:
+    """Zero-copy view of the device slab table: int64 [slab_count, 2] where
+    [:,0] = key and [:,1] = blocks_total | state << 32."""
+    t = C.c_void_p()
+    check(L.lib.ks_slab_table_device(pool.handle, C.byref(t)))
+    n = pool.slab_count()
+    raw = torch.as_tensor(_CAI(t.value, n * 16), device=f"cuda:{pool.device}")
+    return raw.view(torch.int64).view(n, 2)
+
+
+def block_table_update(pool: SlabPool, table: torch.Tensor, rows: Sequence[int],
+                       cols: Sequence[int], vals: Sequence[int], stream=None) -> None:
+    """Delta upload of block-table entries (host triples -> device scatter)."""
+    n = len(rows)
+    if n == 0:
+        return
+    r = (C.c_int32 * n)(*rows)
+    c = (C.c_int32 * n)(*cols)
+    v = (C.c_int32 * n)(*vals)
+    check(L.lib.ks_block_table_update(pool.handle, _ptr(table), table.stride(0), r, c, v, n,
+                                      _stream(stream)))
+
+
+def block_table_validate(pool: SlabPool, key: int, table: torch.Tensor, ctx_lens: torch.Tensor,
+                         tokens_per_block: int = 16, stream=None) -> int:
+    bad = C.c_uint64()
+    check(L.lib.ks_block_table_validate(pool.handle, key, _ptr(table), table.stride(0),
+                                        _ptr(ctx_lens), table.shape[0], tokens_per_block,
+                                        _stream(stream), C.byref(bad)))
+    return bad.value
+
+
+def kv_append(pool: SlabPool, fmt: KvFormat, layer: int, k: torch.Tensor, v: torch.Tensor,
+              tok_seq: torch.Tensor, tok_pos: torch.Tensor, block_table: torch.Tensor,
+              kv_scales: Optional[torch.Tensor] = None, stream=None) -> None:
+    """K1: quantise + write n tokens' K/V ([n, Hkv, d] fp16) into their slab blocks."""
+    assert k.dtype == torch.float16 and v.dtype == torch.float16
+    assert k.is_contiguous() and v.is_contiguous() and block_table.dtype == torch.int32
+    f = fmt.to_c()
+    check(L.lib.ks_kv_append(pool.handle, C.byref(f), layer, _ptr(k), _ptr(v), k.shape[0],
+                             _ptr(tok_seq), _ptr(tok_pos), _ptr(block_table),
+                             block_table.stride(0), _ptr(kv_scales), _stream(stream)))
+
+
+class DecodeWorkspace:
+    """Zero-initialised K2 scratch (partials + per-unit counters), reusable."""
+
+    def __init__(self, pool: SlabPool, fmt: KvFormat, max_batch: int):
+        f = fmt.to_c()
+        n = C.c_size_t()
+        check(L.lib.ks_paged_decode_workspace_size(pool.handle, C.byref(f), max_batch,
+                                                   C.byref(n)))
+        self.nbytes = n.value
+        self.max_batch = max_batch
+        self.buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=f"cuda:{pool.device}")
+
+
+_WS: Dict[Tuple[int, int, int], DecodeWorkspace] = {}
+
+
+def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
+                 block_table: torch.Tensor, ctx_lens: torch.Tensor,
+                 out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
+                 sm_scale: Optional[float] = None, kv_scales: Optional[torch.Tensor] = None,
+                 workspace: Optional[DecodeWorkspace] = None, stream=None) -> torch.Tensor:
+    """K2: O = softmax(sm_scale * Q K^T) V over each sequence's slab blocks.
+
+    q: fp16 [B, Hq, d]; block_table: int32 [B, max_blocks] of global block
+    ids; ctx_lens: int32 [B] (device).  Returns out fp16 [B, Hq, d]."""
+    assert q.dtype == torch.float16 and q.is_contiguous()
+    assert block_table.dtype == torch.int32 and ctx_lens.dtype == torch.int32
+    B = q.shape[0]
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        k = (id(pool), fmt.group, B)
+        workspace = _WS.get(k)
+        if workspace is None or workspace.max_batch < B:
+            workspace = _WS[k] = DecodeWorkspace(pool, fmt, B)
+    f = fmt.to_c()
+    check(L.lib.ks_paged_decode(pool.handle, C.byref(f), layer, _ptr(q), _ptr(out), _ptr(lse),
+                                _ptr(block_table), block_table.stride(0), _ptr(ctx_lens), B,
+                                0.0 if sm_scale is None else float(sm_scale), _ptr(kv_scales),
+                                _ptr(workspace.buf), workspace.nbytes, _stream(stream)))
+    return out
+
+
+def compact(pool: SlabPool, key: int, max_moves: int = 1 << 20,
+            tables: Sequence[torch.Tensor] = (), stream=None) -> Tuple[List[Tuple[int, int]], int]:
+    """K3: plan (host, applied to the slab table), move the bytes on the GPU,
+    and remap the given device block tables.  Returns (moves, slabs_freed)."""
+    moves, freed = pool.plan_compaction(key, max_moves)
+    if moves:
+        buf = (L.ks_block_move * len(moves))(*[L.ks_block_move(s, d) for s, d in moves])
+        check(L.lib.ks_compact_apply(pool.handle, key, buf, len(moves), _stream(stream)))
+        for t in tables:
+            check(L.lib.ks_block_table_remap(pool.handle, _ptr(t), t.numel(), buf, len(moves),
+                                             _stream(stream)))
+    return moves, freed
+
+
+def launch_count() -> int:
+    return L.lib.ks_launch_count()
+
+
+def default_sm_scale(head_dim: int) -> float:
+    return 1.0 / math.sqrt(head_dim)

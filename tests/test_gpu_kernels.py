@@ -1,0 +1,265 @@
+"""GPU parity of the device path against the CPU oracle (oracle/kvslab_oracle.c).
+
+K1 append: appended slab bytes bit-exact for FP16/FP8/INT8/INT4.
+K2 decode: outputs within 1e-3 (FP16/FP8) / 1e-2 (INT8/INT4) relative to the
+fp64 oracle, normwise per (sequence, query head): max|o-r| / max|r|.
+K3 compaction: bytes moved and tables remapped; decode unchanged.
+All calls go through libkvslab.so (the C ABI).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2509_06261_b200 as ks
+from paper_2509_06261_b200 import kv
+from paper_2509_06261_b200.kv import KvDtype, KvFormat
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {KvDtype.FP16: 1e-3, KvDtype.FP8_E4M3: 1e-3, KvDtype.INT8: 1e-2, KvDtype.INT4: 1e-2}
+
+
+def make_world(fmt: KvFormat, ctx_lens, slab_blocks=8, extra_keys=(), seed=0, churn=True,
+               fp8_scale=None):
+    """Pool + scattered block tables (allocated after churn) + K/V appended by K1."""
+    rng = np.random.default_rng(seed)
+    key = fmt.key
+    slab = key * slab_blocks
+    for k in extra_keys:
+        slab = slab * k // math.gcd(slab, k)
+    nblk = [(c + 15) // 16 for c in ctx_lens]
+    need = sum(nblk) + 8
+    nslabs = need // max(1, slab // key) + 6 + 2 * len(extra_keys)
+    pool = ks.SlabPool(ks.SlabPoolConfig(nslabs * slab, slab, [key, *extra_keys]), device=0)
+    kv.kv_tensor(pool).zero_()
+    # churn so physical blocks are scattered and interleaved with other keys
+    junk = []
+    if churn:
+        keys = [key, *extra_keys]
+        for _ in range(need):
+            h = pool.try_alloc_block(keys[rng.integers(len(keys))])
+            if h:
+                junk.append(h)
+        for i in rng.permutation(len(junk))[: len(junk) * 2 // 3]:
+            pool.free_block(junk[i])
+    B = len(ctx_lens)
+    maxb = max(1, max(nblk))
+    table = np.zeros((B, maxb), dtype=np.int32)
+    order = [(s, b) for s in range(B) for b in range(nblk[s])]
+    rng.shuffle(order)
+    for s, b in order:
+        table[s, b] = pool.alloc_block(key).global_block_id
+    H, D = fmt.num_kv_heads, fmt.head_dim
+    T = int(sum(ctx_lens))
+    k = rng.standard_normal((T, H, D)).astype(np.float16)
+    v = rng.standard_normal((T, H, D)).astype(np.float16)
+    if fmt.kv_dtype in (KvDtype.INT8, KvDtype.INT4):  # 1% outliers at 8 sigma
+        m = rng.random((T, H, D)) < 0.01
+        k[m] *= 8
+        v[m] *= 8
+    tok_seq = np.concatenate([np.full(c, s, np.int32) for s, c in enumerate(ctx_lens)] or
+                             [np.zeros(0, np.int32)])
+    tok_pos = np.concatenate([np.arange(c, dtype=np.int32) for c in ctx_lens] or
+                             [np.zeros(0, np.int32)])
+    scales = None
+    if fmt.kv_dtype == KvDtype.FP8_E4M3:
+        scales = (np.full(2 * H, 1.0, np.float32) if fp8_scale is None else
+                  np.asarray(fp8_scale, np.float32))
+    return dict(pool=pool, table=table, k=k, v=v, tok_seq=tok_seq, tok_pos=tok_pos,
+                scales=scales, ctx=np.asarray(ctx_lens, np.int32), rng=rng)
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return t if dtype is None else t.to(dtype)
+
+
+def append_gpu(w, fmt, layer):
+    kv.kv_append(w["pool"], fmt, layer, dev(w["k"]), dev(w["v"]), dev(w["tok_seq"]),
+                 dev(w["tok_pos"]), dev(w["table"]),
+                 None if w["scales"] is None else dev(w["scales"]))
+    torch.cuda.synchronize()
+
+
+def oracle_image(w, fmt, layer):
+    pool = w["pool"]
+    img = np.zeros(pool.usable_capacity_bytes(), dtype=np.uint8)
+    f = oracle.fmt(int(fmt.kv_dtype), fmt.num_kv_heads, fmt.num_q_heads, fmt.head_dim,
+                   fmt.num_layers, fmt.tokens_per_block, fmt.qparams)
+    oracle.append(img, pool.slab_size(), pool.blocks_per_slab(fmt.key), f, layer,
+                  w["k"].view(np.uint16), w["v"].view(np.uint16), w["tok_seq"], w["tok_pos"],
+                  w["table"], w["scales"])
+    return img, f
+
+
+FORMATS = [KvDtype.FP16, KvDtype.FP8_E4M3, KvDtype.INT8, KvDtype.INT4]
+
+
+@pytest.mark.parametrize("dt", FORMATS, ids=[d.name for d in FORMATS])
+@pytest.mark.parametrize("layers,layer", [(1, 0), (3, 2)])
+def test_append_bit_exact(dt, layers, layer):
+    fmt = KvFormat(dt, 4, 8, num_layers=layers)
+    w = make_world(fmt, [1, 15, 16, 17, 100, 33], seed=int(dt) * 7 + layer,
+                   fp8_scale=[0.5, 1.0, 2.0, 0.25, 1.5, 3.0, 0.125, 1.0] if dt == KvDtype.FP8_E4M3 else None)
+    append_gpu(w, fmt, layer)
+    img, _ = oracle_image(w, fmt, layer)
+    got = kv.kv_tensor(w["pool"]).cpu().numpy()
+    bad = np.nonzero(got != img)[0]
+    assert bad.size == 0, f"{bad.size} bytes differ, first at {bad[:8]}"
+
+
+def test_fp8_conversion_special_values():
+    """e4m3 saturation/subnormal/tie cases through K1 vs the oracle conversion."""
+    fmt = KvFormat(KvDtype.FP8_E4M3, 1, 1)
+    vals = np.array([0.0, -0.0, 448.0, 449.0, 464.0, 465.0, 1e4, 65504.0, -65504.0,
+                     2.0 ** -6, 2.0 ** -7, 2.0 ** -9, 2.0 ** -10, 1.5 * 2.0 ** -9, 0.001,
+                     240.0, 248.0, 232.0, 1.0625, 1.1875, -3.3, 0.0195],
+                    dtype=np.float32)
+    allh = np.arange(65536, dtype=np.uint16).view(np.float16)
+    allh = allh[np.isfinite(allh)]
+    x = np.concatenate([vals.astype(np.float16), allh])
+    n = (x.size + 127) // 128
+    x = np.concatenate([x, np.zeros(n * 128 - x.size, np.float16)]).reshape(n, 1, 128)
+    w = make_world(fmt, [n], seed=5, churn=False)
+    w["k"], w["v"] = x, x[::-1].copy()
+    append_gpu(w, fmt, 0)
+    img, _ = oracle_image(w, fmt, 0)
+    got = kv.kv_tensor(w["pool"]).cpu().numpy()
+    assert (got == img).all()
+    # the oracle conversion itself against ml_dtypes (independent third party)
+    import ml_dtypes
+    xf = np.float32(allh)
+    want = np.clip(xf, -448, 448).astype(ml_dtypes.float8_e4m3fn).view(np.uint8)
+    mine = np.array([oracle.lib.orc_f32_to_e4m3(float(v)) for v in xf], dtype=np.uint8)
+    assert (mine == want).all()
+
+
+def rel_err(o, r):
+    o = o.reshape(-1, o.shape[-1]).astype(np.float64)
+    r = r.reshape(-1, r.shape[-1])
+    den = np.maximum(np.abs(r).max(axis=1), 1e-30)
+    return (np.abs(o - r).max(axis=1) / den).max()
+
+
+CASES = [
+    # (dtype, Hkv, Hq, ctx lens)
+    (KvDtype.FP16, 32, 32, [1024] * 4),
+    (KvDtype.FP16, 8, 32, [1, 16, 17, 300, 2048, 0, 5]),
+    (KvDtype.FP16, 2, 32, [777, 64]),
+    (KvDtype.FP8_E4M3, 8, 32, [2048, 100, 31, 1]),
+    (KvDtype.FP8_E4M3, 4, 4, [512, 513]),
+    (KvDtype.INT8, 8, 32, [1000, 16, 3]),
+    (KvDtype.INT8, 8, 64, [600]),
+    (KvDtype.INT4, 8, 32, [8192, 17]),
+    (KvDtype.INT4, 8, 8, [1, 2, 3, 4, 50, 129]),
+    (KvDtype.INT4, 4, 40, [333]),
+]
+
+
+@pytest.mark.parametrize("dt,Hkv,Hq,ctx", CASES,
+                         ids=[f"{c[0].name}-{c[1]}x{c[2]}-{len(c[3])}" for c in CASES])
+def test_decode_matches_oracle(dt, Hkv, Hq, ctx):
+    fmt = KvFormat(dt, Hkv, Hq, num_layers=2)
+    sc = None
+    if dt == KvDtype.FP8_E4M3:
+        sc = list(np.linspace(0.25, 2.0, 2 * Hkv))
+    w = make_world(fmt, ctx, seed=len(ctx) + Hq, fp8_scale=sc)
+    append_gpu(w, fmt, 1)
+    img = kv.kv_tensor(w["pool"]).cpu().numpy()
+    q = w["rng"].standard_normal((len(ctx), Hq, 128)).astype(np.float16)
+    lse = torch.empty((len(ctx), Hq), dtype=torch.float32, device="cuda")
+    out = kv.paged_decode(w["pool"], fmt, 1, dev(q), dev(w["table"]), dev(w["ctx"]), lse=lse,
+                          kv_scales=None if w["scales"] is None else dev(w["scales"]))
+    torch.cuda.synchronize()
+    f = oracle.fmt(int(dt), Hkv, Hq, 128, 2, 16, fmt.qparams)
+    ref, ref_lse = oracle.paged_decode(img, w["pool"].slab_size(),
+                                       w["pool"].blocks_per_slab(fmt.key), f, 1, q.view(np.uint16),
+                                       w["table"], w["ctx"], 1 / math.sqrt(128), w["scales"],
+                                       nthreads=oracle.NPROC)
+    o = out.cpu().numpy()
+    live = w["ctx"] > 0
+    err = rel_err(o[live], ref[live])
+    assert err <= TOL[dt], err
+    assert (o[~live] == 0).all()
+    l = lse.cpu().numpy()
+    assert np.abs(l[live] - ref_lse[live]).max() < 1e-3
+    assert np.isneginf(l[~live]).all()
+
+
+@pytest.mark.parametrize("dt", FORMATS, ids=[d.name for d in FORMATS])
+def test_decode_repeatable_and_workspace_clean(dt):
+    """Two launches give identical bits (merge counters reset themselves)."""
+    fmt = KvFormat(dt, 8, 32)
+    w = make_world(fmt, [4096, 3000, 1, 0, 700], seed=3)
+    append_gpu(w, fmt, 0)
+    q = dev(w["rng"].standard_normal((5, 32, 128)).astype(np.float16))
+    sc = None if w["scales"] is None else dev(w["scales"])
+    a = kv.paged_decode(w["pool"], fmt, 0, q, dev(w["table"]), dev(w["ctx"]), kv_scales=sc).clone()
+    b = kv.paged_decode(w["pool"], fmt, 0, q, dev(w["table"]), dev(w["ctx"]), kv_scales=sc)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+def test_compaction_moves_bytes_and_keeps_outputs():
+    fmt = KvFormat(KvDtype.INT4, 8, 32, num_layers=2)
+    other = KvFormat(KvDtype.FP16, 8, 32).key
+    w = make_world(fmt, [700, 300, 1200, 64], seed=9, extra_keys=(other,))
+    pool = w["pool"]
+    append_gpu(w, fmt, 1)
+    table = dev(w["table"])
+    ctx = dev(w["ctx"])
+    q = dev(w["rng"].standard_normal((3, 32, 128)).astype(np.float16))
+    t3, c3 = table[:3].contiguous(), ctx[:3].contiguous()
+    before = kv.paged_decode(pool, fmt, 1, q, t3, c3).clone()
+    # drop sequence 3 to open holes, then compact the key
+    nb3 = (64 + 15) // 16
+    for b in range(nb3):
+        gid = int(w["table"][3, b])
+        s, l = ks.SlabPool.split_global_block_id(gid, pool.blocks_per_slab(fmt.key))
+        pool.free_block(ks.BlockHandle(s, l, gid, fmt.key))
+    st0 = pool.snapshot_stats()
+    moves, freed = kv.compact(pool, fmt.key, tables=[t3])
+    torch.cuda.synchronize()
+    assert len(moves) > 0 and freed > 0
+    assert pool.check_integrity()[0]
+    assert pool.snapshot_stats().allocated_bytes == st0.allocated_bytes
+    after = kv.paged_decode(pool, fmt, 1, q, t3, c3)
+    torch.cuda.synchronize()
+    assert torch.equal(before, after)
+    host = t3.cpu().numpy()
+    srcs = {s_ for s_, _ in moves}
+    for s in range(3):
+        nb = (int(w["ctx"][s]) + 15) // 16
+        assert not (set(host[s, :nb].tolist()) & srcs)
+    kv.slab_table_sync(pool)
+    bad = kv.block_table_validate(pool, fmt.key, t3, c3)
+    assert bad == 0
+
+
+def test_block_table_update_and_validate():
+    fmt = KvFormat(KvDtype.FP16, 8, 8)
+    pool = ks.SlabPool(ks.SlabPoolConfig(16 * fmt.key * 4, fmt.key * 4, [fmt.key]), device=0)
+    from paper_2509_06261_b200.engine import SlabModel
+    m = SlabModel(pool, fmt, max_seqs=4, max_blocks_per_seq=8)
+    assert m.admit(0, 40) and m.admit(1, 16) and m.admit(2, 1)
+    m.cached[0] = 40
+    assert m.ensure_capacity(0, 49)
+    m.sync()
+    torch.cuda.synchronize()
+    host = m.table.cpu().numpy()
+    for s in range(3):
+        for b, h in enumerate(m.handles[s]):
+            assert host[s, b] == h.global_block_id
+    kv.slab_table_sync(pool)
+    ctx = torch.tensor([49, 16, 1, 0], dtype=torch.int32, device="cuda")
+    assert kv.block_table_validate(pool, fmt.key, m.table, ctx) == 0
+    m.release(1)
+    kv.slab_table_sync(pool)
+    assert kv.block_table_validate(pool, fmt.key, m.table, ctx) > 0
+    st = kv.slab_table_tensor(pool).cpu().numpy()
+    for i in range(pool.slab_count()):
+        assert st[i, 0] == pool.slab_key(i)
+        assert (st[i, 1] >> 32) == int(pool.slab_state(i))
