@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -739,6 +740,8 @@ ks_status ks_paged_decode(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer
     p.partials = static_cast<float*>(d_workspace);
     p.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_workspace) + part);
     p.max_ctas = 0;
+    if (const char* dbg = std::getenv("KVSLAB_DECODE_DEBUG")) p.debug = std::atoi(dbg);
+    if (const char* mc = std::getenv("KVSLAB_DECODE_MAX_CTAS")) p.max_ctas = std::atoi(mc);
     cudaError_t e = kvslab::launch_paged_decode(p, static_cast<int>(fmt->kv_dtype), pool->num_sms,
                                                 static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "paged_decode launch");

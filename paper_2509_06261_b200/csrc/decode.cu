@@ -78,26 +78,76 @@ __device__ __forceinline__ void cursor_next(Cursor& c, const uint32_t* pre, uint
 }
 
 // ------------------------------------------------------ fragment loaders
-// K tile as the MMA A operand (rows = tokens g, g+8; k = dims permuted per
-// format, see header).  a[kk][0..3] for k-step kk.
+// Per-thread byte offsets (inside a K or V chunk) of the fragment loads; they
+// only depend on (g, t) so they are computed once per kernel.
+struct FragOff {
+  uint32_t k[4];
+  uint32_t v[4];
+};
+
+// token held in PV k-slot: slot 2t -> ta(t), 2t+1 -> tb(t), +8 for 2t+8/2t+9
 template <int FMT>
-__device__ __forceinline__ void load_k_frags(uint32_t sK, int g, int t, uint32_t (&a)[8][4]) {
+__device__ __forceinline__ int tok_a(int t) {
+  if constexpr (FMT == kFP16) return t;
+  else if constexpr (FMT == kINT4) return (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}
+  else return 2 * t;
+}
+template <int FMT>
+__device__ __forceinline__ int tok_b(int t) {
+  if constexpr (FMT == kFP16) return t + 4;
+  else if constexpr (FMT == kINT4) return 2 + (t & 1) + ((t >> 1) << 2);  // {2,3,6,7}
+  else return 2 * t + 1;
+}
+
+template <int FMT>
+__device__ __forceinline__ FragOff make_offsets(int g, int t) {
+  FragOff o;
+  const int ta = tok_a<FMT>(t), tb = tok_b<FMT>(t);
   if constexpr (FMT == kFP16) {
     const int gt = (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}[t]
 #pragma unroll
+    for (int c = 0; c < 4; ++c) o.k[c] = swz(g * 256 + 16 * (8 * (c >> 1) + gt + 2 * (c & 1)));
+    o.v[0] = swz(ta * 256 + 16 * g);
+    o.v[1] = swz(ta * 256 + 16 * (g + 8));
+    o.v[2] = swz(tb * 256 + 16 * g);
+    o.v[3] = swz(tb * 256 + 16 * (g + 8));
+  } else if constexpr (FMT == kFP8 || FMT == kINT8) {
+    o.k[0] = swz(g * 128 + 16 * (2 * t));
+    o.k[1] = swz(g * 128 + 16 * (2 * t + 1));
+    o.k[2] = o.k[3] = 0;
+    o.v[0] = swz(ta * 128 + 16 * g);
+    o.v[1] = swz(tb * 128 + 16 * g);
+    o.v[2] = o.v[3] = 0;
+  } else {
+    o.k[0] = swz(g * 64 + 16 * t);
+    o.k[1] = swz((g + 8) * 64 + 16 * t);
+    o.k[2] = o.k[3] = 0;
+    o.v[0] = swz(ta * 64 + 8 * g);
+    o.v[1] = swz(tb * 64 + 8 * g);
+    o.v[2] = swz((ta + 8) * 64 + 8 * g);
+    o.v[3] = swz((tb + 8) * 64 + 8 * g);
+  }
+  return o;
+}
+
+// K tile as the MMA A operand (rows = tokens g, g+8; k = dims permuted per
+// format).  a[kk][0..3] for k-step kk.  Row g+8 sits 8 rows further, which is
+// a constant (swizzle-preserving) offset for 256- and 128-byte rows.
+template <int FMT>
+__device__ __forceinline__ void load_k_frags(uint32_t sK, const FragOff& o, uint32_t (&a)[8][4]) {
+  if constexpr (FMT == kFP16) {
+#pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int G = 8 * (c >> 1) + gt + 2 * (c & 1);
-      const uint4 lo = lds128(sK + swz(g * 256 + 16 * G));
-      const uint4 hi = lds128(sK + swz((g + 8) * 256 + 16 * G));
+      const uint4 lo = lds128(sK + o.k[c]);
+      const uint4 hi = lds128(sK + o.k[c] + 2048);
       a[2 * c][0] = lo.x; a[2 * c][1] = hi.x; a[2 * c][2] = lo.y; a[2 * c][3] = hi.y;
       a[2 * c + 1][0] = lo.z; a[2 * c + 1][1] = hi.z; a[2 * c + 1][2] = lo.w; a[2 * c + 1][3] = hi.w;
     }
   } else if constexpr (FMT == kFP8 || FMT == kINT8) {
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const int G = 2 * t + c;
-      const uint4 lo = lds128(sK + swz(g * 128 + 16 * G));
-      const uint4 hi = lds128(sK + swz((g + 8) * 128 + 16 * G));
+      const uint4 lo = lds128(sK + o.k[c]);
+      const uint4 hi = lds128(sK + o.k[c] + 1024);
       const uint32_t wl[4] = {lo.x, lo.y, lo.z, lo.w};
       const uint32_t wh[4] = {hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
@@ -118,8 +168,8 @@ __device__ __forceinline__ void load_k_frags(uint32_t sK, int g, int t, uint32_t
       }
     }
   } else {  // INT4: one granule (32 dims) per row per thread
-    const uint4 lo = lds128(sK + swz(g * 64 + 16 * t));
-    const uint4 hi = lds128(sK + swz((g + 8) * 64 + 16 * t));
+    const uint4 lo = lds128(sK + o.k[0]);
+    const uint4 hi = lds128(sK + o.k[1]);
     const uint32_t wl[4] = {lo.x, lo.y, lo.z, lo.w};
     const uint32_t wh[4] = {hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
@@ -136,50 +186,55 @@ __device__ __forceinline__ void load_k_frags(uint32_t sK, int g, int t, uint32_t
   }
 }
 
-// dims pi(kk, t, j) of the K permutation (used to gather Q into B fragments)
-template <int FMT>
-__device__ __forceinline__ int kdim(int kk, int t, int j) {
-  if constexpr (FMT == kFP16) {
-    const int gt = (t & 1) + ((t >> 1) << 2);
-    const int c = kk >> 1, e = kk & 1;
-    const int G = 8 * (c >> 1) + gt + 2 * (c & 1);
-    return 8 * G + 4 * e + j;
-  } else if constexpr (FMT == kFP8 || FMT == kINT8) {
-    return 32 * t + 4 * kk + j;
-  } else {
-    const int i = kk >> 1, e = kk & 1;
-    const int base = 32 * t + 8 * i + 2 * e;
-    return base + (j == 0 ? 0 : j == 1 ? 4 : j == 2 ? 1 : 5);
+// Q rows of the unit -> MMA B fragments for query g of each n-tile, with the
+// K dims permuted exactly like load_k_frags (the reduction order is free).
+template <int FMT, int NT>
+__device__ __forceinline__ void load_q_frags(uint32_t sQ, int g, int t, uint32_t G,
+                                             uint32_t (&qf)[NT][8][2]) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int qrow = nt * 8 + g;
+    const bool ok = qrow < static_cast<int>(G);
+    const uint32_t row = sQ + qrow * kD * 2;
+    if constexpr (FMT == kFP16) {
+      const int gt = (t & 1) + ((t >> 1) << 2);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int gr = 8 * (c >> 1) + gt + 2 * (c & 1);
+        const uint4 v = ok ? lds128(row + 16 * gr) : make_uint4(0, 0, 0, 0);
+        qf[nt][2 * c][0] = v.x; qf[nt][2 * c][1] = v.y;
+        qf[nt][2 * c + 1][0] = v.z; qf[nt][2 * c + 1][1] = v.w;
+      }
+    } else if constexpr (FMT == kFP8 || FMT == kINT8) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // dims 32t + 8c .. +7 -> k-steps 2c, 2c+1
+        const uint4 v = ok ? lds128(row + 64 * t + 16 * c) : make_uint4(0, 0, 0, 0);
+        qf[nt][2 * c][0] = v.x; qf[nt][2 * c][1] = v.y;
+        qf[nt][2 * c + 1][0] = v.z; qf[nt][2 * c + 1][1] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // dims 32t + 8i .. +7: pairs (0,4),(1,5) | (2,6),(3,7)
+        const uint4 v = ok ? lds128(row + 64 * t + 16 * i) : make_uint4(0, 0, 0, 0);
+        qf[nt][2 * i][0] = __byte_perm(v.x, v.z, 0x5410);
+        qf[nt][2 * i][1] = __byte_perm(v.x, v.z, 0x7632);
+        qf[nt][2 * i + 1][0] = __byte_perm(v.y, v.w, 0x5410);
+        qf[nt][2 * i + 1][1] = __byte_perm(v.y, v.w, 0x7632);
+      }
+    }
   }
 }
 
-// token held in PV k-slot: slot 2t -> ta(t), 2t+1 -> tb(t), +8 for 2t+8/2t+9
-template <int FMT>
-__device__ __forceinline__ int tok_a(int t) {
-  if constexpr (FMT == kFP16) return t;
-  else if constexpr (FMT == kINT4) return (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}
-  else return 2 * t;
-}
-template <int FMT>
-__device__ __forceinline__ int tok_b(int t) {
-  if constexpr (FMT == kFP16) return t + 4;
-  else if constexpr (FMT == kINT4) return 2 + (t & 1) + ((t >> 1) << 2);  // {2,3,6,7}
-  else return 2 * t + 1;
-}
-
 // V tile as the MMA A operand of O^T = V^T P^T (rows = dims, k = tokens).
-// a[mt][0..3] for the 8 m-tiles; dim of (mt, row r8) given by vdim().
 template <int FMT>
-__device__ __forceinline__ void load_v_frags(uint32_t sV, int g, int t, uint32_t (&a)[8][4]) {
-  const int ta = tok_a<FMT>(t), tb = tok_b<FMT>(t);
+__device__ __forceinline__ void load_v_frags(uint32_t sV, const FragOff& o, uint32_t (&a)[8][4]) {
   if constexpr (FMT == kFP16) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int G = g + 8 * h;
-      const uint4 va = lds128(sV + swz(ta * 256 + 16 * G));
-      const uint4 vb = lds128(sV + swz(tb * 256 + 16 * G));
-      const uint4 vc = lds128(sV + swz((ta + 8) * 256 + 16 * G));
-      const uint4 vd = lds128(sV + swz((tb + 8) * 256 + 16 * G));
+      const uint4 va = lds128(sV + o.v[h]);
+      const uint4 vb = lds128(sV + o.v[2 + h]);
+      const uint4 vc = lds128(sV + o.v[h] + 2048);
+      const uint4 vd = lds128(sV + o.v[2 + h] + 2048);
       const uint32_t A[4] = {va.x, va.y, va.z, va.w}, B[4] = {vb.x, vb.y, vb.z, vb.w};
       const uint32_t C[4] = {vc.x, vc.y, vc.z, vc.w}, Dd[4] = {vd.x, vd.y, vd.z, vd.w};
 #pragma unroll
@@ -192,12 +247,12 @@ __device__ __forceinline__ void load_v_frags(uint32_t sV, int g, int t, uint32_t
       }
     }
   } else if constexpr (FMT == kFP8 || FMT == kINT8) {
-    const uint4 va = lds128(sV + swz(ta * 128 + 16 * g));
-    const uint4 vb = lds128(sV + swz(tb * 128 + 16 * g));
-    const uint4 vc = lds128(sV + swz((ta + 8) * 128 + 16 * g));
-    const uint4 vd = lds128(sV + swz((tb + 8) * 128 + 16 * g));
-    uint32_t A[4] = {va.x, va.y, va.z, va.w}, B[4] = {vb.x, vb.y, vb.z, vb.w};
-    uint32_t C[4] = {vc.x, vc.y, vc.z, vc.w}, Dd[4] = {vd.x, vd.y, vd.z, vd.w};
+    const uint4 va = lds128(sV + o.v[0]);
+    const uint4 vb = lds128(sV + o.v[1]);
+    const uint4 vc = lds128(sV + o.v[0] + 1024);
+    const uint4 vd = lds128(sV + o.v[1] + 1024);
+    const uint32_t A[4] = {va.x, va.y, va.z, va.w}, B[4] = {vb.x, vb.y, vb.z, vb.w};
+    const uint32_t C[4] = {vc.x, vc.y, vc.z, vc.w}, Dd[4] = {vd.x, vd.y, vd.z, vd.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
@@ -221,11 +276,10 @@ __device__ __forceinline__ void load_v_frags(uint32_t sV, int g, int t, uint32_t
       }
     }
   } else {  // INT4: 8 bytes (16 dims) per token per thread
-    const uint32_t off = 8 * g;
-    const uint2 va = lds64(sV + swz(ta * 64 + off));
-    const uint2 vb = lds64(sV + swz(tb * 64 + off));
-    const uint2 vc = lds64(sV + swz((ta + 8) * 64 + off));
-    const uint2 vd = lds64(sV + swz((tb + 8) * 64 + off));
+    const uint2 va = lds64(sV + o.v[0]);
+    const uint2 vb = lds64(sV + o.v[1]);
+    const uint2 vc = lds64(sV + o.v[2]);
+    const uint2 vd = lds64(sV + o.v[3]);
     const uint32_t A[2] = {va.x, va.y}, B[2] = {vb.x, vb.y}, C[2] = {vc.x, vc.y},
                    Dd[2] = {vd.x, vd.y};
 #pragma unroll
@@ -250,18 +304,92 @@ __device__ __forceinline__ int vdim(int mt, int g, int r8) {
   else return 16 * g + 2 * mt + r8;
 }
 
+// CTA-wide named barrier for the kDecodeWarps consumer warps (id 1).
+__device__ __forceinline__ void cta_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kDecodeWarps * 32) : "memory");
+}
+
+// First flat index (CTA range start) of CTA c: floor(c * total / C).
+__device__ __forceinline__ uint32_t cta_start(uint32_t c, uint32_t total, uint32_t C) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(c) * total) / C);
+}
+
+// Merge the CTA-level fp32 partials of one unit (run by the CTA that
+// contributes last): O = sum_j 2^(m_j - M) acc_j / sum_j 2^(m_j - M) l_j.
+// Warps split the queries; lanes split segments (max) and then dims, with the
+// segment loads unrolled so every pass is ~one memory round trip.
+template <int NQ>
+__device__ __noinline__ void merge_unit(const DecodeParams& p, const uint32_t* pre, uint32_t C,
+                                        uint32_t total, uint32_t s, uint32_t h, uint32_t nblk,
+                                        int warp, int lane) {
+  constexpr int kSlot = NQ * (kD + 2);
+  const uint64_t U0 = pre[s] + static_cast<uint64_t>(h) * nblk;
+  const uint64_t U1 = U0 + nblk;
+  const uint32_t ca = static_cast<uint32_t>(((U0 + 1) * C + total - 1) / total - 1);
+  const uint32_t cb = static_cast<uint32_t>((U1 * C + total - 1) / total - 1);
+  const uint32_t Hq = p.H * p.G;
+  for (int q = warp; q < static_cast<int>(p.G); q += kDecodeWarps) {
+    // pass 1: lanes over segments -> M (and the segment list)
+    float M = -INFINITY;
+    for (uint32_t c0 = ca; c0 <= cb; c0 += 32) {
+      const uint32_t c = c0 + lane;
+      if (c <= cb) {
+        const uint32_t cs = cta_start(c, total, C), ce = cta_start(c + 1, total, C);
+        if (cs < ce) {
+          const uint32_t sl = 2 * c + (cs < U0 ? 1 : 0);
+          M = fmaxf(M, __ldcg(p.partials + static_cast<uint64_t>(sl) * kSlot + q));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    // pass 2: all lanes over dims (4 each), segments unrolled
+    float L = 0.f;
+    float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (uint32_t c = ca; c <= cb; ++c) {
+      const uint32_t cs = cta_start(c, total, C), ce = cta_start(c + 1, total, C);
+      if (cs >= ce) continue;
+      const uint32_t sl = 2 * c + (cs < U0 ? 1 : 0);
+      const float* pp = p.partials + static_cast<uint64_t>(sl) * kSlot;
+      const float f = ex2(__ldcg(pp + q) - M);
+      L += f * __ldcg(pp + NQ + q);
+      const float4 a4 = __ldcg(reinterpret_cast<const float4*>(pp + 2 * NQ + q * kD) + lane);
+      o4.x += f * a4.x; o4.y += f * a4.y; o4.z += f * a4.z; o4.w += f * a4.w;
+    }
+    const float inv = 1.f / L;
+    __half* orow = p.out + (static_cast<uint64_t>(s) * Hq + h * p.G + q) * kD + 4 * lane;
+    *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(o4.x * inv, o4.y * inv);
+    *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(o4.z * inv, o4.w * inv);
+    if (p.lse && lane == 0)
+      p.lse[static_cast<uint64_t>(s) * Hq + h * p.G + q] = (M + __log2f(L)) * 0.69314718055994531f;
+  }
+}
+
 // ------------------------------------------------------------------ kernel
+// Work split: the flattened (seq, kv-head, block) list is cut into one equal
+// contiguous range per CTA (persistent grid).  Inside a CTA, block i of the
+// range belongs to warp i % 4; each warp streams its own blocks through its
+// private ring and keeps an online-softmax state per unit.  At the end of each
+// unit segment the 4 warp states are combined in shared memory; a unit cut by
+// a CTA-range boundary leaves one fp32 partial per CTA, merged by the CTA
+// that finishes last (per-unit counter, no second launch).
 template <int FMT, int NT, int STAGES>
-__global__ void __launch_bounds__(kDecodeWarps * 32)
+__global__ void __launch_bounds__(kDecodeWarps * 32, NT == 1 ? 3 : 2)
 paged_decode_kernel(const DecodeParams p) {
   using Gm = Geo<FMT>;
+  constexpr int NW = kDecodeWarps;
   constexpr int kNQ = NT * 8;
+  constexpr int kSlot = kNQ * (kD + 2);
+  constexpr float kRescaleSlack = 8.0f;  // log2 units: P <= 2^8 before a rescale
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
 
   // ---- per-CTA prefix of blocks over sequences (x H) ----
   uint32_t* pre = reinterpret_cast<uint32_t*>(smem + p.prefix_offset);
+  __shared__ uint32_t wsum[NW];
+  __shared__ uint32_t s_last;
   {
     const uint32_t nthr = blockDim.x, per = (p.batch + nthr - 1) / nthr;
     const uint32_t b0 = min(p.batch, threadIdx.x * per), b1 = min(p.batch, b0 + per);
@@ -270,7 +398,6 @@ paged_decode_kernel(const DecodeParams p) {
       const int c = p.ctx_lens[s];
       sum += c > 0 ? (static_cast<uint32_t>(c) + kTPB - 1) / kTPB : 0;
     }
-    __shared__ uint32_t wsum[kDecodeWarps];
     uint32_t incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -303,15 +430,15 @@ paged_decode_kernel(const DecodeParams p) {
     }
   }
 
-  const uint32_t W = gridDim.x * kDecodeWarps;
-  const uint32_t wid = blockIdx.x * kDecodeWarps + warp;
-  const uint32_t start = static_cast<uint32_t>((static_cast<uint64_t>(wid) * total) / W);
-  const uint32_t end = static_cast<uint32_t>((static_cast<uint64_t>(wid + 1) * total) / W);
-  if (start >= end) return;
-  const uint32_t n = end - start;
+  const uint32_t C = gridDim.x;
+  const uint32_t cs = cta_start(blockIdx.x, total, C), ce = cta_start(blockIdx.x + 1, total, C);
+  if (cs >= ce) return;  // uniform across the CTA
+  // this warp's blocks: flat cs + warp + NW*k, k < nmine
+  const uint32_t nmine = ce > cs + warp ? (ce - cs - warp + NW - 1) / NW : 0;
 
   uint8_t* wbuf = smem + static_cast<size_t>(warp) * STAGES * p.stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_offset) + warp * STAGES;
+  float* comb = reinterpret_cast<float*>(smem + p.comb_offset);  // [NW][kSlot]
   const uint32_t q_off = 2 * Gm::kChunk + 2 * Gm::kParam;
   if (lane == 0) {
 #pragma unroll
@@ -326,31 +453,34 @@ paged_decode_kernel(const DecodeParams p) {
 
   // ---- producer (lane 0 issues; all lanes track the cursor) ----
   // Block-table entries are fetched 32 at a time (lane j holds the entry of
-  // block base+j), double-buffered one window ahead of the issue point.
+  // this warp's block base+j), double-buffered one window ahead.
   auto load_window = [&](uint32_t base) -> int32_t {
     int32_t e = 0;
-    if (base + lane < n) {
+    if (base + lane < nmine) {
       Cursor c;
-      cursor_seek(c, pre, p.batch, p.H, start + base + lane);
+      cursor_seek(c, pre, p.batch, p.H, cs + warp + NW * (base + lane));
       e = __ldg(p.block_table + static_cast<uint64_t>(c.s) * p.bt_stride + c.b);
     }
     return e;
   };
-  int32_t win0 = load_window(0);
-  int32_t win1 = n > 32 ? load_window(32) : 0;
+  int32_t win0 = nmine ? load_window(0) : 0;
+  int32_t win1 = nmine > 32 ? load_window(32) : 0;
   Cursor pc;  // cursor of the next block to issue
-  cursor_seek(pc, pre, p.batch, p.H, start);
+  if (nmine) cursor_seek(pc, pre, p.batch, p.H, cs + warp);
+  uint32_t prev_unit = 0xffffffffu;
   uint32_t issued = 0;
 
-  auto issue = [&](uint32_t i) {
-    const uint32_t st = i % STAGES;
+  auto issue = [&](uint32_t k) {
+    const uint32_t st = k % STAGES;
     uint8_t* sb = wbuf + st * p.stage_bytes;
-    const bool need_q = (i == 0) || (pc.b == 0);
-    if ((i & 31) == 0 && i > 0 && i + 32 < n) {
-      if ((i >> 5) & 1) win0 = load_window(i + 32);
-      else win1 = load_window(i + 32);
+    const uint32_t unit = pc.s * p.H + pc.h;
+    const bool need_q = unit != prev_unit;
+    prev_unit = unit;
+    if ((k & 31) == 0 && k > 0 && k + 32 < nmine) {
+      if ((k >> 5) & 1) win0 = load_window(k + 32);
+      else win1 = load_window(k + 32);
     }
-    const int32_t ent = __shfl_sync(0xffffffffu, ((i >> 5) & 1) ? win1 : win0, i & 31);
+    const int32_t ent = __shfl_sync(0xffffffffu, ((k >> 5) & 1) ? win1 : win0, k & 31);
     if (lane == 0) {
       const uint64_t boff = block_offset(p.geom, static_cast<uint32_t>(ent)) + p.layer_off;
       const uint8_t* blk = p.pool + boff;
@@ -371,180 +501,192 @@ paged_decode_kernel(const DecodeParams p) {
                  p.G * kD * 2, &bars[st], pol);
       }
     }
-    cursor_next(pc, pre, p.batch, p.H);
+#pragma unroll
+    for (int j = 0; j < NW; ++j) cursor_next(pc, pre, p.batch, p.H);
   };
-  const uint32_t prologue = n < STAGES ? n : STAGES;
-  for (uint32_t i = 0; i < prologue; ++i) issue(i);
+  const uint32_t prologue = nmine < STAGES ? nmine : STAGES;
+  for (uint32_t k = 0; k < prologue; ++k) issue(k);
   issued = prologue;
 
-  // ---- consumer state ----
-  Cursor cc;
-  cursor_seek(cc, pre, p.batch, p.H, start);
+  // ---- consumer ----
+  const FragOff fo = make_offsets<FMT>(g, t);
   uint32_t qf[NT][8][2];
   float acc[8][NT][4];
   float m_run[NT][2], l_run[NT][2], z_run[NT][2], qsum[NT][2];
   float kscale = 1.f, vscale = 1.f;
-  uint32_t seg_b0 = cc.b;
-  int ctx_cur = 0;
+  uint32_t k = 0;  // this warp's consumed blocks
 
-  for (uint32_t i = 0; i < n; ++i) {
-    const uint32_t st = i % STAGES;
-    const uint8_t* sb = wbuf + st * p.stage_bytes;
-    const uint32_t sK = smem_u32(sb), sV = sK + Gm::kChunk;
-    const uint32_t sKp = sK + 2 * Gm::kChunk, sVp = sKp + Gm::kParam;
-    mbar_wait(&bars[st], (i / STAGES) & 1);
-
-    const bool first = (i == 0) || (cc.b == 0);
-    if (first) {
-      seg_b0 = cc.b;
-      ctx_cur = p.ctx_lens[cc.s];
-      // Q rows of this unit -> B fragments (query g of each n-tile, permuted dims)
-      const uint32_t sQ = sK + q_off;
+  Cursor cu;  // CTA-level unit cursor at `flat`
+  cursor_seek(cu, pre, p.batch, p.H, cs);
+  uint32_t flat = cs;
+  while (flat < ce) {
+    const uint32_t ustart = flat - cu.b;           // flat index of the unit's block 0
+    const uint32_t uend = ustart + cu.nblk;
+    const uint32_t segb = min(ce, uend);
+    const uint32_t unit = cu.s * p.H + cu.h;
+    const int ctx_cur = p.ctx_lens[cu.s];
+    // reset the online-softmax state
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int qrow = nt * 8 + g;
-        float qs = 0.f;
+    for (int nt = 0; nt < NT; ++nt) {
+      m_run[nt][0] = m_run[nt][1] = -INFINITY;
+      l_run[nt][0] = l_run[nt][1] = 0.f;
+      z_run[nt][0] = z_run[nt][1] = 0.f;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          uint32_t b0 = 0, b1 = 0;
-          if (qrow < static_cast<int>(p.G)) {
-            const uint32_t rowa = sQ + qrow * kD * 2;
-            const int d0 = kdim<FMT>(kk, t, 0), d1 = kdim<FMT>(kk, t, 1);
-            const int d2 = kdim<FMT>(kk, t, 2), d3 = kdim<FMT>(kk, t, 3);
-            b0 = static_cast<uint32_t>(lds16(rowa + 2 * d0)) |
-                 (static_cast<uint32_t>(lds16(rowa + 2 * d1)) << 16);
-            b1 = static_cast<uint32_t>(lds16(rowa + 2 * d2)) |
-                 (static_cast<uint32_t>(lds16(rowa + 2 * d3)) << 16);
-          }
-          qf[nt][kk][0] = b0;
-          qf[nt][kk][1] = b1;
-          if constexpr (FMT == kINT4) {
-            const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&b0));
-            const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&b1));
-            qs += (f0.x + f0.y) + (f1.x + f1.y);
-          }
-        }
+      for (int mt = 0; mt < 8; ++mt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
+    }
+    if constexpr (FMT == kFP8) {
+      if (p.kv_scales) {
+        kscale = p.kv_scales[cu.h];
+        vscale = p.kv_scales[p.H + cu.h];
+      }
+    }
+    // this warp's first block in [flat, segb)
+    const uint32_t i0 = flat + ((static_cast<uint32_t>(warp) + NW - ((flat - cs) % NW)) % NW);
+    bool first = true;
+    for (uint32_t i = i0; i < segb; i += NW, ++k) {
+      const uint32_t st = k % STAGES;
+      const uint32_t sK = smem_u32(wbuf + st * p.stage_bytes), sV = sK + Gm::kChunk;
+      const uint32_t sKp = sK + 2 * Gm::kChunk, sVp = sKp + Gm::kParam;
+      mbar_wait(&bars[st], (k / STAGES) & 1);
+      if (first) {
+        first = false;
+        load_q_frags<FMT, NT>(sK + q_off, g, t, p.G, qf);
         if constexpr (FMT == kINT4) {
-          qs += __shfl_xor_sync(0xffffffffu, qs, 1);
-          qs += __shfl_xor_sync(0xffffffffu, qs, 2);
-          // C-fragment columns are queries 2t, 2t+1 of this n-tile
-          qsum[nt][0] = __shfl_sync(0xffffffffu, qs, (2 * t) * 4);
-          qsum[nt][1] = __shfl_sync(0xffffffffu, qs, (2 * t + 1) * 4);
-        }
-        m_run[nt][0] = m_run[nt][1] = -INFINITY;
-        l_run[nt][0] = l_run[nt][1] = 0.f;
-        z_run[nt][0] = z_run[nt][1] = 0.f;
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
-      }
-      if constexpr (FMT == kFP8) {
-        if (p.kv_scales) {
-          kscale = p.kv_scales[cc.h];
-          vscale = p.kv_scales[p.H + cc.h];
+          for (int nt = 0; nt < NT; ++nt) {
+            float qs = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][0]));
+              const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][1]));
+              qs += (f0.x + f0.y) + (f1.x + f1.y);
+            }
+            qs += __shfl_xor_sync(0xffffffffu, qs, 1);
+            qs += __shfl_xor_sync(0xffffffffu, qs, 2);
+            qsum[nt][0] = __shfl_sync(0xffffffffu, qs, (2 * t) * 4);
+            qsum[nt][1] = __shfl_sync(0xffffffffu, qs, (2 * t + 1) * 4);
+          }
         }
       }
+      if (!(p.debug & 1)) {
+        // ---- S^T = K . Q^T (two accumulators halve the dependent MMA chain) ----
+        uint32_t ka[8][4];
+        load_k_frags<FMT>(sK, fo, ka);
+        float sacc[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          float s2[4] = {0.f, 0.f, 0.f, 0.f};
+          sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+          for (int kk = 0; kk < 8; kk += 2) {
+            mma16816(sacc[nt], ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
+            mma16816(s2, ka[kk + 1][0], ka[kk + 1][1], ka[kk + 1][2], ka[kk + 1][3],
+                     qf[nt][kk + 1][0], qf[nt][kk + 1][1]);
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sacc[nt][e] += s2[e];
+        }
+        uint32_t va[8][4];
+        load_v_frags<FMT>(sV, fo, va);
+
+        float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f}, sv[2] = {1.f, 1.f}, zv[2] = {0.f, 0.f};
+        if constexpr (FMT == kINT8) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
+            sv[r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
+          }
+        } else if constexpr (FMT == kINT4) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
+            sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
+            zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
+            sv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
+            zv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
+          }
+        }
+        const int bb = static_cast<int>(i - ustart);
+        const int valid = min(kTPB, ctx_cur - bb * kTPB);
+
+        uint32_t pb[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          float sc[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = e >> 1, tok = g + 8 * r;
+            float x = sacc[nt][e] * sk[r];
+            if constexpr (FMT == kINT4) x += zk[r] * qsum[nt][e & 1];
+            x *= p.sm_scale_log2;
+            sc[e] = tok < valid ? x : -INFINITY;
+          }
+          float mx[2] = {fmaxf(sc[0], sc[2]), fmaxf(sc[1], sc[3])};
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
+            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
+            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
+          }
+          // Lazy rescaling: keep the reference max until a score exceeds it by
+          // kRescaleSlack (P stays <= 2^8), so the accumulator rescale runs
+          // only when the running max really moves.
+          const bool grow = (mx[0] > m_run[nt][0] + kRescaleSlack) ||
+                            (mx[1] > m_run[nt][1] + kRescaleSlack);
+          if (__any_sync(0xffffffffu, grow)) {
+            float alpha[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const float mn = fmaxf(m_run[nt][c], mx[c]);
+              alpha[c] = ex2(m_run[nt][c] - mn);
+              m_run[nt][c] = mn;
+              l_run[nt][c] *= alpha[c];
+              z_run[nt][c] *= alpha[c];
+            }
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+              acc[mt][nt][0] *= alpha[0];
+              acc[mt][nt][1] *= alpha[1];
+              acc[mt][nt][2] *= alpha[0];
+              acc[mt][nt][3] *= alpha[1];
+            }
+          }
+          float pr[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[e] - m_run[nt][e & 1]);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            l_run[nt][c] += pr[c] + pr[c + 2];
+            if constexpr (FMT == kINT4) z_run[nt][c] += pr[c] * zv[0] + pr[c + 2] * zv[1];
+          }
+          const uint32_t plo = pack_h2(pr[0] * sv[0], pr[1] * sv[0]);
+          const uint32_t phi = pack_h2(pr[2] * sv[1], pr[3] * sv[1]);
+          const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
+          const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
+          const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
+          const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
+          pb[nt][0] = __byte_perm(xa, xb, sel);
+          pb[nt][1] = __byte_perm(ya, yb, sel);
+        }
+
+        // ---- O^T += V^T . P^T ----
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            mma16816(acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[nt][0], pb[nt][1]);
+      }
+      // the stage is consumed: refill it
+      __syncwarp();
+      if (issued < nmine) {
+        issue(issued);
+        ++issued;
+      }
     }
 
-    // ---- S^T = K . Q^T ----
-    uint32_t ka[8][4];
-    load_k_frags<FMT>(sK, g, t, ka);
-    float sacc[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        mma16816(sacc[nt], ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
-    }
-
-    // per-token K/V scale (and zero) for tokens g, g+8
-    float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f}, sv[2] = {1.f, 1.f}, zv[2] = {0.f, 0.f};
-    if constexpr (FMT == kINT8) {
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
-        sv[r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
-      }
-    } else if constexpr (FMT == kINT4) {
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
-        sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
-        zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
-        sv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
-        zv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
-      }
-    }
-    const int valid = min(kTPB, ctx_cur - static_cast<int>(cc.b) * kTPB);
-
-    uint32_t pb[NT][2];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      float sc[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = e >> 1, tok = g + 8 * r;
-        float x = sacc[nt][e] * sk[r];
-        if constexpr (FMT == kINT4) x += zk[r] * qsum[nt][e & 1];
-        x *= p.sm_scale_log2;
-        sc[e] = tok < valid ? x : -INFINITY;
-      }
-      float mx[2] = {fmaxf(sc[0], sc[2]), fmaxf(sc[1], sc[3])};
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
-        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
-        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
-      }
-      float alpha[2];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const float mn = fmaxf(m_run[nt][c], mx[c]);
-        alpha[c] = ex2(m_run[nt][c] - mn);
-        m_run[nt][c] = mn;
-      }
-      float pr[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[e] - m_run[nt][e & 1]);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        l_run[nt][c] = l_run[nt][c] * alpha[c] + pr[c] + pr[c + 2];
-        if constexpr (FMT == kINT4)
-          z_run[nt][c] = z_run[nt][c] * alpha[c] + pr[c] * zv[0] + pr[c + 2] * zv[1];
-      }
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        acc[mt][nt][0] *= alpha[0];
-        acc[mt][nt][1] *= alpha[1];
-        acc[mt][nt][2] *= alpha[0];
-        acc[mt][nt][3] *= alpha[1];
-      }
-      // fold V scales into P, pack, and move into B-fragment layout
-      const uint32_t plo = pack_h2(pr[0] * sv[0], pr[1] * sv[0]);
-      const uint32_t phi = pack_h2(pr[2] * sv[1], pr[3] * sv[1]);
-      const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
-      const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
-      const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
-      const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
-      pb[nt][0] = __byte_perm(xa, xb, sel);
-      pb[nt][1] = __byte_perm(ya, yb, sel);
-    }
-
-    // ---- O^T += V^T . P^T ----
-    uint32_t va[8][4];
-    load_v_frags<FMT>(sV, g, t, va);
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        mma16816(acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[nt][0], pb[nt][1]);
-
-    // ---- end of a unit segment ----
-    const bool last = (i == n - 1) || (cc.b == cc.nblk - 1);
-    if (last) {
-      const uint32_t unit = cc.s * p.H + cc.h;
-      const bool whole = (seg_b0 == 0) && (cc.b == cc.nblk - 1);
-      float lf[NT][2], zf[NT][2];
+    // ---- combine the 4 warp states of this unit segment in shared memory ----
+    {
+      float* my = comb + warp * kSlot;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -558,118 +700,89 @@ paged_decode_kernel(const DecodeParams p) {
             z += __shfl_xor_sync(0xffffffffu, z, 8);
             z += __shfl_xor_sync(0xffffffffu, z, 16);
           }
-          lf[nt][c] = l;
-          zf[nt][c] = z;
+          const int q = nt * 8 + 2 * t + c;
+          if (g == 0) {
+            my[q] = m_run[nt][c];
+            my[kNQ + q] = l;
+          }
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            const int d0 = vdim<FMT>(mt, g, 0);
+            float2 v;
+            v.x = acc[mt][nt][c] * vscale + z;
+            v.y = acc[mt][nt][2 + c] * vscale + z;
+            *reinterpret_cast<float2*>(my + 2 * kNQ + q * kD + d0) = v;
+          }
         }
+    }
+    cta_bar();
+    const bool whole = (flat == ustart) && (segb == uend);
+    // seg slot in global partials: 2*cta (first segment of the CTA) or 2*cta+1
+    float* ps = p.partials + static_cast<uint64_t>(2 * blockIdx.x + (flat == cs ? 0 : 1)) * kSlot;
+    for (int q = warp; q < static_cast<int>(p.G); q += NW) {
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) M = fmaxf(M, comb[w * kSlot + q]);
+      float L = 0.f;
+      float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const float* sw = comb + w * kSlot;
+        const float f = sw[q] == -INFINITY ? 0.f : ex2(sw[q] - M);
+        L += f * sw[kNQ + q];
+        const float4 a4 = reinterpret_cast<const float4*>(sw + 2 * kNQ + q * kD)[lane];
+        o4.x += f * a4.x; o4.y += f * a4.y; o4.z += f * a4.z; o4.w += f * a4.w;
+      }
       if (whole) {
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int q = nt * 8 + 2 * t + c;
-            if (q >= static_cast<int>(p.G)) continue;
-            const float inv = 1.f / lf[nt][c];
-            __half* orow = p.out + (static_cast<uint64_t>(cc.s) * Hq + cc.h * p.G + q) * kD;
-#pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-              const int d0 = vdim<FMT>(mt, g, 0);
-              const float o0 = (acc[mt][nt][c] * vscale + zf[nt][c]) * inv;
-              const float o1 = (acc[mt][nt][2 + c] * vscale + zf[nt][c]) * inv;
-              *reinterpret_cast<__half2*>(orow + d0) = __floats2half2_rn(o0, o1);
-            }
-            if (p.lse && g == 0)
-              p.lse[static_cast<uint64_t>(cc.s) * Hq + cc.h * p.G + q] =
-                  (m_run[nt][c] + __log2f(lf[nt][c])) * 0.69314718055994531f;
-          }
+        const float inv = 1.f / L;
+        __half* orow = p.out + (static_cast<uint64_t>(cu.s) * Hq + cu.h * p.G + q) * kD + 4 * lane;
+        *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(o4.x * inv, o4.y * inv);
+        *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(o4.z * inv, o4.w * inv);
+        if (p.lse && lane == 0)
+          p.lse[static_cast<uint64_t>(cu.s) * Hq + cu.h * p.G + q] =
+              (M + __log2f(L)) * 0.69314718055994531f;
       } else {
-        // partial slot: 2*wid (first segment of this warp) or 2*wid+1 (last)
-        const uint32_t slot = 2 * wid + (i + 1 == cc.b - seg_b0 + 1 ? 0 : 1);
-        float* ps = p.partials + static_cast<uint64_t>(slot) * kNQ * (kD + 2);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int q = nt * 8 + 2 * t + c;
-            if (g == 0) {
-              ps[q] = m_run[nt][c];
-              ps[kNQ + q] = lf[nt][c];
-            }
-#pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-              const int d0 = vdim<FMT>(mt, g, 0);
-              float2 v;
-              v.x = acc[mt][nt][c] * vscale + zf[nt][c];
-              v.y = acc[mt][nt][2 + c] * vscale + zf[nt][c];
-              *reinterpret_cast<float2*>(ps + 2 * kNQ + q * kD + d0) = v;
-            }
-          }
-        __threadfence();
-        __syncwarp();
-        uint32_t old = 0;
-        const uint32_t nseg = cc.b - seg_b0 + 1;
-        if (lane == 0) old = atomicAdd(p.counters + unit, nseg);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        if (old + nseg == cc.nblk) {
-          // last contributor: merge every partial of this unit
-          __threadfence();
-          const uint64_t U0 = pre[cc.s] + static_cast<uint64_t>(cc.h) * cc.nblk;
-          const uint64_t U1 = U0 + cc.nblk;
-          const uint32_t wa = static_cast<uint32_t>(((U0 + 1) * W + total - 1) / total - 1);
-          const uint32_t wb = static_cast<uint32_t>((U1 * W + total - 1) / total - 1);
-          for (int q = 0; q < static_cast<int>(p.G); ++q) {
-            float M = -INFINITY;
-            for (uint32_t w = wa; w <= wb; ++w) {
-              const uint32_t ws = static_cast<uint32_t>((static_cast<uint64_t>(w) * total) / W);
-              const uint32_t we = static_cast<uint32_t>((static_cast<uint64_t>(w + 1) * total) / W);
-              if (ws >= we) continue;
-              const uint32_t sl = 2 * w + (ws < U0 ? 1 : 0);
-              M = fmaxf(M, __ldcg(p.partials + static_cast<uint64_t>(sl) * kNQ * (kD + 2) + q));
-            }
-            float L = 0.f;
-            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (uint32_t w = wa; w <= wb; ++w) {
-              const uint32_t ws = static_cast<uint32_t>((static_cast<uint64_t>(w) * total) / W);
-              const uint32_t we = static_cast<uint32_t>((static_cast<uint64_t>(w + 1) * total) / W);
-              if (ws >= we) continue;
-              const uint32_t sl = 2 * w + (ws < U0 ? 1 : 0);
-              const float* pp = p.partials + static_cast<uint64_t>(sl) * kNQ * (kD + 2);
-              const float f = ex2(__ldcg(pp + q) - M);
-              L += f * __ldcg(pp + kNQ + q);
-              const float4 a4 = __ldcg(reinterpret_cast<const float4*>(pp + 2 * kNQ + q * kD) + lane);
-              o.x += f * a4.x; o.y += f * a4.y; o.z += f * a4.z; o.w += f * a4.w;
-            }
-            const float inv = 1.f / L;
-            __half* orow = p.out + (static_cast<uint64_t>(cc.s) * Hq + cc.h * p.G + q) * kD;
-            *reinterpret_cast<__half2*>(orow + 4 * lane) = __floats2half2_rn(o.x * inv, o.y * inv);
-            *reinterpret_cast<__half2*>(orow + 4 * lane + 2) = __floats2half2_rn(o.z * inv, o.w * inv);
-            if (p.lse && lane == 0)
-              p.lse[static_cast<uint64_t>(cc.s) * Hq + cc.h * p.G + q] = (M + __log2f(L)) * 0.69314718055994531f;
-          }
-          if (lane == 0) p.counters[unit] = 0;
+        if (lane == 0) {
+          ps[q] = M;
+          ps[kNQ + q] = L;
         }
+        reinterpret_cast<float4*>(ps + 2 * kNQ + q * kD)[lane] = o4;
       }
     }
-
-    __syncwarp();
-    if (issued < n) {
-      issue(issued);
-      ++issued;
+    if (!whole) {
+      __threadfence();
+      cta_bar();
+      if (threadIdx.x == 0) {
+        const uint32_t nseg = segb - flat;
+        const uint32_t old = atomicAdd(p.counters + unit, nseg);
+        const uint32_t last = (old + nseg == cu.nblk) ? 1u : 0u;
+        if (last) p.counters[unit] = 0;
+        s_last = last;
+      }
+      cta_bar();
+      if (s_last && !(p.debug & 2)) {
+        __threadfence();
+        merge_unit<kNQ>(p, pre, C, total, cu.s, cu.h, cu.nblk, warp, lane);
+      }
     }
-    cursor_next(cc, pre, p.batch, p.H);
+    cta_bar();  // comb / s_last reusable
+    // advance to the next unit
+    flat = segb;
+    if (flat < ce) cursor_seek(cu, pre, p.batch, p.H, flat);
   }
 }
 
-template <int FMT, int NT>
+template <int FMT, int NT, int STAGES>
 static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t stream) {
-  constexpr int kStages = 4;
   using Gm = Geo<FMT>;
   DecodeParams p = p0;
   p.stage_bytes = (2 * Gm::kChunk + 2 * Gm::kParam + p.G * kD * 2 + 127) / 128 * 128;
-  const size_t ring = static_cast<size_t>(kDecodeWarps) * kStages * p.stage_bytes;
+  const size_t ring = static_cast<size_t>(kDecodeWarps) * STAGES * p.stage_bytes;
   p.bar_offset = static_cast<uint32_t>(ring);
-  p.prefix_offset = p.bar_offset + kDecodeWarps * kStages * 8;
+  p.comb_offset = (p.bar_offset + kDecodeWarps * STAGES * 8 + 15) / 16 * 16;
+  p.prefix_offset = p.comb_offset + kDecodeWarps * NT * 8 * (kD + 2) * 4;
   const size_t smem = p.prefix_offset + (p.batch + 1) * 4;
-  auto kern = paged_decode_kernel<FMT, NT, kStages>;
+  auto kern = paged_decode_kernel<FMT, NT, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -681,6 +794,15 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;
   kern<<<grid, kDecodeWarps * 32, smem, stream>>>(p);
   return cudaGetLastError();
+}
+
+// Ring depth per format: enough bytes in flight per SM (~100-200 KB) while
+// leaving room for 3 CTAs (12 warps) per SM.
+template <int FMT, int NT>
+static cudaError_t launch_fmt(const DecodeParams& p, int num_sms, cudaStream_t stream) {
+  if constexpr (FMT == kFP16) return launch_fmt<FMT, NT, 2>(p, num_sms, stream);
+  else if constexpr (FMT == kINT4) return launch_fmt<FMT, NT, 4>(p, num_sms, stream);
+  else return launch_fmt<FMT, NT, 3>(p, num_sms, stream);
 }
 
 }  // namespace dev
@@ -699,10 +821,10 @@ cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms
 }
 
 size_t decode_partials_bytes(int num_sms, int G) {
-  // upper bound of warps in a persistent launch x 2 slots x 16 queries
+  // upper bound of CTAs in a persistent launch x 2 slots x 16 queries
   (void)G;
-  const size_t warps = static_cast<size_t>(num_sms) * 64;  // <= 64 warps/SM resident
-  return warps * 2 * 16 * (dev::kD + 2) * sizeof(float);
+  const size_t ctas = static_cast<size_t>(num_sms) * 16;
+  return ctas * 2 * 16 * (dev::kD + 2) * sizeof(float);
 }
 
 }  // namespace kvslab

@@ -29,8 +29,9 @@ struct DecodeParams {
   float* partials;
   uint32_t* counters;
   // filled by the launcher
-  uint32_t stage_bytes, bar_offset, prefix_offset;
+  uint32_t stage_bytes, bar_offset, comb_offset, prefix_offset;
   int max_ctas;  // 0 = persistent full machine
+  int debug;     // bit0: skip math, bit1: skip partial merge (probes only)
 };
 
 struct AppendParams {

@@ -32,7 +32,7 @@ def make_world(fmt: KvFormat, ctx_lens, slab_blocks=8, extra_keys=(), seed=0, ch
         slab = slab * k // math.gcd(slab, k)
     nblk = [(c + 15) // 16 for c in ctx_lens]
     need = sum(nblk) + 8
-    nslabs = need // max(1, slab // key) + 6 + 2 * len(extra_keys)
+    nslabs = 2 * (need // max(1, slab // key)) + 8 + 4 * len(extra_keys)
     pool = ks.SlabPool(ks.SlabPoolConfig(nslabs * slab, slab, [key, *extra_keys]), device=0)
     kv.kv_tensor(pool).zero_()
     # churn so physical blocks are scattered and interleaved with other keys
@@ -113,7 +113,7 @@ def test_append_bit_exact(dt, layers, layer):
 
 def test_fp8_conversion_special_values():
     """e4m3 saturation/subnormal/tie cases through K1 vs the oracle conversion."""
-    fmt = KvFormat(KvDtype.FP8_E4M3, 1, 1)
+    fmt = KvFormat(KvDtype.FP8_E4M3, 1, 1, quant_param_bytes_per_block=0)
     vals = np.array([0.0, -0.0, 448.0, 449.0, 464.0, 465.0, 1e4, 65504.0, -65504.0,
                      2.0 ** -6, 2.0 ** -7, 2.0 ** -9, 2.0 ** -10, 1.5 * 2.0 ** -9, 0.001,
                      240.0, 248.0, 232.0, 1.0625, 1.1875, -3.3, 0.0195],
@@ -206,7 +206,7 @@ def test_decode_repeatable_and_workspace_clean(dt):
 def test_compaction_moves_bytes_and_keeps_outputs():
     fmt = KvFormat(KvDtype.INT4, 8, 32, num_layers=2)
     other = KvFormat(KvDtype.FP16, 8, 32).key
-    w = make_world(fmt, [700, 300, 1200, 64], seed=9, extra_keys=(other,))
+    w = make_world(fmt, [700, 300, 64, 1200], seed=9, extra_keys=(other,))
     pool = w["pool"]
     append_gpu(w, fmt, 1)
     table = dev(w["table"])
@@ -214,11 +214,11 @@ def test_compaction_moves_bytes_and_keeps_outputs():
     q = dev(w["rng"].standard_normal((3, 32, 128)).astype(np.float16))
     t3, c3 = table[:3].contiguous(), ctx[:3].contiguous()
     before = kv.paged_decode(pool, fmt, 1, q, t3, c3).clone()
-    # drop sequence 3 to open holes, then compact the key
-    nb3 = (64 + 15) // 16
-    for b in range(nb3):
+    # drop the longest sequence to open holes in many slabs, then compact
+    bps = pool.blocks_per_slab(fmt.key)
+    for b in range((1200 + 15) // 16):
         gid = int(w["table"][3, b])
-        s, l = ks.SlabPool.split_global_block_id(gid, pool.blocks_per_slab(fmt.key))
+        s, l = ks.SlabPool.split_global_block_id(gid, bps)
         pool.free_block(ks.BlockHandle(s, l, gid, fmt.key))
     st0 = pool.snapshot_stats()
     moves, freed = kv.compact(pool, fmt.key, tables=[t3])
@@ -226,6 +226,7 @@ def test_compaction_moves_bytes_and_keeps_outputs():
     assert len(moves) > 0 and freed > 0
     assert pool.check_integrity()[0]
     assert pool.snapshot_stats().allocated_bytes == st0.allocated_bytes
+    assert pool.snapshot_stats().free_slab_bytes > st0.free_slab_bytes
     after = kv.paged_decode(pool, fmt, 1, q, t3, c3)
     torch.cuda.synchronize()
     assert torch.equal(before, after)
@@ -235,8 +236,7 @@ def test_compaction_moves_bytes_and_keeps_outputs():
         nb = (int(w["ctx"][s]) + 15) // 16
         assert not (set(host[s, :nb].tolist()) & srcs)
     kv.slab_table_sync(pool)
-    bad = kv.block_table_validate(pool, fmt.key, t3, c3)
-    assert bad == 0
+    assert kv.block_table_validate(pool, fmt.key, t3, c3) == 0
 
 
 def test_block_table_update_and_validate():
@@ -256,7 +256,8 @@ def test_block_table_update_and_validate():
     kv.slab_table_sync(pool)
     ctx = torch.tensor([49, 16, 1, 0], dtype=torch.int32, device="cuda")
     assert kv.block_table_validate(pool, fmt.key, m.table, ctx) == 0
-    m.release(1)
+    for s in range(3):  # all blocks freed -> every slab returns FREE
+        m.release(s)
     kv.slab_table_sync(pool)
     assert kv.block_table_validate(pool, fmt.key, m.table, ctx) > 0
     st = kv.slab_table_tensor(pool).cpu().numpy()
