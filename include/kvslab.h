@@ -246,6 +246,20 @@ ks_status ks_paged_decode(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer
                           float sm_scale, const float* d_kv_scales, void* d_workspace,
                           size_t workspace_bytes, void* stream);
 
+/* K1+K2 fused, the decode-step form: first appends the new token of every
+ * sequence (d_k_new, d_v_new: fp16 [batch][Hkv][d], the token at position
+ * d_ctx_lens[s]-1, whose block must already be in the table), then attends
+ * over all d_ctx_lens[s] tokens.  The warp that owns a sequence-head's last
+ * block writes the token before its bulk copy reads the block, so there is no
+ * separate K1 launch and no inter-kernel dependency.  Bytes written are
+ * identical to ks_kv_append. */
+ks_status ks_paged_decode_append(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer,
+                                 const void* d_q, const void* d_k_new, const void* d_v_new,
+                                 void* d_out, float* d_lse, const int32_t* d_block_table,
+                                 uint32_t bt_stride, const int32_t* d_ctx_lens, uint32_t batch,
+                                 float sm_scale, const float* d_kv_scales, void* d_workspace,
+                                 size_t workspace_bytes, void* stream);
+
 /* K3 -- slab compaction for one key (new; the reference never migrates,
  * SPEC.md:223).  plan: host-side, deterministic; it
  * moves blocks out of the least-occupied PARTIAL slabs of `key` so they

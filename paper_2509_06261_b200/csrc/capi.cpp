@@ -700,8 +700,8 @@ ks_status ks_paged_decode_workspace_size(const ks_pool* pool, const ks_kv_format
   return KS_OK;
 }
 
-ks_status ks_paged_decode(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
-                          void* d_out, float* d_lse, const int32_t* d_block_table,
+static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
+                             const void* d_k_new, const void* d_v_new, void* d_out, float* d_lse, const int32_t* d_block_table,
                           uint32_t bt_stride, const int32_t* d_ctx_lens, uint32_t batch,
                           float sm_scale, const float* d_kv_scales, void* d_workspace,
                           size_t workspace_bytes, void* stream) {
@@ -736,6 +736,12 @@ ks_status ks_paged_decode(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer
     const float scale = sm_scale > 0.f ? sm_scale : 1.0f / std::sqrt(static_cast<float>(fmt->head_dim));
     p.sm_scale_log2 = scale * 1.4426950408889634f;
     p.kv_scales = fmt->kv_dtype == KS_KV_FP8_E4M3 ? d_kv_scales : nullptr;
+    p.k_new = static_cast<const __half*>(d_k_new);
+    p.v_new = static_cast<const __half*>(d_v_new);
+    p.params_off = static_cast<uint32_t>(2 * p.H * fi.chunk);
+    p.fp8_inblock = fmt->kv_dtype == KS_KV_FP8_E4M3 && fmt->quant_param_bytes_per_block > 0;
+    if ((d_k_new == nullptr) != (d_v_new == nullptr))
+      return fail(KS_INVALID_ARGUMENT, "k_new and v_new must both be set or both be null");
     const size_t part = kvslab::decode_partials_bytes(pool->num_sms, static_cast<int>(p.G));
     p.partials = static_cast<float*>(d_workspace);
     p.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_workspace) + part);
@@ -748,6 +754,28 @@ ks_status ks_paged_decode(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer
     ++g_launches;
     return KS_OK;
   });
+}
+
+ks_status ks_paged_decode(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
+                          void* d_out, float* d_lse, const int32_t* d_block_table,
+                          uint32_t bt_stride, const int32_t* d_ctx_lens, uint32_t batch,
+                          float sm_scale, const float* d_kv_scales, void* d_workspace,
+                          size_t workspace_bytes, void* stream) {
+  return decode_impl(pool, fmt, layer, d_q, nullptr, nullptr, d_out, d_lse, d_block_table,
+                     bt_stride, d_ctx_lens, batch, sm_scale, d_kv_scales, d_workspace,
+                     workspace_bytes, stream);
+}
+
+ks_status ks_paged_decode_append(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer,
+                                 const void* d_q, const void* d_k_new, const void* d_v_new,
+                                 void* d_out, float* d_lse, const int32_t* d_block_table,
+                                 uint32_t bt_stride, const int32_t* d_ctx_lens, uint32_t batch,
+                                 float sm_scale, const float* d_kv_scales, void* d_workspace,
+                                 size_t workspace_bytes, void* stream) {
+  if (!d_k_new || !d_v_new) return fail(KS_INVALID_ARGUMENT, "null k_new/v_new");
+  return decode_impl(pool, fmt, layer, d_q, d_k_new, d_v_new, d_out, d_lse, d_block_table,
+                     bt_stride, d_ctx_lens, batch, sm_scale, d_kv_scales, d_workspace,
+                     workspace_bytes, stream);
 }
 
 ks_status ks_compact_plan(ks_pool* pool, uint64_t key, uint32_t max_moves, ks_block_move* moves,

@@ -481,7 +481,27 @@ paged_decode_kernel(const DecodeParams p) {
       else win1 = load_window(k + 32);
     }
     const int32_t ent = __shfl_sync(0xffffffffu, ((k >> 5) & 1) ? win1 : win0, k & 31);
+    if (p.k_new != nullptr && pc.b == pc.nblk - 1) {
+      // Fused K1: this warp owns the unit's last block, which holds the new
+      // token (position ctx-1).  Quantise + store it, then order the generic
+      // writes before the bulk (async-proxy) copy that reads the block.
+      uint8_t* blk = const_cast<uint8_t*>(p.pool) +
+                     block_offset(p.geom, static_cast<uint32_t>(ent)) + p.layer_off;
+      const uint32_t slot = static_cast<uint32_t>(p.ctx_lens[pc.s] - 1) % kTPB;
+      const uint64_t row = (static_cast<uint64_t>(pc.s) * p.H + pc.h) * kD + lane * 4;
+      const uint2 rk = *reinterpret_cast<const uint2*>(p.k_new + row);
+      const uint2 rv = *reinterpret_cast<const uint2*>(p.v_new + row);
+      const float sck = (FMT == kFP8 && p.kv_scales) ? p.kv_scales[pc.h] : 1.0f;
+      const float scv = (FMT == kFP8 && p.kv_scales) ? p.kv_scales[p.H + pc.h] : 1.0f;
+      store_row<FMT>(blk + static_cast<uint64_t>(pc.h) * Gm::kChunk, blk + p.params_off, slot, 0,
+                     pc.h, p.H, kTPB, rk, sck, p.fp8_inblock, lane);
+      store_row<FMT>(blk + static_cast<uint64_t>(p.H + pc.h) * Gm::kChunk, blk + p.params_off, slot,
+                     1, pc.h, p.H, kTPB, rv, scv, p.fp8_inblock, lane);
+      fence_proxy_async_global();
+      __syncwarp();
+    }
     if (lane == 0) {
+      if (p.k_new != nullptr) fence_proxy_async_global();
       const uint64_t boff = block_offset(p.geom, static_cast<uint32_t>(ent)) + p.layer_off;
       const uint8_t* blk = p.pool + boff;
       const uint32_t tx = stage_tx_kv + (need_q ? p.G * kD * 2 : 0);

@@ -26,6 +26,10 @@ struct DecodeParams {
   uint32_t batch;
   float sm_scale_log2;
   const float* kv_scales;  // FP8 [2][H]
+  const __half* k_new;     // fused append: new token K/V [batch][H][d] (nullable)
+  const __half* v_new;
+  uint32_t params_off;     // 2*H*chunk: quant params inside a layer sub-block
+  bool fp8_inblock;
   float* partials;
   uint32_t* counters;
   // filled by the launcher

@@ -195,11 +195,15 @@ def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
                  block_table: torch.Tensor, ctx_lens: torch.Tensor,
                  out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
                  sm_scale: Optional[float] = None, kv_scales: Optional[torch.Tensor] = None,
-                 workspace: Optional[DecodeWorkspace] = None, stream=None) -> torch.Tensor:
+                 workspace: Optional[DecodeWorkspace] = None, stream=None,
+                 k_new: Optional[torch.Tensor] = None,
+                 v_new: Optional[torch.Tensor] = None) -> torch.Tensor:
     """K2: O = softmax(sm_scale * Q K^T) V over each sequence's slab blocks.
 
     q: fp16 [B, Hq, d]; block_table: int32 [B, max_blocks] of global block
-    ids; ctx_lens: int32 [B] (device).  Returns out fp16 [B, Hq, d]."""
+    ids; ctx_lens: int32 [B] (device).  With k_new/v_new (fp16 [B, Hkv, d])
+    the new token at position ctx_lens-1 is appended first (fused K1).
+    Returns out fp16 [B, Hq, d]."""
     assert q.dtype == torch.float16 and q.is_contiguous()
     assert block_table.dtype == torch.int32 and ctx_lens.dtype == torch.int32
     B = q.shape[0]
@@ -211,10 +215,19 @@ def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
         if workspace is None or workspace.max_batch < B:
             workspace = _WS[k] = DecodeWorkspace(pool, fmt, B)
     f = fmt.to_c()
-    check(L.lib.ks_paged_decode(pool.handle, C.byref(f), layer, _ptr(q), _ptr(out), _ptr(lse),
-                                _ptr(block_table), block_table.stride(0), _ptr(ctx_lens), B,
-                                0.0 if sm_scale is None else float(sm_scale), _ptr(kv_scales),
-                                _ptr(workspace.buf), workspace.nbytes, _stream(stream)))
+    scale = 0.0 if sm_scale is None else float(sm_scale)
+    if k_new is None:
+        check(L.lib.ks_paged_decode(pool.handle, C.byref(f), layer, _ptr(q), _ptr(out), _ptr(lse),
+                                    _ptr(block_table), block_table.stride(0), _ptr(ctx_lens), B,
+                                    scale, _ptr(kv_scales), _ptr(workspace.buf), workspace.nbytes,
+                                    _stream(stream)))
+    else:
+        assert k_new.dtype == torch.float16 and k_new.is_contiguous() and v_new.is_contiguous()
+        check(L.lib.ks_paged_decode_append(pool.handle, C.byref(f), layer, _ptr(q), _ptr(k_new),
+                                           _ptr(v_new), _ptr(out), _ptr(lse), _ptr(block_table),
+                                           block_table.stride(0), _ptr(ctx_lens), B, scale,
+                                           _ptr(kv_scales), _ptr(workspace.buf), workspace.nbytes,
+                                           _stream(stream)))
     return out
 
 

@@ -264,3 +264,34 @@ def test_block_table_update_and_validate():
     for i in range(pool.slab_count()):
         assert st[i, 0] == pool.slab_key(i)
         assert (st[i, 1] >> 32) == int(pool.slab_state(i))
+
+
+@pytest.mark.parametrize("dt", FORMATS, ids=[d.name for d in FORMATS])
+def test_fused_append_decode_matches_separate_k1_k2(dt):
+    """ks_paged_decode_append == ks_kv_append(last token) + ks_paged_decode,
+    bit for bit (bytes written and outputs)."""
+    fmt = KvFormat(dt, 8, 32, num_layers=2)
+    ctx = [1, 16, 17, 600, 2049, 33]
+    w = make_world(fmt, ctx, seed=21 + int(dt))
+    pool = w["pool"]
+    # the prefix (all but the last token of each sequence) is appended by K1
+    keep = np.concatenate([np.arange(c - 1) + sum(ctx[:s]) for s, c in enumerate(ctx)]).astype(int)
+    last = np.array([sum(ctx[:s + 1]) - 1 for s in range(len(ctx))])
+    sc = None if w["scales"] is None else dev(w["scales"])
+    kv.kv_append(pool, fmt, 1, dev(w["k"][keep]), dev(w["v"][keep]), dev(w["tok_seq"][keep]),
+                 dev(w["tok_pos"][keep]), dev(w["table"]), sc)
+    torch.cuda.synchronize()
+    base = kv.kv_tensor(pool).clone()
+    q = dev(w["rng"].standard_normal((len(ctx), 32, 128)).astype(np.float16))
+    table, ctxd = dev(w["table"]), dev(w["ctx"])
+    knew, vnew = dev(w["k"][last]), dev(w["v"][last])
+    fused = kv.paged_decode(pool, fmt, 1, q, table, ctxd, kv_scales=sc, k_new=knew, v_new=vnew)
+    torch.cuda.synchronize()
+    img_fused = kv.kv_tensor(pool).clone()
+    kv.kv_tensor(pool).copy_(base)
+    kv.kv_append(pool, fmt, 1, knew, vnew, dev(np.arange(len(ctx), dtype=np.int32)),
+                 dev(w["ctx"] - 1), table, sc)
+    sep = kv.paged_decode(pool, fmt, 1, q, table, ctxd, kv_scales=sc)
+    torch.cuda.synchronize()
+    assert torch.equal(img_fused, kv.kv_tensor(pool))
+    assert torch.equal(fused, sep)
