@@ -748,6 +748,10 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
     p.max_ctas = 0;
     if (const char* dbg = std::getenv("KVSLAB_DECODE_DEBUG")) p.debug = std::atoi(dbg);
     if (const char* mc = std::getenv("KVSLAB_DECODE_MAX_CTAS")) p.max_ctas = std::atoi(mc);
+    p.pdl = 1;
+    if (const char* tr = std::getenv("KVSLAB_DECODE_TRACE"))
+      p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(tr, nullptr, 0));
+    if (const char* np = std::getenv("KVSLAB_NO_PDL")) p.pdl = std::atoi(np) ? 0 : 1;
     cudaError_t e = kvslab::launch_paged_decode(p, static_cast<int>(fmt->kv_dtype), pool->num_sms,
                                                 static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "paged_decode launch");

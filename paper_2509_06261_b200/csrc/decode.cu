@@ -304,92 +304,145 @@ __device__ __forceinline__ int vdim(int mt, int g, int r8) {
   else return 16 * g + 2 * mt + r8;
 }
 
-// CTA-wide named barrier for the kDecodeWarps consumer warps (id 1).
-__device__ __forceinline__ void cta_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kDecodeWarps * 32) : "memory");
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
-// First flat index (CTA range start) of CTA c: floor(c * total / C).
-__device__ __forceinline__ uint32_t cta_start(uint32_t c, uint32_t total, uint32_t C) {
-  return static_cast<uint32_t>((static_cast<uint64_t>(c) * total) / C);
+// First flat index (CTA range start) of CTA c: floor(c * total / C), with
+// 32-bit arithmetic only (c, r0 < C <= 2^16): c*q0 + (c*r0)/C.
+struct CtaSplit {
+  uint32_t total, C, q0, r0;
+};
+__device__ __forceinline__ CtaSplit make_split(uint32_t total, uint32_t C) {
+  return CtaSplit{total, C, total / C, total % C};
+}
+__device__ __forceinline__ uint32_t cta_start(uint32_t c, const CtaSplit& sp) {
+  return c * sp.q0 + (c * sp.r0) / sp.C;
+}
+// CTA whose range contains flat index f: the largest c with start(c) <= f.
+__device__ __forceinline__ uint32_t cta_of(uint32_t f, const CtaSplit& sp) {
+  uint32_t lo = 0, hi = sp.C;  // start(lo) <= f < start(hi) (start(C) = total > f)
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (cta_start(mid, sp) <= f) lo = mid; else hi = mid;
+  }
+  return lo;
 }
 
-// Merge the CTA-level fp32 partials of one unit (run by the CTA that
-// contributes last): O = sum_j 2^(m_j - M) acc_j / sum_j 2^(m_j - M) l_j.
-// Warps split the queries; lanes split segments (max) and then dims, with the
-// segment loads unrolled so every pass is ~one memory round trip.
-template <int NQ>
-__device__ __noinline__ void merge_unit(const DecodeParams& p, const uint32_t* pre, uint32_t C,
-                                        uint32_t total, uint32_t s, uint32_t h, uint32_t nblk,
-                                        int warp, int lane) {
-  constexpr int kSlot = NQ * (kD + 2);
-  const uint64_t U0 = pre[s] + static_cast<uint64_t>(h) * nblk;
-  const uint64_t U1 = U0 + nblk;
-  const uint32_t ca = static_cast<uint32_t>(((U0 + 1) * C + total - 1) / total - 1);
-  const uint32_t cb = static_cast<uint32_t>((U1 * C + total - 1) / total - 1);
-  const uint32_t Hq = p.H * p.G;
-  for (int q = warp; q < static_cast<int>(p.G); q += kDecodeWarps) {
-    // pass 1: lanes over segments -> M (and the segment list)
-    float M = -INFINITY;
-    for (uint32_t c0 = ca; c0 <= cb; c0 += 32) {
-      const uint32_t c = c0 + lane;
-      if (c <= cb) {
-        const uint32_t cs = cta_start(c, total, C), ce = cta_start(c + 1, total, C);
-        if (cs < ce) {
-          const uint32_t sl = 2 * c + (cs < U0 ? 1 : 0);
-          M = fmaxf(M, __ldcg(p.partials + static_cast<uint64_t>(sl) * kSlot + q));
-        }
+// Merge the fp32 partials of one (sequence, head) unit -- run by the warp
+// whose CTA contributes last:  O = sum_j 2^(m_j-M) acc_j / sum_j 2^(m_j-M) l_j.
+// Lanes split (query, dims) with GP = pow2 >= G queries; segments are merged
+// online in batches of SB whose loads are all issued before any is used, so
+// the merge costs ~ceil(nseg / SB) memory round trips.
+template <int GP>
+__device__ __forceinline__ void merge_unit(const DecodeParams& p, const uint32_t* pre,
+                                           const CtaSplit& sp, uint32_t s, uint32_t grp,
+                                           uint32_t nblk, uint32_t hw, uint32_t HG, int lane) {
+  constexpr int LPQ = 32 / GP;   // lanes per query
+  constexpr int DPL = kD / LPQ;  // dims per lane
+  constexpr int F4 = DPL / 4;    // float4 per lane per segment
+  constexpr int SB = F4 >= 24 ? 1 : 24 / F4;  // segments per batch (<= 24 float4 in flight)
+  const uint32_t G = p.G;
+  const uint32_t hdr = (2 * G + 3) & ~3u;  // m[G], l[G], padded to 16 B
+  const uint32_t slot_f = hdr + G * kD;
+  const uint32_t U0 = pre[s] + grp * nblk;
+  const uint32_t ca = cta_of(U0, sp), cb = cta_of(U0 + nblk - 1, sp);
+  const int q = lane / LPQ, sub = lane % LPQ;
+  if (q >= static_cast<int>(G)) return;
+  float M = -INFINITY, L = 0.f;
+  float acc[DPL];
+#pragma unroll
+  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+  uint32_t c_lo = cta_start(ca, sp);
+  for (uint32_t c0 = ca; c0 <= cb; c0 += SB) {
+    float mv[SB], lv[SB];
+    float4 av[SB][F4];
+#pragma unroll
+    for (int j = 0; j < SB; ++j) {
+      const uint32_t c = c0 + j;
+      const uint32_t c_hi = cta_start(c + 1, sp);
+      const bool valid = c <= cb && c_lo < c_hi;
+      const float* pp =
+          p.partials + ((2ull * c + (c_lo < U0 ? 1 : 0)) * HG + hw) * static_cast<uint64_t>(slot_f);
+      mv[j] = valid ? __ldcg(pp + q) : -INFINITY;
+      lv[j] = valid ? __ldcg(pp + G + q) : 0.f;
+      const float4* src = reinterpret_cast<const float4*>(pp + hdr + q * kD + sub * DPL);
+#pragma unroll
+      for (int i = 0; i < F4; ++i) av[j][i] = valid ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      c_lo = c_hi;
+    }
+    float Mb = M;
+#pragma unroll
+    for (int j = 0; j < SB; ++j) Mb = fmaxf(Mb, mv[j]);
+    const float a = ex2(M - Mb);  // 0 when M == -inf
+    L *= a;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) acc[i] *= a;
+#pragma unroll
+    for (int j = 0; j < SB; ++j) {
+      const float f = ex2(mv[j] - Mb);  // 0 for invalid segments
+      L += f * lv[j];
+#pragma unroll
+      for (int i = 0; i < F4; ++i) {
+        acc[4 * i] += f * av[j][i].x; acc[4 * i + 1] += f * av[j][i].y;
+        acc[4 * i + 2] += f * av[j][i].z; acc[4 * i + 3] += f * av[j][i].w;
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    // pass 2: all lanes over dims (4 each), segments unrolled
-    float L = 0.f;
-    float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-    for (uint32_t c = ca; c <= cb; ++c) {
-      const uint32_t cs = cta_start(c, total, C), ce = cta_start(c + 1, total, C);
-      if (cs >= ce) continue;
-      const uint32_t sl = 2 * c + (cs < U0 ? 1 : 0);
-      const float* pp = p.partials + static_cast<uint64_t>(sl) * kSlot;
-      const float f = ex2(__ldcg(pp + q) - M);
-      L += f * __ldcg(pp + NQ + q);
-      const float4 a4 = __ldcg(reinterpret_cast<const float4*>(pp + 2 * NQ + q * kD) + lane);
-      o4.x += f * a4.x; o4.y += f * a4.y; o4.z += f * a4.z; o4.w += f * a4.w;
-    }
-    const float inv = 1.f / L;
-    __half* orow = p.out + (static_cast<uint64_t>(s) * Hq + h * p.G + q) * kD + 4 * lane;
-    *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(o4.x * inv, o4.y * inv);
-    *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(o4.z * inv, o4.w * inv);
-    if (p.lse && lane == 0)
-      p.lse[static_cast<uint64_t>(s) * Hq + h * p.G + q] = (M + __log2f(L)) * 0.69314718055994531f;
+    M = Mb;
   }
+  const uint32_t Hq = p.H * G;
+  const uint32_t head = grp * HG + hw;
+  const float inv = 1.f / L;
+  __half* orow = p.out + (static_cast<uint64_t>(s) * Hq + head * G + q) * kD + sub * DPL;
+#pragma unroll
+  for (int i = 0; i < DPL; i += 2)
+    *reinterpret_cast<__half2*>(orow + i) = __floats2half2_rn(acc[i] * inv, acc[i + 1] * inv);
+  if (p.lse && sub == 0)
+    p.lse[static_cast<uint64_t>(s) * Hq + head * G + q] = (M + __log2f(L)) * 0.69314718055994531f;
+}
+
+template <int NT>
+__device__ __forceinline__ void merge_dispatch(const DecodeParams& p, const uint32_t* pre,
+                                               const CtaSplit& sp, uint32_t s, uint32_t grp,
+                                               uint32_t nblk, uint32_t hw, uint32_t HG, int lane) {
+  if (p.G <= 1) merge_unit<1>(p, pre, sp, s, grp, nblk, hw, HG, lane);
+  else if (p.G <= 2) merge_unit<2>(p, pre, sp, s, grp, nblk, hw, HG, lane);
+  else if (p.G <= 4) merge_unit<4>(p, pre, sp, s, grp, nblk, hw, HG, lane);
+  else if (p.G <= 8) merge_unit<8>(p, pre, sp, s, grp, nblk, hw, HG, lane);
+  else if constexpr (NT == 2) merge_unit<16>(p, pre, sp, s, grp, nblk, hw, HG, lane);
 }
 
 // ------------------------------------------------------------------ kernel
-// Work split: the flattened (seq, kv-head, block) list is cut into one equal
-// contiguous range per CTA (persistent grid).  Inside a CTA, block i of the
-// range belongs to warp i % 4; each warp streams its own blocks through its
-// private ring and keeps an online-softmax state per unit.  At the end of each
-// unit segment the 4 warp states are combined in shared memory; a unit cut by
-// a CTA-range boundary leaves one fp32 partial per CTA, merged by the CTA
-// that finishes last (per-unit counter, no second launch).
-template <int FMT, int NT, int STAGES>
-__global__ void __launch_bounds__(kDecodeWarps * 32, NT == 1 ? 3 : 2)
+// CTA = HG consumer warps (one KV head each, a head group) + 1 producer warp.
+// Work = the flattened list of (sequence, head group, block) cut into one
+// equal contiguous range per CTA of a persistent grid (stream-K: ragged
+// contexts balance exactly).  The producer streams each block's K, V and
+// params for the whole head group with ONE bulk copy each (they are
+// contiguous in the layer sub-block) into a shared STAGES-deep ring
+// (full/empty mbarriers), and the group's Q rows into a ping-pong Q buffer at
+// each unit start.  Every consumer warp runs the tensor-core online softmax
+// for its head; a (sequence, head) cut by a CTA-range boundary leaves an fp32
+// partial that the warp finishing the unit last merges (per-unit counter).
+template <int FMT, int NT>
+__global__ void __launch_bounds__(NT == 1 ? 288 : 160, 1)
 paged_decode_kernel(const DecodeParams p) {
   using Gm = Geo<FMT>;
-  constexpr int NW = kDecodeWarps;
-  constexpr int kNQ = NT * 8;
-  constexpr int kSlot = kNQ * (kD + 2);
   constexpr float kRescaleSlack = 8.0f;  // log2 units: P <= 2^8 before a rescale
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  const uint32_t HG = p.hg, NG = p.H / p.hg, S = p.stages;
+  // PDL contract: before griddepcontrol.wait this kernel reads only data no
+  // PDL-enabled predecessor writes (ctx_lens, block tables, KV of other
+  // layers); Q, new K/V, outputs and the workspace come after the wait.
+  pdl_launch_dependents();
+  const uint64_t t_start = p.trace ? gtimer() : 0;
 
-  // ---- per-CTA prefix of blocks over sequences (x H) ----
+  // ---- per-CTA prefix of blocks over sequences (x NG head groups) ----
   uint32_t* pre = reinterpret_cast<uint32_t*>(smem + p.prefix_offset);
-  __shared__ uint32_t wsum[NW];
-  __shared__ uint32_t s_last;
+  __shared__ uint32_t wsum[9];
   {
     const uint32_t nthr = blockDim.x, per = (p.batch + nthr - 1) / nthr;
     const uint32_t b0 = min(p.batch, threadIdx.x * per), b1 = min(p.batch, b0 + per);
@@ -410,19 +463,40 @@ paged_decode_kernel(const DecodeParams p) {
     for (int w = 0; w < warp; ++w) wbase += wsum[w];
     uint32_t run = wbase + incl - sum;
     for (uint32_t s = b0; s < b1; ++s) {
-      pre[s] = run * p.H;
+      pre[s] = run * NG;
       const int c = p.ctx_lens[s];
       run += c > 0 ? (static_cast<uint32_t>(c) + kTPB - 1) / kTPB : 0;
     }
-    if (threadIdx.x == nthr - 1) pre[p.batch] = run * p.H;
-    __syncthreads();
+    if (threadIdx.x == nthr - 1) pre[p.batch] = run * NG;
   }
+  // barriers: full[S], empty[S], qfull[2], qempty[2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_offset);
+  uint64_t* empty = full + S;
+  uint64_t* qfull = empty + S;
+  uint64_t* qempty = qfull + 2;
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], HG);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], HG);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
   const uint32_t total = pre[p.batch];
 
   // CTA 0 writes empty outputs for sequences with no context.
   if (blockIdx.x == 0) {
+    bool waited = false;
     for (uint32_t s = threadIdx.x; s < p.batch; s += blockDim.x) {
       if (pre[s + 1] != pre[s]) continue;
+      if (!waited) {
+        pdl_wait();
+        waited = true;
+      }
       for (uint32_t i = 0; i < p.H * p.G * kD; ++i)
         p.out[(static_cast<uint64_t>(s) * p.H * p.G) * kD + i] = __float2half(0.f);
       if (p.lse)
@@ -431,282 +505,280 @@ paged_decode_kernel(const DecodeParams p) {
   }
 
   const uint32_t C = gridDim.x;
-  const uint32_t cs = cta_start(blockIdx.x, total, C), ce = cta_start(blockIdx.x + 1, total, C);
+  const CtaSplit sp = make_split(total, C);
+  const uint32_t cs = cta_start(blockIdx.x, sp), ce = cta_start(blockIdx.x + 1, sp);
   if (cs >= ce) return;  // uniform across the CTA
-  // this warp's blocks: flat cs + warp + NW*k, k < nmine
-  const uint32_t nmine = ce > cs + warp ? (ce - cs - warp + NW - 1) / NW : 0;
-
-  uint8_t* wbuf = smem + static_cast<size_t>(warp) * STAGES * p.stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.bar_offset) + warp * STAGES;
-  float* comb = reinterpret_cast<float*>(smem + p.comb_offset);  // [NW][kSlot]
-  const uint32_t q_off = 2 * Gm::kChunk + 2 * Gm::kParam;
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < STAGES; ++i) mbar_init(&bars[i], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-
-  const uint64_t pol = policy_evict_first();
+  const uint32_t n = ce - cs;
   const uint32_t Hq = p.H * p.G;
-  const uint32_t stage_tx_kv = 2 * Gm::kChunk + 2 * Gm::kParam;
+  const uint32_t kvq = HG * Gm::kChunk;          // bytes of the group's K (or V) chunks
+  const uint32_t pq = HG * Gm::kParam;           // bytes of the group's K (or V) params
+  const uint32_t qbytes = HG * p.G * kD * 2;
+  uint8_t* ring = smem;
+  uint8_t* qbuf = smem + p.qbuf_offset;
 
-  // ---- producer (lane 0 issues; all lanes track the cursor) ----
-  // Block-table entries are fetched 32 at a time (lane j holds the entry of
-  // this warp's block base+j), double-buffered one window ahead.
-  auto load_window = [&](uint32_t base) -> int32_t {
-    int32_t e = 0;
-    if (base + lane < nmine) {
-      Cursor c;
-      cursor_seek(c, pre, p.batch, p.H, cs + warp + NW * (base + lane));
-      e = __ldg(p.block_table + static_cast<uint64_t>(c.s) * p.bt_stride + c.b);
-    }
-    return e;
-  };
-  int32_t win0 = nmine ? load_window(0) : 0;
-  int32_t win1 = nmine > 32 ? load_window(32) : 0;
-  Cursor pc;  // cursor of the next block to issue
-  if (nmine) cursor_seek(pc, pre, p.batch, p.H, cs + warp);
-  uint32_t prev_unit = 0xffffffffu;
-  uint32_t issued = 0;
-
-  auto issue = [&](uint32_t k) {
-    const uint32_t st = k % STAGES;
-    uint8_t* sb = wbuf + st * p.stage_bytes;
-    const uint32_t unit = pc.s * p.H + pc.h;
-    const bool need_q = unit != prev_unit;
-    prev_unit = unit;
-    if ((k & 31) == 0 && k > 0 && k + 32 < nmine) {
-      if ((k >> 5) & 1) win0 = load_window(k + 32);
-      else win1 = load_window(k + 32);
-    }
-    const int32_t ent = __shfl_sync(0xffffffffu, ((k >> 5) & 1) ? win1 : win0, k & 31);
-    if (p.k_new != nullptr && pc.b == pc.nblk - 1) {
-      // Fused K1: this warp owns the unit's last block, which holds the new
-      // token (position ctx-1).  Quantise + store it, then order the generic
-      // writes before the bulk (async-proxy) copy that reads the block.
-      uint8_t* blk = const_cast<uint8_t*>(p.pool) +
-                     block_offset(p.geom, static_cast<uint32_t>(ent)) + p.layer_off;
-      const uint32_t slot = static_cast<uint32_t>(p.ctx_lens[pc.s] - 1) % kTPB;
-      const uint64_t row = (static_cast<uint64_t>(pc.s) * p.H + pc.h) * kD + lane * 4;
-      const uint2 rk = *reinterpret_cast<const uint2*>(p.k_new + row);
-      const uint2 rv = *reinterpret_cast<const uint2*>(p.v_new + row);
-      const float sck = (FMT == kFP8 && p.kv_scales) ? p.kv_scales[pc.h] : 1.0f;
-      const float scv = (FMT == kFP8 && p.kv_scales) ? p.kv_scales[p.H + pc.h] : 1.0f;
-      store_row<FMT>(blk + static_cast<uint64_t>(pc.h) * Gm::kChunk, blk + p.params_off, slot, 0,
-                     pc.h, p.H, kTPB, rk, sck, p.fp8_inblock, lane);
-      store_row<FMT>(blk + static_cast<uint64_t>(p.H + pc.h) * Gm::kChunk, blk + p.params_off, slot,
-                     1, pc.h, p.H, kTPB, rv, scv, p.fp8_inblock, lane);
-      fence_proxy_async_global();
-      __syncwarp();
-    }
-    if (lane == 0) {
-      if (p.k_new != nullptr) fence_proxy_async_global();
-      const uint64_t boff = block_offset(p.geom, static_cast<uint32_t>(ent)) + p.layer_off;
-      const uint8_t* blk = p.pool + boff;
-      const uint32_t tx = stage_tx_kv + (need_q ? p.G * kD * 2 : 0);
-      mbar_expect_tx(&bars[st], tx);
-      bulk_g2s(sb, blk + static_cast<uint64_t>(pc.h) * Gm::kChunk, Gm::kChunk, &bars[st], pol);
-      bulk_g2s(sb + Gm::kChunk, blk + static_cast<uint64_t>(p.H + pc.h) * Gm::kChunk, Gm::kChunk,
-               &bars[st], pol);
-      if constexpr (Gm::kParam > 0) {
-        const uint8_t* prm = blk + 2ull * p.H * Gm::kChunk;
-        bulk_g2s(sb + 2 * Gm::kChunk, prm + static_cast<uint64_t>(pc.h) * Gm::kParam, Gm::kParam,
-                 &bars[st], pol);
-        bulk_g2s(sb + 2 * Gm::kChunk + Gm::kParam,
-                 prm + static_cast<uint64_t>(p.H + pc.h) * Gm::kParam, Gm::kParam, &bars[st], pol);
+  if (warp == static_cast<int>(HG)) {
+    // ============================ producer warp ============================
+    const uint64_t pol = policy_evict_first();
+    auto load_window = [&](uint32_t base) -> int32_t {
+      int32_t e = 0;
+      if (base + lane < n) {
+        Cursor c;
+        cursor_seek(c, pre, p.batch, NG, cs + base + lane);
+        e = __ldg(p.block_table + static_cast<uint64_t>(c.s) * p.bt_stride + c.b);
       }
-      if (need_q) {
-        bulk_g2s(sb + q_off, p.q + (static_cast<uint64_t>(pc.s) * Hq + pc.h * p.G) * kD,
-                 p.G * kD * 2, &bars[st], pol);
+      return e;
+    };
+    int32_t win0 = load_window(0);
+    int32_t win1 = n > 32 ? load_window(32) : 0;
+    Cursor pc;
+    cursor_seek(pc, pre, p.batch, NG, cs);
+    bool dep_ready = false;
+    uint32_t ui = 0, st = 0, ph = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+      if ((k & 31) == 0 && k > 0 && k + 32 < n) {
+        if ((k >> 5) & 1) win0 = load_window(k + 32);
+        else win1 = load_window(k + 32);
+      }
+      const int32_t ent = __shfl_sync(0xffffffffu, ((k >> 5) & 1) ? win1 : win0, k & 31);
+      const uint32_t g0 = pc.h * HG;  // first head of the group (cursor field h = group)
+      const uint8_t* blk = p.pool + block_offset(p.geom, static_cast<uint32_t>(ent)) + p.layer_off;
+      const bool first_of_unit = (k == 0) || (pc.b == 0);
+      mbar_wait(&empty[st], ph ^ 1);
+      if (p.k_new != nullptr && pc.b == pc.nblk - 1) {
+        // Fused K1: this block holds the new token (position ctx-1) of every
+        // head of the group.  Quantise + store it, then order the generic
+        // writes before the bulk (async-proxy) copy that reads the block.
+        if (!dep_ready) {
+          pdl_wait();
+          dep_ready = true;
+        }
+        uint8_t* wblk = const_cast<uint8_t*>(blk);
+        const uint32_t slot = static_cast<uint32_t>(p.ctx_lens[pc.s] - 1) % kTPB;
+        for (uint32_t hh = 0; hh < HG; ++hh) {
+          const uint32_t h = g0 + hh;
+          const uint64_t row = (static_cast<uint64_t>(pc.s) * p.H + h) * kD + lane * 4;
+          const uint2 rk = *reinterpret_cast<const uint2*>(p.k_new + row);
+          const uint2 rv = *reinterpret_cast<const uint2*>(p.v_new + row);
+          const float sck = (FMT == kFP8 && p.kv_scales) ? p.kv_scales[h] : 1.0f;
+          const float scv = (FMT == kFP8 && p.kv_scales) ? p.kv_scales[p.H + h] : 1.0f;
+          store_row<FMT>(wblk + static_cast<uint64_t>(h) * Gm::kChunk, wblk + p.params_off, slot,
+                         0, h, p.H, kTPB, rk, sck, p.fp8_inblock, lane);
+          store_row<FMT>(wblk + static_cast<uint64_t>(p.H + h) * Gm::kChunk, wblk + p.params_off,
+                         slot, 1, h, p.H, kTPB, rv, scv, p.fp8_inblock, lane);
+        }
+        fence_proxy_async_global();
+        __syncwarp();
+      }
+      if (first_of_unit && !dep_ready) {  // Q comes from the predecessor
+        pdl_wait();
+        dep_ready = true;
+      }
+      if (lane == 0) {
+        if (p.k_new != nullptr) fence_proxy_async_global();
+        uint8_t* sb = ring + static_cast<size_t>(st) * p.stage_bytes;
+        mbar_expect_tx(&full[st], 2 * kvq + 2 * pq);
+        bulk_g2s(sb, blk + static_cast<uint64_t>(g0) * Gm::kChunk, kvq, &full[st], pol);
+        bulk_g2s(sb + kvq, blk + static_cast<uint64_t>(p.H + g0) * Gm::kChunk, kvq, &full[st], pol);
+        if constexpr (Gm::kParam > 0) {
+          const uint8_t* prm = blk + 2ull * p.H * Gm::kChunk;
+          bulk_g2s(sb + 2 * kvq, prm + static_cast<uint64_t>(g0) * Gm::kParam, pq, &full[st], pol);
+          bulk_g2s(sb + 2 * kvq + pq, prm + static_cast<uint64_t>(p.H + g0) * Gm::kParam, pq,
+                   &full[st], pol);
+        }
+        if (first_of_unit) {
+          const uint32_t qs = ui & 1;
+          mbar_wait(&qempty[qs], ((ui >> 1) & 1) ^ 1);
+          mbar_expect_tx(&qfull[qs], qbytes);
+          bulk_g2s(qbuf + qs * qbytes, p.q + (static_cast<uint64_t>(pc.s) * Hq + g0 * p.G) * kD,
+                   qbytes, &qfull[qs], pol);
+        }
+      }
+      if (first_of_unit) ++ui;
+      cursor_next(pc, pre, p.batch, NG);
+      if (++st == S) {
+        st = 0;
+        ph ^= 1;
       }
     }
-#pragma unroll
-    for (int j = 0; j < NW; ++j) cursor_next(pc, pre, p.batch, p.H);
-  };
-  const uint32_t prologue = nmine < STAGES ? nmine : STAGES;
-  for (uint32_t k = 0; k < prologue; ++k) issue(k);
-  issued = prologue;
+    return;
+  }
 
-  // ---- consumer ----
+  // ============================ consumer warps ============================
   const FragOff fo = make_offsets<FMT>(g, t);
   uint32_t qf[NT][8][2];
   float acc[8][NT][4];
   float m_run[NT][2], l_run[NT][2], z_run[NT][2], qsum[NT][2];
   float kscale = 1.f, vscale = 1.f;
-  uint32_t k = 0;  // this warp's consumed blocks
+  uint32_t seg_b0 = 0, ui = 0, st = 0, ph = 0;
+  int ctx_cur = 0;
+  Cursor cc;
+  cursor_seek(cc, pre, p.batch, NG, cs);
+  uint32_t pend_s[2], pend_g[2], pend_n[2], npend = 0;
+  uint64_t t_atom = 0, t_fence = 0;
+  const uint32_t slot_hdr = (2 * p.G + 3) & ~3u;  // m[G], l[G], padded to 16 B
+  const uint32_t slot_f = slot_hdr + p.G * kD;
 
-  Cursor cu;  // CTA-level unit cursor at `flat`
-  cursor_seek(cu, pre, p.batch, p.H, cs);
-  uint32_t flat = cs;
-  while (flat < ce) {
-    const uint32_t ustart = flat - cu.b;           // flat index of the unit's block 0
-    const uint32_t uend = ustart + cu.nblk;
-    const uint32_t segb = min(ce, uend);
-    const uint32_t unit = cu.s * p.H + cu.h;
-    const int ctx_cur = p.ctx_lens[cu.s];
-    // reset the online-softmax state
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      m_run[nt][0] = m_run[nt][1] = -INFINITY;
-      l_run[nt][0] = l_run[nt][1] = 0.f;
-      z_run[nt][0] = z_run[nt][1] = 0.f;
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
-    }
-    if constexpr (FMT == kFP8) {
-      if (p.kv_scales) {
-        kscale = p.kv_scales[cu.h];
-        vscale = p.kv_scales[p.H + cu.h];
-      }
-    }
-    // this warp's first block in [flat, segb)
-    const uint32_t i0 = flat + ((static_cast<uint32_t>(warp) + NW - ((flat - cs) % NW)) % NW);
-    bool first = true;
-    for (uint32_t i = i0; i < segb; i += NW, ++k) {
-      const uint32_t st = k % STAGES;
-      const uint32_t sK = smem_u32(wbuf + st * p.stage_bytes), sV = sK + Gm::kChunk;
-      const uint32_t sKp = sK + 2 * Gm::kChunk, sVp = sKp + Gm::kParam;
-      mbar_wait(&bars[st], (k / STAGES) & 1);
-      if (first) {
-        first = false;
-        load_q_frags<FMT, NT>(sK + q_off, g, t, p.G, qf);
-        if constexpr (FMT == kINT4) {
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            float qs = 0.f;
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][0]));
-              const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][1]));
-              qs += (f0.x + f0.y) + (f1.x + f1.y);
-            }
-            qs += __shfl_xor_sync(0xffffffffu, qs, 1);
-            qs += __shfl_xor_sync(0xffffffffu, qs, 2);
-            qsum[nt][0] = __shfl_sync(0xffffffffu, qs, (2 * t) * 4);
-            qsum[nt][1] = __shfl_sync(0xffffffffu, qs, (2 * t + 1) * 4);
-          }
-        }
-      }
-      if (!(p.debug & 1)) {
-        // ---- S^T = K . Q^T (two accumulators halve the dependent MMA chain) ----
-        uint32_t ka[8][4];
-        load_k_frags<FMT>(sK, fo, ka);
-        float sacc[NT][4];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          float s2[4] = {0.f, 0.f, 0.f, 0.f};
-          sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-#pragma unroll
-          for (int kk = 0; kk < 8; kk += 2) {
-            mma16816(sacc[nt], ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
-            mma16816(s2, ka[kk + 1][0], ka[kk + 1][1], ka[kk + 1][2], ka[kk + 1][3],
-                     qf[nt][kk + 1][0], qf[nt][kk + 1][1]);
-          }
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sacc[nt][e] += s2[e];
-        }
-        uint32_t va[8][4];
-        load_v_frags<FMT>(sV, fo, va);
-
-        float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f}, sv[2] = {1.f, 1.f}, zv[2] = {0.f, 0.f};
-        if constexpr (FMT == kINT8) {
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
-            sv[r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
-          }
-        } else if constexpr (FMT == kINT4) {
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
-            sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
-            zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
-            sv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
-            zv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
-          }
-        }
-        const int bb = static_cast<int>(i - ustart);
-        const int valid = min(kTPB, ctx_cur - bb * kTPB);
-
-        uint32_t pb[NT][2];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          float sc[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = e >> 1, tok = g + 8 * r;
-            float x = sacc[nt][e] * sk[r];
-            if constexpr (FMT == kINT4) x += zk[r] * qsum[nt][e & 1];
-            x *= p.sm_scale_log2;
-            sc[e] = tok < valid ? x : -INFINITY;
-          }
-          float mx[2] = {fmaxf(sc[0], sc[2]), fmaxf(sc[1], sc[3])};
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
-            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
-            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
-          }
-          // Lazy rescaling: keep the reference max until a score exceeds it by
-          // kRescaleSlack (P stays <= 2^8), so the accumulator rescale runs
-          // only when the running max really moves.
-          const bool grow = (mx[0] > m_run[nt][0] + kRescaleSlack) ||
-                            (mx[1] > m_run[nt][1] + kRescaleSlack);
-          if (__any_sync(0xffffffffu, grow)) {
-            float alpha[2];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const float mn = fmaxf(m_run[nt][c], mx[c]);
-              alpha[c] = ex2(m_run[nt][c] - mn);
-              m_run[nt][c] = mn;
-              l_run[nt][c] *= alpha[c];
-              z_run[nt][c] *= alpha[c];
-            }
-#pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-              acc[mt][nt][0] *= alpha[0];
-              acc[mt][nt][1] *= alpha[1];
-              acc[mt][nt][2] *= alpha[0];
-              acc[mt][nt][3] *= alpha[1];
-            }
-          }
-          float pr[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[e] - m_run[nt][e & 1]);
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            l_run[nt][c] += pr[c] + pr[c + 2];
-            if constexpr (FMT == kINT4) z_run[nt][c] += pr[c] * zv[0] + pr[c + 2] * zv[1];
-          }
-          const uint32_t plo = pack_h2(pr[0] * sv[0], pr[1] * sv[0]);
-          const uint32_t phi = pack_h2(pr[2] * sv[1], pr[3] * sv[1]);
-          const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
-          const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
-          const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
-          const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
-          pb[nt][0] = __byte_perm(xa, xb, sel);
-          pb[nt][1] = __byte_perm(ya, yb, sel);
-        }
-
-        // ---- O^T += V^T . P^T ----
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-            mma16816(acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[nt][0], pb[nt][1]);
-      }
-      // the stage is consumed: refill it
+  for (uint32_t k = 0; k < n; ++k) {
+    const uint32_t head = cc.h * HG + warp;
+    if (k == 0 || cc.b == 0) {  // first block of a unit segment
+      seg_b0 = cc.b;
+      ctx_cur = p.ctx_lens[cc.s];
+      const uint32_t qs = ui & 1;
+      mbar_wait(&qfull[qs], (ui >> 1) & 1);
+      load_q_frags<FMT, NT>(smem_u32(qbuf + qs * qbytes) + warp * p.G * kD * 2, g, t, p.G, qf);
       __syncwarp();
-      if (issued < nmine) {
-        issue(issued);
-        ++issued;
+      if (lane == 0) mbar_arrive(&qempty[qs]);
+      ++ui;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        if constexpr (FMT == kINT4) {
+          float qsm = 0.f;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][0]));
+            const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][1]));
+            qsm += (f0.x + f0.y) + (f1.x + f1.y);
+          }
+          qsm += __shfl_xor_sync(0xffffffffu, qsm, 1);
+          qsm += __shfl_xor_sync(0xffffffffu, qsm, 2);
+          qsum[nt][0] = __shfl_sync(0xffffffffu, qsm, (2 * t) * 4);
+          qsum[nt][1] = __shfl_sync(0xffffffffu, qsm, (2 * t + 1) * 4);
+        }
+        m_run[nt][0] = m_run[nt][1] = -INFINITY;
+        l_run[nt][0] = l_run[nt][1] = 0.f;
+        z_run[nt][0] = z_run[nt][1] = 0.f;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
+      }
+      if constexpr (FMT == kFP8) {
+        if (p.kv_scales) {
+          kscale = p.kv_scales[head];
+          vscale = p.kv_scales[p.H + head];
+        }
       }
     }
 
-    // ---- combine the 4 warp states of this unit segment in shared memory ----
-    {
-      float* my = comb + warp * kSlot;
+    mbar_wait(&full[st], ph);
+    const uint32_t sb = smem_u32(ring + static_cast<size_t>(st) * p.stage_bytes);
+    const uint32_t sK = sb + warp * Gm::kChunk, sV = sb + kvq + warp * Gm::kChunk;
+    const uint32_t sKp = sb + 2 * kvq + warp * Gm::kParam, sVp = sb + 2 * kvq + pq + warp * Gm::kParam;
+    if (!(p.debug & 1)) {
+      // ---- S^T = K . Q^T (two accumulators halve the dependent MMA chain) ----
+      uint32_t ka[8][4];
+      load_k_frags<FMT>(sK, fo, ka);
+      float sacc[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        float s2[4] = {0.f, 0.f, 0.f, 0.f};
+        sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 2) {
+          mma16816(sacc[nt], ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
+          mma16816(s2, ka[kk + 1][0], ka[kk + 1][1], ka[kk + 1][2], ka[kk + 1][3],
+                   qf[nt][kk + 1][0], qf[nt][kk + 1][1]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sacc[nt][e] += s2[e];
+      }
+      uint32_t va[8][4];
+      load_v_frags<FMT>(sV, fo, va);
+
+      float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f}, sv[2] = {1.f, 1.f}, zv[2] = {0.f, 0.f};
+      if constexpr (FMT == kINT8) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
+          sv[r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
+        }
+      } else if constexpr (FMT == kINT4) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
+          sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
+          zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
+          sv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
+          zv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
+        }
+      }
+      const int valid = min(kTPB, ctx_cur - static_cast<int>(cc.b) * kTPB);
+
+      uint32_t pb[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        float sc[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = e >> 1, tok = g + 8 * r;
+          float x = sacc[nt][e] * sk[r];
+          if constexpr (FMT == kINT4) x += zk[r] * qsum[nt][e & 1];
+          x *= p.sm_scale_log2;
+          sc[e] = tok < valid ? x : -INFINITY;
+        }
+        float mx[2] = {fmaxf(sc[0], sc[2]), fmaxf(sc[1], sc[3])};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
+          mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
+          mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
+        }
+        // Lazy rescaling: the reference max moves (and the accumulator is
+        // rescaled) only when a score exceeds it by kRescaleSlack.
+        const bool grow = (mx[0] > m_run[nt][0] + kRescaleSlack) ||
+                          (mx[1] > m_run[nt][1] + kRescaleSlack);
+        if (__any_sync(0xffffffffu, grow)) {
+          float alpha[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const float mn = fmaxf(m_run[nt][c], mx[c]);
+            alpha[c] = ex2(m_run[nt][c] - mn);
+            m_run[nt][c] = mn;
+            l_run[nt][c] *= alpha[c];
+            z_run[nt][c] *= alpha[c];
+          }
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            acc[mt][nt][0] *= alpha[0];
+            acc[mt][nt][1] *= alpha[1];
+            acc[mt][nt][2] *= alpha[0];
+            acc[mt][nt][3] *= alpha[1];
+          }
+        }
+        float pr[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[e] - m_run[nt][e & 1]);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          l_run[nt][c] += pr[c] + pr[c + 2];
+          if constexpr (FMT == kINT4) z_run[nt][c] += pr[c] * zv[0] + pr[c + 2] * zv[1];
+        }
+        const uint32_t plo = pack_h2(pr[0] * sv[0], pr[1] * sv[0]);
+        const uint32_t phi = pack_h2(pr[2] * sv[1], pr[3] * sv[1]);
+        const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
+        const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
+        const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
+        const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
+        pb[nt][0] = __byte_perm(xa, xb, sel);
+        pb[nt][1] = __byte_perm(ya, yb, sel);
+      }
+      // ---- O^T += V^T . P^T ----
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          mma16816(acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[nt][0], pb[nt][1]);
+    }
+    // release the stage to the producer
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (++st == S) {
+      st = 0;
+      ph ^= 1;
+    }
+
+    // ---- end of a unit segment ----
+    if (k == n - 1 || cc.b == cc.nblk - 1) {
+      const bool whole = (seg_b0 == 0) && (cc.b == cc.nblk - 1);
+      float lf[NT][2], zf[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -720,109 +792,136 @@ paged_decode_kernel(const DecodeParams p) {
             z += __shfl_xor_sync(0xffffffffu, z, 8);
             z += __shfl_xor_sync(0xffffffffu, z, 16);
           }
-          const int q = nt * 8 + 2 * t + c;
-          if (g == 0) {
-            my[q] = m_run[nt][c];
-            my[kNQ + q] = l;
-          }
-#pragma unroll
-          for (int mt = 0; mt < 8; ++mt) {
-            const int d0 = vdim<FMT>(mt, g, 0);
-            float2 v;
-            v.x = acc[mt][nt][c] * vscale + z;
-            v.y = acc[mt][nt][2 + c] * vscale + z;
-            *reinterpret_cast<float2*>(my + 2 * kNQ + q * kD + d0) = v;
-          }
+          lf[nt][c] = l;
+          zf[nt][c] = z;
         }
-    }
-    cta_bar();
-    const bool whole = (flat == ustart) && (segb == uend);
-    // seg slot in global partials: 2*cta (first segment of the CTA) or 2*cta+1
-    float* ps = p.partials + static_cast<uint64_t>(2 * blockIdx.x + (flat == cs ? 0 : 1)) * kSlot;
-    for (int q = warp; q < static_cast<int>(p.G); q += NW) {
-      float M = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) M = fmaxf(M, comb[w * kSlot + q]);
-      float L = 0.f;
-      float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const float* sw = comb + w * kSlot;
-        const float f = sw[q] == -INFINITY ? 0.f : ex2(sw[q] - M);
-        L += f * sw[kNQ + q];
-        const float4 a4 = reinterpret_cast<const float4*>(sw + 2 * kNQ + q * kD)[lane];
-        o4.x += f * a4.x; o4.y += f * a4.y; o4.z += f * a4.z; o4.w += f * a4.w;
-      }
       if (whole) {
-        const float inv = 1.f / L;
-        __half* orow = p.out + (static_cast<uint64_t>(cu.s) * Hq + cu.h * p.G + q) * kD + 4 * lane;
-        *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(o4.x * inv, o4.y * inv);
-        *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(o4.z * inv, o4.w * inv);
-        if (p.lse && lane == 0)
-          p.lse[static_cast<uint64_t>(cu.s) * Hq + cu.h * p.G + q] =
-              (M + __log2f(L)) * 0.69314718055994531f;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int q = nt * 8 + 2 * t + c;
+            if (q >= static_cast<int>(p.G)) continue;
+            const float inv = 1.f / lf[nt][c];
+            __half* orow = p.out + (static_cast<uint64_t>(cc.s) * Hq + head * p.G + q) * kD;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+              const int d0 = vdim<FMT>(mt, g, 0);
+              const float o0 = (acc[mt][nt][c] * vscale + zf[nt][c]) * inv;
+              const float o1 = (acc[mt][nt][2 + c] * vscale + zf[nt][c]) * inv;
+              *reinterpret_cast<__half2*>(orow + d0) = __floats2half2_rn(o0, o1);
+            }
+            if (p.lse && g == 0)
+              p.lse[static_cast<uint64_t>(cc.s) * Hq + head * p.G + q] =
+                  (m_run[nt][c] + __log2f(lf[nt][c])) * 0.69314718055994531f;
+          }
       } else {
-        if (lane == 0) {
-          ps[q] = M;
-          ps[kNQ + q] = L;
+        // partial slot: (2*cta + [0 first | 1 last segment of the CTA]) * HG + warp
+        const uint32_t nseg = cc.b - seg_b0 + 1;
+        const bool first_seg = (k + 1 == nseg);
+        float* ps = p.partials + ((2ull * blockIdx.x + (first_seg ? 0 : 1)) * HG + warp) * slot_f;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int q = nt * 8 + 2 * t + c;
+            if (q >= static_cast<int>(p.G)) continue;
+            if (g == 0) {
+              ps[q] = m_run[nt][c];
+              ps[p.G + q] = lf[nt][c];
+            }
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+              const int d0 = vdim<FMT>(mt, g, 0);
+              float2 v;
+              v.x = acc[mt][nt][c] * vscale + zf[nt][c];
+              v.y = acc[mt][nt][2 + c] * vscale + zf[nt][c];
+              *reinterpret_cast<float2*>(ps + slot_hdr + q * kD + d0) = v;
+            }
+          }
+        // one acq_rel RMW publishes this warp's partial (the warp's stores are
+        // ordered before it by __syncwarp) and acquires the other segments'
+        __syncwarp();
+        const uint32_t unit = cc.s * p.H + head;
+        uint32_t old = 0;
+        if (lane == 0 && !(p.debug & 8)) old = atom_add_acq_rel(p.counters + unit, nseg);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (p.trace && lane == 0) t_atom = gtimer();
+        if (old + nseg == cc.nblk) {  // this warp finishes the unit: merge after the loop
+          if (lane == 0) p.counters[unit] = 0;
+          pend_s[npend] = cc.s;
+          pend_g[npend] = cc.h;
+          pend_n[npend] = cc.nblk;
+          ++npend;
         }
-        reinterpret_cast<float4*>(ps + 2 * kNQ + q * kD)[lane] = o4;
       }
     }
-    if (!whole) {
-      __threadfence();
-      cta_bar();
-      if (threadIdx.x == 0) {
-        const uint32_t nseg = segb - flat;
-        const uint32_t old = atomicAdd(p.counters + unit, nseg);
-        const uint32_t last = (old + nseg == cu.nblk) ? 1u : 0u;
-        if (last) p.counters[unit] = 0;
-        s_last = last;
-      }
-      cta_bar();
-      if (s_last && !(p.debug & 2)) {
-        __threadfence();
-        merge_unit<kNQ>(p, pre, C, total, cu.s, cu.h, cu.nblk, warp, lane);
-      }
-    }
-    cta_bar();  // comb / s_last reusable
-    // advance to the next unit
-    flat = segb;
-    if (flat < ce) cursor_seek(cu, pre, p.batch, p.H, flat);
+    cursor_next(cc, pre, p.batch, NG);
+  }
+  // merges of the units this warp completed (at most its first and last
+  // segment), kept out of the streaming loop
+  const uint64_t t_loop = p.trace ? gtimer() : 0;
+  if (npend && !(p.debug & 2)) {
+    fence_acq_rel_gpu();
+    if (p.trace) t_fence = gtimer();
+    for (uint32_t i = 0; i < npend; ++i)
+      merge_dispatch<NT>(p, pre, sp, pend_s[i], pend_g[i], pend_n[i], warp, HG, lane);
+  }
+  if (p.trace && lane == 0) {
+    unsigned long long* tr = p.trace + (static_cast<uint64_t>(blockIdx.x) * 16 + warp) * 6;
+    tr[0] = t_start;
+    tr[1] = t_loop;
+    tr[2] = gtimer();
+    tr[3] = npend;
+    tr[4] = t_atom;
+    tr[5] = t_fence;
   }
 }
 
-template <int FMT, int NT, int STAGES>
+// Ring depth per format: ~150-200 KB in flight per SM with one CTA (HG
+// consumer warps + a producer) per SM.
+template <int FMT, int NT>
 static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t stream) {
   using Gm = Geo<FMT>;
   DecodeParams p = p0;
-  p.stage_bytes = (2 * Gm::kChunk + 2 * Gm::kParam + p.G * kD * 2 + 127) / 128 * 128;
-  const size_t ring = static_cast<size_t>(kDecodeWarps) * STAGES * p.stage_bytes;
-  p.bar_offset = static_cast<uint32_t>(ring);
-  p.comb_offset = (p.bar_offset + kDecodeWarps * STAGES * 8 + 15) / 16 * 16;
-  p.prefix_offset = p.comb_offset + kDecodeWarps * NT * 8 * (kD + 2) * 4;
+  const uint32_t hg_max = NT == 1 ? 8 : 4;
+  uint32_t hg = 1;
+  while (hg * 2 <= hg_max && p.H % (hg * 2) == 0) hg *= 2;
+  p.hg = hg;
+  p.stage_bytes = (2 * hg * (Gm::kChunk + Gm::kParam) + 127) / 128 * 128;
+  const uint32_t qbytes = hg * p.G * kD * 2;
+  const size_t budget = 200 * 1024;
+  uint32_t stages = static_cast<uint32_t>((budget - 2 * qbytes) / p.stage_bytes);
+  if (stages > 16) stages = 16;
+  if (stages < 2) stages = 2;
+  p.stages = stages;
+  p.qbuf_offset = stages * p.stage_bytes;
+  p.bar_offset = (p.qbuf_offset + 2 * qbytes + 15) / 16 * 16;
+  p.prefix_offset = p.bar_offset + (2 * stages + 4) * 8;
   const size_t smem = p.prefix_offset + (p.batch + 1) * 4;
-  auto kern = paged_decode_kernel<FMT, NT, STAGES>;
+  auto kern = paged_decode_kernel<FMT, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
+  const int threads = static_cast<int>((hg + 1) * 32);
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecodeWarps * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  if (per_sm > 2) per_sm = 2;  // workspace partials are sized for <= 2 CTAs per SM
   int grid = per_sm * num_sms;
   if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;
-  kern<<<grid, kDecodeWarps * 32, smem, stream>>>(p);
-  return cudaGetLastError();
-}
-
-// Ring depth per format: enough bytes in flight per SM (~100-200 KB) while
-// leaving room for 3 CTAs (12 warps) per SM.
-template <int FMT, int NT>
-static cudaError_t launch_fmt(const DecodeParams& p, int num_sms, cudaStream_t stream) {
-  if constexpr (FMT == kFP16) return launch_fmt<FMT, NT, 2>(p, num_sms, stream);
-  else if constexpr (FMT == kINT4) return launch_fmt<FMT, NT, 4>(p, num_sms, stream);
-  else return launch_fmt<FMT, NT, 3>(p, num_sms, stream);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 }  // namespace dev
@@ -841,10 +940,10 @@ cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms
 }
 
 size_t decode_partials_bytes(int num_sms, int G) {
-  // upper bound of CTAs in a persistent launch x 2 slots x 16 queries
+  // <= 2 CTAs per SM (smem) x 2 segments x (group heads x G) <= 64 query rows
   (void)G;
-  const size_t ctas = static_cast<size_t>(num_sms) * 16;
-  return ctas * 2 * 16 * (dev::kD + 2) * sizeof(float);
+  const size_t ctas = static_cast<size_t>(num_sms) * 2;
+  return ctas * 2 * 64 * (dev::kD + 4) * sizeof(float);
 }
 
 }  // namespace kvslab

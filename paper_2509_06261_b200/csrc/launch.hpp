@@ -33,9 +33,11 @@ struct DecodeParams {
   float* partials;
   uint32_t* counters;
   // filled by the launcher
-  uint32_t stage_bytes, bar_offset, comb_offset, prefix_offset;
+  uint32_t stage_bytes, bar_offset, qbuf_offset, prefix_offset, hg, stages;
   int max_ctas;  // 0 = persistent full machine
   int debug;     // bit0: skip math, bit1: skip partial merge (probes only)
+  int pdl;       // launch with programmatic stream serialization
+  unsigned long long* trace;  // probes: per-warp globaltimer stamps (nullable)
 };
 
 struct AppendParams {

@@ -27,7 +27,7 @@ for dt in dts:
     sc = torch.ones(16, device="cuda")
     ws = kv.DecodeWorkspace(pool, fmt, B)
     by = fmt.decode_bytes([ctx0] * B)
-    for dbg in (0, 1, 2, 3):
+    for dbg in [int(x) for x in os.environ.get("DBGS", "0,1,2,3").split(",")]:
         os.environ["KVSLAB_DECODE_DEBUG"] = str(dbg)
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
