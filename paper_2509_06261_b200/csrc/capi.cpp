@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -121,6 +122,7 @@ struct ks_pool {
   ks_clock_fn clock_fn = nullptr;
   void* clock_user = nullptr;
   std::vector<uint32_t> dirty;
+  std::map<uint64_t, uint32_t> cta_budget;  // per key: K2 CTAs (SM share), 0 = all
 
   ~ks_pool() {
     if (device >= 0) {
@@ -696,7 +698,7 @@ ks_status ks_paged_decode_workspace_size(const ks_pool* pool, const ks_kv_format
   if (!pool || !fmt || !bytes) return fail(KS_INVALID_ARGUMENT, "null argument");
   const int sms = pool->num_sms > 0 ? pool->num_sms : 148;
   const size_t part = kvslab::decode_partials_bytes(sms, static_cast<int>(fmt->num_q_heads / std::max(1u, fmt->num_kv_heads)));
-  *bytes = part + (static_cast<size_t>(batch) * fmt->num_kv_heads * 4 + 255) / 256 * 256;
+  *bytes = part + (static_cast<size_t>(batch + 1) * 4 + 255) / 256 * 256;
   return KS_OK;
 }
 
@@ -744,10 +746,16 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
       return fail(KS_INVALID_ARGUMENT, "k_new and v_new must both be set or both be null");
     const size_t part = kvslab::decode_partials_bytes(pool->num_sms, static_cast<int>(p.G));
     p.partials = static_cast<float*>(d_workspace);
-    p.counters = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_workspace) + part);
+    p.prefix_out = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_workspace) + part);
     p.max_ctas = 0;
     if (const char* dbg = std::getenv("KVSLAB_DECODE_DEBUG")) p.debug = std::atoi(dbg);
+    {
+      auto it = pool->cta_budget.find(fi.key);
+      if (it != pool->cta_budget.end()) p.max_ctas = static_cast<int>(it->second);
+    }
     if (const char* mc = std::getenv("KVSLAB_DECODE_MAX_CTAS")) p.max_ctas = std::atoi(mc);
+    if (const char* hg = std::getenv("KVSLAB_DECODE_HG")) p.hg_max = static_cast<uint32_t>(std::atoi(hg));
+    if (const char* sb = std::getenv("KVSLAB_DECODE_SMEM")) p.smem_budget = static_cast<uint32_t>(std::atoi(sb));
     p.pdl = 1;
     if (const char* tr = std::getenv("KVSLAB_DECODE_TRACE"))
       p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(tr, nullptr, 0));
@@ -755,7 +763,7 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
     cudaError_t e = kvslab::launch_paged_decode(p, static_cast<int>(fmt->kv_dtype), pool->num_sms,
                                                 static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "paged_decode launch");
-    ++g_launches;
+    g_launches += 2;  // decode + merge
     return KS_OK;
   });
 }
@@ -780,6 +788,16 @@ ks_status ks_paged_decode_append(ks_pool* pool, const ks_kv_format* fmt, uint32_
   return decode_impl(pool, fmt, layer, d_q, d_k_new, d_v_new, d_out, d_lse, d_block_table,
                      bt_stride, d_ctx_lens, batch, sm_scale, d_kv_scales, d_workspace,
                      workspace_bytes, stream);
+}
+
+ks_status ks_set_decode_sm_share(ks_pool* pool, uint64_t key, uint32_t max_ctas) {
+  return guarded([&] {
+    if (!pool) return fail(KS_INVALID_ARGUMENT, "null pool");
+    pool->pool->blocks_per_slab(key);  // InvalidKeyError when unregistered
+    if (max_ctas == 0) pool->cta_budget.erase(key);
+    else pool->cta_budget[key] = max_ctas;
+    return KS_OK;
+  });
 }
 
 ks_status ks_compact_plan(ks_pool* pool, uint64_t key, uint32_t max_moves, ks_block_move* moves,

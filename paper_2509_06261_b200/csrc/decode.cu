@@ -331,34 +331,37 @@ __device__ __forceinline__ uint32_t cta_of(uint32_t f, const CtaSplit& sp) {
   return lo;
 }
 
-// Merge the fp32 partials of one (sequence, head) unit -- run by the warp
-// whose CTA contributes last:  O = sum_j 2^(m_j-M) acc_j / sum_j 2^(m_j-M) l_j.
-// Lanes split (query, dims) with GP = pow2 >= G queries; segments are merged
-// online in batches of SB whose loads are all issued before any is used, so
-// the merge costs ~ceil(nseg / SB) memory round trips.
-template <int GP>
-__device__ __forceinline__ void merge_unit(const DecodeParams& p, const uint32_t* pre,
-                                           const CtaSplit& sp, uint32_t s, uint32_t grp,
-                                           uint32_t nblk, uint32_t hw, uint32_t HG, int lane) {
-  constexpr int LPQ = 32 / GP;   // lanes per query
-  constexpr int DPL = kD / LPQ;  // dims per lane
-  constexpr int F4 = DPL / 4;    // float4 per lane per segment
-  constexpr int SB = F4 >= 24 ? 1 : 24 / F4;  // segments per batch (<= 24 float4 in flight)
-  const uint32_t G = p.G;
-  const uint32_t hdr = (2 * G + 3) & ~3u;  // m[G], l[G], padded to 16 B
-  const uint32_t slot_f = hdr + G * kD;
+// ------------------------------------------------------------ merge kernel
+// Combines the fp32 partials of every (sequence, head) unit that the decode
+// kernel's CTA ranges cut:  O = sum_j 2^(m_j-M) acc_j / sum_j 2^(m_j-M) l_j.
+// One CTA per unit, one warp per query, 4 dims per lane; all segment loads of
+// a pass are issued before use.  Launched right behind the decode kernel with
+// programmatic dependent launch, so it is resident when the decode grid ends.
+__global__ void __launch_bounds__(512) merge_kernel(const DecodeParams p, uint32_t C) {
+  pdl_launch_dependents();
+  const uint32_t unit = blockIdx.x;
+  const uint32_t s = unit / p.H, h = unit % p.H;
+  const uint32_t HG = p.hg, NG = p.H / p.hg, grp = h / HG, hw = h % HG;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();  // partials and the prefix come from the decode kernel
+  const uint32_t* pre = p.prefix_out;
+  const uint32_t total = pre[p.batch];
+  const uint32_t nblk = (pre[s + 1] - pre[s]) / NG;
+  if (nblk == 0 || warp >= static_cast<int>(p.G)) return;
+  const CtaSplit sp = make_split(total, C);
   const uint32_t U0 = pre[s] + grp * nblk;
   const uint32_t ca = cta_of(U0, sp), cb = cta_of(U0 + nblk - 1, sp);
-  const int q = lane / LPQ, sub = lane % LPQ;
-  if (q >= static_cast<int>(G)) return;
+  if (ca == cb) return;  // whole unit: the decode kernel wrote it
+  const uint32_t G = p.G, q = warp;
+  const uint32_t hdr = (2 * G + 3) & ~3u;
+  const uint32_t slot_f = hdr + G * kD;
+  constexpr int SB = 16;
   float M = -INFINITY, L = 0.f;
-  float acc[DPL];
-#pragma unroll
-  for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
+  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t c_lo = cta_start(ca, sp);
   for (uint32_t c0 = ca; c0 <= cb; c0 += SB) {
     float mv[SB], lv[SB];
-    float4 av[SB][F4];
+    float4 av[SB];
 #pragma unroll
     for (int j = 0; j < SB; ++j) {
       const uint32_t c = c0 + j;
@@ -368,50 +371,31 @@ __device__ __forceinline__ void merge_unit(const DecodeParams& p, const uint32_t
           p.partials + ((2ull * c + (c_lo < U0 ? 1 : 0)) * HG + hw) * static_cast<uint64_t>(slot_f);
       mv[j] = valid ? __ldcg(pp + q) : -INFINITY;
       lv[j] = valid ? __ldcg(pp + G + q) : 0.f;
-      const float4* src = reinterpret_cast<const float4*>(pp + hdr + q * kD + sub * DPL);
-#pragma unroll
-      for (int i = 0; i < F4; ++i) av[j][i] = valid ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      av[j] = valid ? __ldcg(reinterpret_cast<const float4*>(pp + hdr + q * kD) + lane)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
       c_lo = c_hi;
     }
     float Mb = M;
 #pragma unroll
     for (int j = 0; j < SB; ++j) Mb = fmaxf(Mb, mv[j]);
-    const float a = ex2(M - Mb);  // 0 when M == -inf
+    const float a = ex2(M - Mb);
     L *= a;
-#pragma unroll
-    for (int i = 0; i < DPL; ++i) acc[i] *= a;
+    o.x *= a; o.y *= a; o.z *= a; o.w *= a;
 #pragma unroll
     for (int j = 0; j < SB; ++j) {
-      const float f = ex2(mv[j] - Mb);  // 0 for invalid segments
+      const float f = ex2(mv[j] - Mb);
       L += f * lv[j];
-#pragma unroll
-      for (int i = 0; i < F4; ++i) {
-        acc[4 * i] += f * av[j][i].x; acc[4 * i + 1] += f * av[j][i].y;
-        acc[4 * i + 2] += f * av[j][i].z; acc[4 * i + 3] += f * av[j][i].w;
-      }
+      o.x += f * av[j].x; o.y += f * av[j].y; o.z += f * av[j].z; o.w += f * av[j].w;
     }
     M = Mb;
   }
   const uint32_t Hq = p.H * G;
-  const uint32_t head = grp * HG + hw;
   const float inv = 1.f / L;
-  __half* orow = p.out + (static_cast<uint64_t>(s) * Hq + head * G + q) * kD + sub * DPL;
-#pragma unroll
-  for (int i = 0; i < DPL; i += 2)
-    *reinterpret_cast<__half2*>(orow + i) = __floats2half2_rn(acc[i] * inv, acc[i + 1] * inv);
-  if (p.lse && sub == 0)
-    p.lse[static_cast<uint64_t>(s) * Hq + head * G + q] = (M + __log2f(L)) * 0.69314718055994531f;
-}
-
-template <int NT>
-__device__ __forceinline__ void merge_dispatch(const DecodeParams& p, const uint32_t* pre,
-                                               const CtaSplit& sp, uint32_t s, uint32_t grp,
-                                               uint32_t nblk, uint32_t hw, uint32_t HG, int lane) {
-  if (p.G <= 1) merge_unit<1>(p, pre, sp, s, grp, nblk, hw, HG, lane);
-  else if (p.G <= 2) merge_unit<2>(p, pre, sp, s, grp, nblk, hw, HG, lane);
-  else if (p.G <= 4) merge_unit<4>(p, pre, sp, s, grp, nblk, hw, HG, lane);
-  else if (p.G <= 8) merge_unit<8>(p, pre, sp, s, grp, nblk, hw, HG, lane);
-  else if constexpr (NT == 2) merge_unit<16>(p, pre, sp, s, grp, nblk, hw, HG, lane);
+  __half* orow = p.out + (static_cast<uint64_t>(s) * Hq + h * G + q) * kD + 4 * lane;
+  *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(o.x * inv, o.y * inv);
+  *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(o.z * inv, o.w * inv);
+  if (p.lse && lane == 0)
+    p.lse[static_cast<uint64_t>(s) * Hq + h * G + q] = (M + __log2f(L)) * 0.69314718055994531f;
 }
 
 // ------------------------------------------------------------------ kernel
@@ -438,7 +422,6 @@ paged_decode_kernel(const DecodeParams p) {
   // PDL-enabled predecessor writes (ctx_lens, block tables, KV of other
   // layers); Q, new K/V, outputs and the workspace come after the wait.
   pdl_launch_dependents();
-  const uint64_t t_start = p.trace ? gtimer() : 0;
 
   // ---- per-CTA prefix of blocks over sequences (x NG head groups) ----
   uint32_t* pre = reinterpret_cast<uint32_t*>(smem + p.prefix_offset);
@@ -488,9 +471,12 @@ paged_decode_kernel(const DecodeParams p) {
   __syncthreads();
   const uint32_t total = pre[p.batch];
 
-  // CTA 0 writes empty outputs for sequences with no context.
+  // CTA 0 publishes the prefix for the merge kernel and writes empty outputs
+  // for sequences with no context (both after the predecessor finished).
   if (blockIdx.x == 0) {
-    bool waited = false;
+    pdl_wait();
+    for (uint32_t s = threadIdx.x; s <= p.batch; s += blockDim.x) p.prefix_out[s] = pre[s];
+    bool waited = true;
     for (uint32_t s = threadIdx.x; s < p.batch; s += blockDim.x) {
       if (pre[s + 1] != pre[s]) continue;
       if (!waited) {
@@ -613,8 +599,6 @@ paged_decode_kernel(const DecodeParams p) {
   int ctx_cur = 0;
   Cursor cc;
   cursor_seek(cc, pre, p.batch, NG, cs);
-  uint32_t pend_s[2], pend_g[2], pend_n[2], npend = 0;
-  uint64_t t_atom = 0, t_fence = 0;
   const uint32_t slot_hdr = (2 * p.G + 3) & ~3u;  // m[G], l[G], padded to 16 B
   const uint32_t slot_f = slot_hdr + p.G * kD;
 
@@ -839,42 +823,9 @@ paged_decode_kernel(const DecodeParams p) {
               *reinterpret_cast<float2*>(ps + slot_hdr + q * kD + d0) = v;
             }
           }
-        // one acq_rel RMW publishes this warp's partial (the warp's stores are
-        // ordered before it by __syncwarp) and acquires the other segments'
-        __syncwarp();
-        const uint32_t unit = cc.s * p.H + head;
-        uint32_t old = 0;
-        if (lane == 0 && !(p.debug & 8)) old = atom_add_acq_rel(p.counters + unit, nseg);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        if (p.trace && lane == 0) t_atom = gtimer();
-        if (old + nseg == cc.nblk) {  // this warp finishes the unit: merge after the loop
-          if (lane == 0) p.counters[unit] = 0;
-          pend_s[npend] = cc.s;
-          pend_g[npend] = cc.h;
-          pend_n[npend] = cc.nblk;
-          ++npend;
-        }
       }
     }
     cursor_next(cc, pre, p.batch, NG);
-  }
-  // merges of the units this warp completed (at most its first and last
-  // segment), kept out of the streaming loop
-  const uint64_t t_loop = p.trace ? gtimer() : 0;
-  if (npend && !(p.debug & 2)) {
-    fence_acq_rel_gpu();
-    if (p.trace) t_fence = gtimer();
-    for (uint32_t i = 0; i < npend; ++i)
-      merge_dispatch<NT>(p, pre, sp, pend_s[i], pend_g[i], pend_n[i], warp, HG, lane);
-  }
-  if (p.trace && lane == 0) {
-    unsigned long long* tr = p.trace + (static_cast<uint64_t>(blockIdx.x) * 16 + warp) * 6;
-    tr[0] = t_start;
-    tr[1] = t_loop;
-    tr[2] = gtimer();
-    tr[3] = npend;
-    tr[4] = t_atom;
-    tr[5] = t_fence;
   }
 }
 
@@ -884,14 +835,16 @@ template <int FMT, int NT>
 static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t stream) {
   using Gm = Geo<FMT>;
   DecodeParams p = p0;
-  const uint32_t hg_max = NT == 1 ? 8 : 4;
+  uint32_t hg_max = NT == 1 ? 8 : 4;
+  if (p.hg_max > 0 && p.hg_max < hg_max) hg_max = p.hg_max;
   uint32_t hg = 1;
   while (hg * 2 <= hg_max && p.H % (hg * 2) == 0) hg *= 2;
   p.hg = hg;
   p.stage_bytes = (2 * hg * (Gm::kChunk + Gm::kParam) + 127) / 128 * 128;
   const uint32_t qbytes = hg * p.G * kD * 2;
-  const size_t budget = 200 * 1024;
-  uint32_t stages = static_cast<uint32_t>((budget - 2 * qbytes) / p.stage_bytes);
+  const size_t budget = p.smem_budget > 0 ? p.smem_budget
+                                          : 224 * 1024 - (p.batch + 1) * 4 - 2 * qbytes - 512;
+  uint32_t stages = static_cast<uint32_t>(budget / p.stage_bytes);
   if (stages > 16) stages = 16;
   if (stages < 2) stages = 2;
   p.stages = stages;
@@ -921,7 +874,14 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   attr[0].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, p);
+  e = cudaLaunchKernelEx(&cfg, kern, p);
+  if (e != cudaSuccess) return e;
+  // merge the partials of units cut by CTA ranges (early-exits otherwise)
+  cudaLaunchConfig_t mcfg = cfg;
+  mcfg.gridDim = dim3(p.batch * p.H);
+  mcfg.blockDim = dim3(p.G * 32);
+  mcfg.dynamicSmemBytes = 0;
+  return cudaLaunchKernelEx(&mcfg, merge_kernel, p, static_cast<uint32_t>(grid));
 }
 
 }  // namespace dev

@@ -31,10 +31,12 @@ struct DecodeParams {
   uint32_t params_off;     // 2*H*chunk: quant params inside a layer sub-block
   bool fp8_inblock;
   float* partials;
-  uint32_t* counters;
+  uint32_t* prefix_out;  // [batch+1] block prefix published for the merge kernel
   // filled by the launcher
   uint32_t stage_bytes, bar_offset, qbuf_offset, prefix_offset, hg, stages;
   int max_ctas;  // 0 = persistent full machine
+  uint32_t hg_max;        // 0 = default head-group size
+  uint32_t smem_budget;   // ring bytes per CTA; 0 = default
   int debug;     // bit0: skip math, bit1: skip partial merge (probes only)
   int pdl;       // launch with programmatic stream serialization
   unsigned long long* trace;  // probes: per-warp globaltimer stamps (nullable)

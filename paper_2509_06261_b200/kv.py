@@ -245,6 +245,11 @@ def compact(pool: SlabPool, key: int, max_moves: int = 1 << 20,
     return moves, freed
 
 
+def set_decode_sm_share(pool: SlabPool, key: int, max_ctas: int) -> None:
+    """Cap the K2 grid of the model with this slab key (MPS-style SM share)."""
+    check(L.lib.ks_set_decode_sm_share(pool.handle, key, max_ctas))
+
+
 def launch_count() -> int:
     return L.lib.ks_launch_count()
 
