@@ -312,30 +312,47 @@ def run_ours():
             kv.kv_append(pool, m.fmt, layer, torch.roll(kpre, layer, 0), vpre, ts, tp, m.table,
                          kv_scales)
     torch.cuda.synchronize()
-    # per-step device inputs (resident): Q per layer/model, new K/V, positions
-    q = [[torch.randn(B, HQ, D, dtype=torch.float16, device=dev) for _ in range(L)]
-         for _ in models]
-    knew = [torch.randn(B, HKV, D, dtype=torch.float16, device=dev) for _ in models]
-    vnew = [torch.randn(B, HKV, D, dtype=torch.float16, device=dev) for _ in models]
-    out = [[torch.empty(B, HQ, D, dtype=torch.float16, device=dev) for _ in range(L)]
-           for _ in models]
+    # per-step device inputs (resident): Q per layer/model, new K/V.  Two
+    # buffer sets (flat, so the e2e leg moves each step with one H2D and one
+    # D2H copy) let the e2e leg overlap copies of step k+1 with compute of k.
+    per_in = L * B * HQ * D + 2 * B * HKV * D
+    per_out = L * B * HQ * D
+
+    def make_set():
+        inbuf = torch.randn(2 * per_in, dtype=torch.float16, device=dev)
+        outbuf = torch.empty(2 * per_out, dtype=torch.float16, device=dev)
+        qv, kv_, vv, ov = [], [], [], []
+        for mi in range(2):
+            base = inbuf[mi * per_in:(mi + 1) * per_in]
+            qv.append([base[l * B * HQ * D:(l + 1) * B * HQ * D].view(B, HQ, D) for l in range(L)])
+            off = L * B * HQ * D
+            kv_.append(base[off:off + B * HKV * D].view(B, HKV, D))
+            vv.append(base[off + B * HKV * D:off + 2 * B * HKV * D].view(B, HKV, D))
+            ob = outbuf[mi * per_out:(mi + 1) * per_out]
+            ov.append([ob[l * B * HQ * D:(l + 1) * B * HQ * D].view(B, HQ, D) for l in range(L)])
+        return dict(inbuf=inbuf, outbuf=outbuf, q=qv, knew=kv_, vnew=vv, out=ov)
+
+    sets = [make_set(), make_set()]
+    q, knew, vnew, out = sets[0]["q"], sets[0]["knew"], sets[0]["vnew"], sets[0]["out"]
     seqs = torch.arange(B, dtype=torch.int32, device=dev)
     ctxd = torch.full((B,), ctx0 + 1, dtype=torch.int32, device=dev)  # includes the new token
     ws = [kv.DecodeWorkspace(pool, f, B) for f in fmts]
 
     side = torch.cuda.Stream()
 
-    def device_step():
+    def device_step(bs=None):
         # the two co-located models run on their own streams (FineServe shares
         # the GPU spatially between co-located engines); per layer one fused
         # K1+K2 launch per model
+        bs = sets[0] if bs is None else bs
         main = torch.cuda.current_stream()
         side.wait_stream(main)
         for layer in range(L):
             for mi, m in enumerate(models):
-                kv.paged_decode(pool, m.fmt, layer, q[mi][layer], m.table, ctxd,
-                                out=out[mi][layer], kv_scales=kv_scales, workspace=ws[mi],
-                                k_new=knew[mi], v_new=vnew[mi], stream=main if mi == 0 else side)
+                kv.paged_decode(pool, m.fmt, layer, bs["q"][mi][layer], m.table, ctxd,
+                                out=bs["out"][mi][layer], kv_scales=kv_scales, workspace=ws[mi],
+                                k_new=bs["knew"][mi], v_new=bs["vnew"][mi],
+                                stream=main if mi == 0 else side)
         main.wait_stream(side)
         ctxd.add_(1)
 
@@ -415,6 +432,12 @@ def run_ours():
             device_step()
     torch.cuda.current_stream().wait_stream(s_cap)
     per_graph = kv.launch_count() - n0
+    g_b = torch.cuda.CUDAGraph()  # same step over buffer set 1 (e2e leg)
+    with torch.cuda.stream(s_cap):
+        with torch.cuda.graph(g_b, stream=s_cap):
+            device_step(sets[1])
+    torch.cuda.current_stream().wait_stream(s_cap)
+    graphs = [g, g_b]
     # the capture advanced nothing on device (graph not yet replayed); the eager
     # warm step advanced pos/ctx by one: keep host mirror consistent
     torch.cuda.synchronize()
@@ -442,30 +465,48 @@ def run_ours():
     table_launches = kv.launch_count() - n_tab0
     gpu_launches = per_graph * ARGS.steps + table_launches
 
-    # e2e through the public API with host buffers (pinned), copies timed
-    hq = [[t.cpu().pin_memory() for t in qq] for qq in q]
-    hk = [t.cpu().pin_memory() for t in knew]
-    hv = [t.cpu().pin_memory() for t in vnew]
-    ho = [[torch.empty_like(t, device="cpu").pin_memory() for t in oo] for oo in out]
-    h2d = sum(t.numel() * 2 for qq in hq for t in qq) + sum(t.numel() * 2 for t in hk + hv)
-    d2h = sum(t.numel() * 2 for oo in ho for t in oo)
+    # e2e through the public API with host buffers (pinned): every step's
+    # Q/new K/V come from host memory and every output goes back; copies run
+    # on a copy stream, double-buffered against compute (step k+1's inputs
+    # and step k-1's outputs move while step k computes).  Timed on device.
+    hin = [torch.empty(2 * per_in, dtype=torch.float16).pin_memory() for _ in range(2)]
+    hout = [torch.empty(2 * per_out, dtype=torch.float16).pin_memory() for _ in range(2)]
+    for h in hin:
+        h.copy_(sets[0]["inbuf"].cpu())
+    h2d, d2h = 2 * per_in * 2, 2 * per_out * 2
+    cstream = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_out = [torch.cuda.Event(), torch.cuda.Event()]
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_bytes = 0
-    e2e_steps = max(3, ARGS.steps // 2)
+    e2e_steps = max(4, ARGS.steps)
     torch.cuda.synchronize()
     e2.record(stream)
-    for _ in range(e2e_steps):
+    cstream.wait_stream(stream)
+    with torch.cuda.stream(cstream):  # inputs of step 0
+        sets[0]["inbuf"].copy_(hin[0], non_blocking=True)
+        ev_in[0].record(cstream)
+    for k in range(e2e_steps):
+        X = k & 1
         host_step()
         e2e_bytes += step_bytes()
-        for mi in range(2):
-            knew[mi].copy_(hk[mi], non_blocking=True)
-            vnew[mi].copy_(hv[mi], non_blocking=True)
-            for layer in range(L):
-                q[mi][layer].copy_(hq[mi][layer], non_blocking=True)
-        g.replay()
-        for mi in range(2):
-            for layer in range(L):
-                ho[mi][layer].copy_(out[mi][layer], non_blocking=True)
+        if k + 1 < e2e_steps:  # prefetch step k+1 into the other set once step k-1 is done
+            Y = X ^ 1
+            with torch.cuda.stream(cstream):
+                if k >= 1:
+                    cstream.wait_event(ev_out[Y])
+                    sets[Y]["outbuf"].view(-1)  # outputs of step k-1 leave first
+                    hout[Y].copy_(sets[Y]["outbuf"], non_blocking=True)
+                sets[Y]["inbuf"].copy_(hin[Y], non_blocking=True)
+                ev_in[Y].record(cstream)
+        stream.wait_event(ev_in[X])
+        graphs[X].replay()
+        ev_out[X].record(stream)
+    with torch.cuda.stream(cstream):  # last outputs
+        X = (e2e_steps - 1) & 1
+        cstream.wait_event(ev_out[X])
+        hout[X].copy_(sets[X]["outbuf"], non_blocking=True)
+    stream.wait_stream(cstream)
     e3.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e2.elapsed_time(e3)

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(512) merge_kernel(const DecodeParams p, uint32
   const uint32_t G = p.G, q = warp;
   const uint32_t hdr = (2 * G + 3) & ~3u;
   const uint32_t slot_f = hdr + G * kD;
-  constexpr int SB = 16;
+  constexpr int SB = 8;
   float M = -INFINITY, L = 0.f;
   float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t c_lo = cta_start(ca, sp);
@@ -530,37 +530,7 @@ paged_decode_kernel(const DecodeParams p) {
       const uint8_t* blk = p.pool + block_offset(p.geom, static_cast<uint32_t>(ent)) + p.layer_off;
       const bool first_of_unit = (k == 0) || (pc.b == 0);
       mbar_wait(&empty[st], ph ^ 1);
-      if (p.k_new != nullptr && pc.b == pc.nblk - 1) {
-        // Fused K1: this block holds the new token (position ctx-1) of every
-        // head of the group.  Quantise + store it, then order the generic
-        // writes before the bulk (async-proxy) copy that reads the block.
-        if (!dep_ready) {
-          pdl_wait();
-          dep_ready = true;
-        }
-        uint8_t* wblk = const_cast<uint8_t*>(blk);
-        const uint32_t slot = static_cast<uint32_t>(p.ctx_lens[pc.s] - 1) % kTPB;
-        for (uint32_t hh = 0; hh < HG; ++hh) {
-          const uint32_t h = g0 + hh;
-          const uint64_t row = (static_cast<uint64_t>(pc.s) * p.H + h) * kD + lane * 4;
-          const uint2 rk = *reinterpret_cast<const uint2*>(p.k_new + row);
-          const uint2 rv = *reinterpret_cast<const uint2*>(p.v_new + row);
-          const float sck = (FMT == kFP8 && p.kv_scales) ? p.kv_scales[h] : 1.0f;
-          const float scv = (FMT == kFP8 && p.kv_scales) ? p.kv_scales[p.H + h] : 1.0f;
-          store_row<FMT>(wblk + static_cast<uint64_t>(h) * Gm::kChunk, wblk + p.params_off, slot,
-                         0, h, p.H, kTPB, rk, sck, p.fp8_inblock, lane);
-          store_row<FMT>(wblk + static_cast<uint64_t>(p.H + h) * Gm::kChunk, wblk + p.params_off,
-                         slot, 1, h, p.H, kTPB, rv, scv, p.fp8_inblock, lane);
-        }
-        fence_proxy_async_global();
-        __syncwarp();
-      }
-      if (first_of_unit && !dep_ready) {  // Q comes from the predecessor
-        pdl_wait();
-        dep_ready = true;
-      }
       if (lane == 0) {
-        if (p.k_new != nullptr) fence_proxy_async_global();
         uint8_t* sb = ring + static_cast<size_t>(st) * p.stage_bytes;
         mbar_expect_tx(&full[st], 2 * kvq + 2 * pq);
         bulk_g2s(sb, blk + static_cast<uint64_t>(g0) * Gm::kChunk, kvq, &full[st], pol);
@@ -571,6 +541,12 @@ paged_decode_kernel(const DecodeParams p) {
           bulk_g2s(sb + 2 * kvq + pq, prm + static_cast<uint64_t>(p.H + g0) * Gm::kParam, pq,
                    &full[st], pol);
         }
+      }
+      if (first_of_unit && !dep_ready) {  // Q comes from the predecessor
+        pdl_wait();
+        dep_ready = true;
+      }
+      if (lane == 0) {
         if (first_of_unit) {
           const uint32_t qs = ui & 1;
           mbar_wait(&qempty[qs], ((ui >> 1) & 1) ^ 1);
@@ -599,6 +575,8 @@ paged_decode_kernel(const DecodeParams p) {
   int ctx_cur = 0;
   Cursor cc;
   cursor_seek(cc, pre, p.batch, NG, cs);
+  uint2 new_k = make_uint2(0, 0), new_v = make_uint2(0, 0);
+  int32_t new_gid = 0;
   const uint32_t slot_hdr = (2 * p.G + 3) & ~3u;  // m[G], l[G], padded to 16 B
   const uint32_t slot_f = slot_hdr + p.G * kD;
 
@@ -640,9 +618,38 @@ paged_decode_kernel(const DecodeParams p) {
           vscale = p.kv_scales[p.H + head];
         }
       }
+      // fused K1: if this CTA range reaches the unit's last block, fetch the
+      // new token's K/V row now so the load latency is hidden
+      if (p.k_new != nullptr && k + (cc.nblk - 1 - cc.b) < n) {
+        const uint64_t row = (static_cast<uint64_t>(cc.s) * p.H + head) * kD + lane * 4;
+        new_k = __ldg(reinterpret_cast<const uint2*>(p.k_new + row));
+        new_v = __ldg(reinterpret_cast<const uint2*>(p.v_new + row));
+        new_gid = __ldg(p.block_table + static_cast<uint64_t>(cc.s) * p.bt_stride + cc.nblk - 1);
+      }
     }
 
     mbar_wait(&full[st], ph);
+    if (p.k_new != nullptr && cc.b == cc.nblk - 1) {
+      // Fused K1: the block holding the new token (position ctx-1) was copied
+      // before the token existed.  Quantise it once (store_row, bit-identical
+      // to K1), write it to its slab block in HBM, and patch the staged copy
+      // in shared memory so this step's attention includes it.
+      uint8_t* gblk = const_cast<uint8_t*>(p.pool) +
+                      block_offset(p.geom, static_cast<uint32_t>(new_gid)) + p.layer_off;
+      const uint32_t slot = static_cast<uint32_t>(ctx_cur - 1) % kTPB;
+      const float sck = (FMT == kFP8 && p.kv_scales) ? kscale : 1.0f;
+      const float scv = (FMT == kFP8 && p.kv_scales) ? vscale : 1.0f;
+      store_row<FMT>(gblk + static_cast<uint64_t>(head) * Gm::kChunk, gblk + p.params_off, slot, 0,
+                     head, p.H, kTPB, new_k, sck, p.fp8_inblock, lane);
+      store_row<FMT>(gblk + static_cast<uint64_t>(p.H + head) * Gm::kChunk, gblk + p.params_off,
+                     slot, 1, head, p.H, kTPB, new_v, scv, p.fp8_inblock, lane);
+      uint8_t* sst = ring + static_cast<size_t>(st) * p.stage_bytes;
+      uint8_t* sprm = sst + 2 * kvq;  // [K params x HG][V params x HG]
+      store_row<FMT>(sst + warp * Gm::kChunk, sprm, slot, 0, warp, HG, kTPB, new_k, sck, false, lane);
+      store_row<FMT>(sst + kvq + warp * Gm::kChunk, sprm, slot, 1, warp, HG, kTPB, new_v, scv, false,
+                     lane);
+      __syncwarp();
+    }
     const uint32_t sb = smem_u32(ring + static_cast<size_t>(st) * p.stage_bytes);
     const uint32_t sK = sb + warp * Gm::kChunk, sV = sb + kvq + warp * Gm::kChunk;
     const uint32_t sKp = sb + 2 * kvq + warp * Gm::kParam, sVp = sb + 2 * kvq + pq + warp * Gm::kParam;
