@@ -63,6 +63,24 @@ class SlabModel:
         self.handles[seq] = []
         self.cached[seq] = 0
 
+    def compact(self, max_moves: int = 1 << 20, stream=None):
+        """K3 for this model's key: moves blocks out of the least-occupied
+        slabs (freeing them for any key), rewrites the device table and the
+        host handles.  Returns (moves, slabs_freed)."""
+        self.sync(stream)
+        moves, freed = kv.compact(self.pool, self.key, max_moves, tables=[self.table],
+                                  stream=stream)
+        if moves:
+            bps = self.pool.blocks_per_slab(self.key)
+            remap = dict(moves)
+            for hs in self.handles:
+                for i, h in enumerate(hs):
+                    dst = remap.get(h.global_block_id)
+                    if dst is not None:
+                        sl, lo = SlabPool.split_global_block_id(dst, bps)
+                        hs[i] = BlockHandle(sl, lo, dst, self.key)
+        return moves, freed
+
     def sync(self, stream=None) -> int:
         """Uploads pending table entries; returns how many were written."""
         n = len(self._pending)
