@@ -41,6 +41,10 @@ struct Geo {
   static constexpr int kRow = kD * Fmt<FMT>::kBits / 8;  // bytes per token row
   static constexpr int kChunk = kTPB * kRow;              // bytes per (K|V, head) chunk
   static constexpr int kParam = FMT == kINT8 ? kTPB * 2 : (FMT == kINT4 ? kTPB * 4 : 0);
+  // integer formats enter the MMA as exact fp16 (q + kBias); the bias is
+  // removed from the 16x8 score tile (kBias * sum(q)) and from O (kBias * sum(p'))
+  static constexpr float kBias = FMT == kINT8 ? 1152.f : (FMT == kINT4 ? 1024.f : 0.f);
+  static constexpr bool kBiased = FMT == kINT8 || FMT == kINT4;
 };
 
 // ------------------------------------------------------------------ cursor
@@ -160,10 +164,11 @@ __device__ __forceinline__ void load_k_frags(uint32_t sK, const FragOff& o, uint
           r[3] = e4m3x2_to_f16x2(static_cast<uint16_t>(wh[e] >> 16));
         } else {
           const uint32_t xl = wl[e] ^ 0x80808080u, xh = wh[e] ^ 0x80808080u;
-          r[0] = hsub2_u32(__byte_perm(xl, 0x64646464u, 0x4140), 0x64806480u);
-          r[2] = hsub2_u32(__byte_perm(xl, 0x64646464u, 0x4342), 0x64806480u);
-          r[1] = hsub2_u32(__byte_perm(xh, 0x64646464u, 0x4140), 0x64806480u);
-          r[3] = hsub2_u32(__byte_perm(xh, 0x64646464u, 0x4342), 0x64806480u);
+          // exact fp16 b + 1152 (the bias is removed after the MMA)
+          r[0] = __byte_perm(xl, 0x64646464u, 0x4140);
+          r[2] = __byte_perm(xl, 0x64646464u, 0x4342);
+          r[1] = __byte_perm(xh, 0x64646464u, 0x4140);
+          r[3] = __byte_perm(xh, 0x64646464u, 0x4342);
         }
       }
     }
@@ -177,10 +182,11 @@ __device__ __forceinline__ void load_k_frags(uint32_t sK, const FragOff& o, uint
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         uint32_t* r = a[2 * i + e];
-        r[0] = hsub2_u32(lop3_and_or(wl[i] >> (8 * e), 0x000F000Fu, 0x64006400u), 0x64006400u);
-        r[2] = hsub2_u32(lop3_and_or(wl[i] >> (8 * e + 4), 0x000F000Fu, 0x64006400u), 0x64006400u);
-        r[1] = hsub2_u32(lop3_and_or(wh[i] >> (8 * e), 0x000F000Fu, 0x64006400u), 0x64006400u);
-        r[3] = hsub2_u32(lop3_and_or(wh[i] >> (8 * e + 4), 0x000F000Fu, 0x64006400u), 0x64006400u);
+        // exact fp16 n + 1024 (the bias is removed after the MMA)
+        r[0] = lop3_and_or(wl[i] >> (8 * e), 0x000F000Fu, 0x64006400u);
+        r[2] = lop3_and_or(wl[i] >> (8 * e + 4), 0x000F000Fu, 0x64006400u);
+        r[1] = lop3_and_or(wh[i] >> (8 * e), 0x000F000Fu, 0x64006400u);
+        r[3] = lop3_and_or(wh[i] >> (8 * e + 4), 0x000F000Fu, 0x64006400u);
       }
     }
   }
@@ -268,10 +274,10 @@ __device__ __forceinline__ void load_v_frags(uint32_t sV, const FragOff& o, uint
         } else {
           const uint32_t ab = __byte_perm(A[j] ^ 0x80808080u, B[j] ^ 0x80808080u, sel);
           const uint32_t cd = __byte_perm(C[j] ^ 0x80808080u, Dd[j] ^ 0x80808080u, sel);
-          r[0] = hsub2_u32(__byte_perm(ab, 0x64646464u, 0x4140), 0x64806480u);
-          r[1] = hsub2_u32(__byte_perm(ab, 0x64646464u, 0x4342), 0x64806480u);
-          r[2] = hsub2_u32(__byte_perm(cd, 0x64646464u, 0x4140), 0x64806480u);
-          r[3] = hsub2_u32(__byte_perm(cd, 0x64646464u, 0x4342), 0x64806480u);
+          r[0] = __byte_perm(ab, 0x64646464u, 0x4140);
+          r[1] = __byte_perm(ab, 0x64646464u, 0x4342);
+          r[2] = __byte_perm(cd, 0x64646464u, 0x4140);
+          r[3] = __byte_perm(cd, 0x64646464u, 0x4342);
         }
       }
     }
@@ -290,10 +296,10 @@ __device__ __forceinline__ void load_v_frags(uint32_t sV, const FragOff& o, uint
       const uint32_t ab = __byte_perm(A[w], B[w], sel);
       const uint32_t cd = __byte_perm(C[w], Dd[w], sel);
       uint32_t* r = a[i];
-      r[0] = hsub2_u32(lop3_and_or(ab, 0x000F000Fu, 0x64006400u), 0x64006400u);
-      r[1] = hsub2_u32(lop3_and_or(ab >> 4, 0x000F000Fu, 0x64006400u), 0x64006400u);
-      r[2] = hsub2_u32(lop3_and_or(cd, 0x000F000Fu, 0x64006400u), 0x64006400u);
-      r[3] = hsub2_u32(lop3_and_or(cd >> 4, 0x000F000Fu, 0x64006400u), 0x64006400u);
+      r[0] = lop3_and_or(ab, 0x000F000Fu, 0x64006400u);
+      r[1] = lop3_and_or(ab >> 4, 0x000F000Fu, 0x64006400u);
+      r[2] = lop3_and_or(cd, 0x000F000Fu, 0x64006400u);
+      r[3] = lop3_and_or(cd >> 4, 0x000F000Fu, 0x64006400u);
     }
   }
 }
@@ -593,7 +599,7 @@ paged_decode_kernel(const DecodeParams p) {
       ++ui;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        if constexpr (FMT == kINT4) {
+        if constexpr (Gm::kBiased) {
           float qsm = 0.f;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
@@ -700,8 +706,11 @@ paged_decode_kernel(const DecodeParams p) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int r = e >> 1, tok = g + 8 * r;
-          float x = sacc[nt][e] * sk[r];
-          if constexpr (FMT == kINT4) x += zk[r] * qsum[nt][e & 1];
+          float x;
+          if constexpr (Gm::kBiased)  // s * (dot' - bias*sum(q)) + z * sum(q)
+            x = sk[r] * (sacc[nt][e] - Gm::kBias * qsum[nt][e & 1]) + zk[r] * qsum[nt][e & 1];
+          else
+            x = sacc[nt][e] * sk[r];
           x *= p.sm_scale_log2;
           sc[e] = tok < valid ? x : -INFINITY;
         }
@@ -737,13 +746,18 @@ paged_decode_kernel(const DecodeParams p) {
         float pr[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[e] - m_run[nt][e & 1]);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          l_run[nt][c] += pr[c] + pr[c + 2];
-          if constexpr (FMT == kINT4) z_run[nt][c] += pr[c] * zv[0] + pr[c + 2] * zv[1];
-        }
         const uint32_t plo = pack_h2(pr[0] * sv[0], pr[1] * sv[0]);
         const uint32_t phi = pack_h2(pr[2] * sv[1], pr[3] * sv[1]);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) l_run[nt][c] += pr[c] + pr[c + 2];
+        if constexpr (Gm::kBiased) {
+          // z_run collects the additive terms of O: sum p*z_v (INT4) minus
+          // bias * sum p' over the exact fp16 P' fed to the MMA
+          const float2 flo = __half22float2(*reinterpret_cast<const __half2*>(&plo));
+          const float2 fhi = __half22float2(*reinterpret_cast<const __half2*>(&phi));
+          z_run[nt][0] += pr[0] * zv[0] + pr[2] * zv[1] - Gm::kBias * (flo.x + fhi.x);
+          z_run[nt][1] += pr[1] * zv[0] + pr[3] * zv[1] - Gm::kBias * (flo.y + fhi.y);
+        }
         const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
         const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
         const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
@@ -778,7 +792,7 @@ paged_decode_kernel(const DecodeParams p) {
           l += __shfl_xor_sync(0xffffffffu, l, 4);
           l += __shfl_xor_sync(0xffffffffu, l, 8);
           l += __shfl_xor_sync(0xffffffffu, l, 16);
-          if constexpr (FMT == kINT4) {
+          if constexpr (Gm::kBiased) {
             z += __shfl_xor_sync(0xffffffffu, z, 4);
             z += __shfl_xor_sync(0xffffffffu, z, 8);
             z += __shfl_xor_sync(0xffffffffu, z, 16);
