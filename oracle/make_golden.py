@@ -135,6 +135,11 @@ def main():
     with open(os.path.join(OUT, "rng.json"), "w") as f:
         json.dump(rng_out, f)
 
+    # reference op logs (slab_pool.cpp:45-49 format) for the replay path
+    oplog = run([f"oplog {16 * 24 * KiB} {24 * KiB} 1 3 2048 3072 4096 77 3000"])
+    with open(os.path.join(OUT, "oplog_ref.txt"), "w") as f:
+        f.write("".join(l[2:] + "\n" for l in oplog if l.startswith("L ")))
+
     meta, arrays = [], {}
     for name, cite, cap, slab, keys, lcm, seed, ops, pf, rm, nrec in CHURNS:
         line = (f"churn {cap} {slab} {lcm} {len(keys)} " + " ".join(map(str, keys)) +

@@ -187,6 +187,34 @@ void run_script(std::istream& in) {
       std::fflush(stdout);
       continue;
     }
+    if (cmd == "oplog") {  // churn with the reference's own op-log writer
+      SlabPoolConfig cfg = read_config(ls);
+      std::uint64_t seed = 0, nops = 0;
+      ls >> seed >> nops;
+      SlabPool pool(cfg);
+      pool.set_op_log([](const OpLogRecord& r) {
+        std::ostringstream os;
+        write_op_log_line(os, r);
+        std::printf("L %s", os.str().c_str());
+      });
+      Rng rng(seed);
+      std::vector<BlockHandle> live;
+      for (std::uint64_t i = 0; i < nops; ++i) {
+        if (!live.empty() && rng.uniform01() < 0.45) {
+          const std::size_t pick = static_cast<std::size_t>(rng.uniform01() * live.size());
+          pool.free_block(live[pick]);
+          live[pick] = live.back();
+          live.pop_back();
+        } else {
+          const Bytes key = cfg.block_size_keys[static_cast<std::size_t>(
+              rng.uniform01() * cfg.block_size_keys.size())];
+          auto h = pool.try_alloc_block(key);
+          if (h) live.push_back(*h);
+        }
+      }
+      std::printf("END\n");
+      continue;
+    }
     if (cmd == "rng") {
       std::uint64_t seed = 0, n = 0;
       ls >> seed >> n;

@@ -337,71 +337,102 @@ __device__ __forceinline__ uint32_t cta_of(uint32_t f, const CtaSplit& sp) {
   return lo;
 }
 
+constexpr uint32_t kMinBlocksPerCta = 4;
+__device__ __forceinline__ uint32_t effective_ctas(uint32_t total, uint32_t grid) {
+  const uint32_t want = (total + kMinBlocksPerCta - 1) / kMinBlocksPerCta;
+  return max(1u, min(grid, want));
+}
+
 // ------------------------------------------------------------ merge kernel
 // Combines the fp32 partials of every (sequence, head) unit that the decode
 // kernel's CTA ranges cut:  O = sum_j 2^(m_j-M) acc_j / sum_j 2^(m_j-M) l_j.
-// One CTA per unit, one warp per query, 4 dims per lane; all segment loads of
-// a pass are issued before use.  Launched right behind the decode kernel with
-// programmatic dependent launch, so it is resident when the decode grid ends.
-__global__ void __launch_bounds__(512) merge_kernel(const DecodeParams p, uint32_t C) {
+// One CTA per unit; warp (q, w) merges segments j = w (mod WS) of query q
+// online (all loads of a batch issued before use, 4 dims per lane), then the
+// WS partial states of each query are combined through shared memory.
+// Launched right behind the decode kernel with programmatic dependent launch,
+// so it is resident when the decode grid ends.
+constexpr int kMergeThreads = 512;  // G <= 16 warps x up to 8 segment warps, capped
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(const DecodeParams p, uint32_t grid) {
   pdl_launch_dependents();
+  __shared__ float s_m[kMergeThreads / 32], s_l[kMergeThreads / 32];
+  __shared__ float4 s_o[kMergeThreads / 32][32];
   const uint32_t unit = blockIdx.x;
   const uint32_t s = unit / p.H, h = unit % p.H;
   const uint32_t HG = p.hg, NG = p.H / p.hg, grp = h / HG, hw = h % HG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t G = p.G;
+  const uint32_t WS = blockDim.x / 32 / G;  // warps per query
+  const uint32_t q = warp / WS, w = warp % WS;
   pdl_wait();  // partials and the prefix come from the decode kernel
   const uint32_t* pre = p.prefix_out;
   const uint32_t total = pre[p.batch];
   const uint32_t nblk = (pre[s + 1] - pre[s]) / NG;
-  if (nblk == 0 || warp >= static_cast<int>(p.G)) return;
+  if (nblk == 0) return;
+  const uint32_t C = effective_ctas(total, grid);
   const CtaSplit sp = make_split(total, C);
   const uint32_t U0 = pre[s] + grp * nblk;
   const uint32_t ca = cta_of(U0, sp), cb = cta_of(U0 + nblk - 1, sp);
   if (ca == cb) return;  // whole unit: the decode kernel wrote it
-  const uint32_t G = p.G, q = warp;
   const uint32_t hdr = (2 * G + 3) & ~3u;
   const uint32_t slot_f = hdr + G * kD;
-  constexpr int SB = 8;
+  constexpr int SB = 4;
   float M = -INFINITY, L = 0.f;
   float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-  uint32_t c_lo = cta_start(ca, sp);
-  for (uint32_t c0 = ca; c0 <= cb; c0 += SB) {
-    float mv[SB], lv[SB];
-    float4 av[SB];
+  if (q < G) {
+    for (uint32_t c0 = ca + w; c0 <= cb; c0 += SB * WS) {
+      float mv[SB], lv[SB];
+      float4 av[SB];
 #pragma unroll
-    for (int j = 0; j < SB; ++j) {
-      const uint32_t c = c0 + j;
-      const uint32_t c_hi = cta_start(c + 1, sp);
-      const bool valid = c <= cb && c_lo < c_hi;
-      const float* pp =
-          p.partials + ((2ull * c + (c_lo < U0 ? 1 : 0)) * HG + hw) * static_cast<uint64_t>(slot_f);
-      mv[j] = valid ? __ldcg(pp + q) : -INFINITY;
-      lv[j] = valid ? __ldcg(pp + G + q) : 0.f;
-      av[j] = valid ? __ldcg(reinterpret_cast<const float4*>(pp + hdr + q * kD) + lane)
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-      c_lo = c_hi;
+      for (int j = 0; j < SB; ++j) {
+        const uint32_t c = c0 + j * WS;
+        const bool inr = c <= cb;
+        const uint32_t c_lo = inr ? cta_start(c, sp) : 0, c_hi = inr ? cta_start(c + 1, sp) : 0;
+        const bool valid = inr && c_lo < c_hi;
+        const float* pp =
+            p.partials + ((2ull * c + (c_lo < U0 ? 1 : 0)) * HG + hw) * static_cast<uint64_t>(slot_f);
+        mv[j] = valid ? __ldcg(pp + q) : -INFINITY;
+        lv[j] = valid ? __ldcg(pp + G + q) : 0.f;
+        av[j] = valid ? __ldcg(reinterpret_cast<const float4*>(pp + hdr + q * kD) + lane)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float Mb = M;
+#pragma unroll
+      for (int j = 0; j < SB; ++j) Mb = fmaxf(Mb, mv[j]);
+      const float a = M == -INFINITY ? 0.f : ex2(M - Mb);
+      L *= a;
+      o.x *= a; o.y *= a; o.z *= a; o.w *= a;
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        const float f = mv[j] == -INFINITY ? 0.f : ex2(mv[j] - Mb);
+        L += f * lv[j];
+        o.x += f * av[j].x; o.y += f * av[j].y; o.z += f * av[j].z; o.w += f * av[j].w;
+      }
+      M = Mb;
     }
-    float Mb = M;
-#pragma unroll
-    for (int j = 0; j < SB; ++j) Mb = fmaxf(Mb, mv[j]);
-    const float a = ex2(M - Mb);
-    L *= a;
-    o.x *= a; o.y *= a; o.z *= a; o.w *= a;
-#pragma unroll
-    for (int j = 0; j < SB; ++j) {
-      const float f = ex2(mv[j] - Mb);
-      L += f * lv[j];
-      o.x += f * av[j].x; o.y += f * av[j].y; o.z += f * av[j].z; o.w += f * av[j].w;
-    }
-    M = Mb;
+  }
+  s_m[warp] = M;
+  s_l[warp] = L;
+  s_o[warp][lane] = o;
+  __syncthreads();
+  if (q >= G || w != 0) return;
+  float Mq = -INFINITY;
+  for (uint32_t i = 0; i < WS; ++i) Mq = fmaxf(Mq, s_m[warp + i]);
+  float Lq = 0.f;
+  float4 oq = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t i = 0; i < WS; ++i) {
+    const float mi = s_m[warp + i];
+    const float f = mi == -INFINITY ? 0.f : ex2(mi - Mq);
+    Lq += f * s_l[warp + i];
+    const float4 v = s_o[warp + i][lane];
+    oq.x += f * v.x; oq.y += f * v.y; oq.z += f * v.z; oq.w += f * v.w;
   }
   const uint32_t Hq = p.H * G;
-  const float inv = 1.f / L;
+  const float inv = 1.f / Lq;
   __half* orow = p.out + (static_cast<uint64_t>(s) * Hq + h * G + q) * kD + 4 * lane;
-  *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(o.x * inv, o.y * inv);
-  *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(o.z * inv, o.w * inv);
+  *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(oq.x * inv, oq.y * inv);
+  *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(oq.z * inv, oq.w * inv);
   if (p.lse && lane == 0)
-    p.lse[static_cast<uint64_t>(s) * Hq + h * G + q] = (M + __log2f(L)) * 0.69314718055994531f;
+    p.lse[static_cast<uint64_t>(s) * Hq + h * G + q] = (Mq + __log2f(Lq)) * 0.69314718055994531f;
 }
 
 // ------------------------------------------------------------------ kernel
@@ -496,7 +527,10 @@ paged_decode_kernel(const DecodeParams p) {
     }
   }
 
-  const uint32_t C = gridDim.x;
+  // small launches use fewer CTAs (>= kMinBlocksPerCta blocks each) so a unit
+  // is not cut into more partials than the work justifies
+  const uint32_t C = effective_ctas(total, gridDim.x);
+  if (blockIdx.x >= C) return;  // uniform across the CTA
   const CtaSplit sp = make_split(total, C);
   const uint32_t cs = cta_start(blockIdx.x, sp), ce = cta_start(blockIdx.x + 1, sp);
   if (cs >= ce) return;  // uniform across the CTA
@@ -900,7 +934,12 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   // merge the partials of units cut by CTA ranges (early-exits otherwise)
   cudaLaunchConfig_t mcfg = cfg;
   mcfg.gridDim = dim3(p.batch * p.H);
-  mcfg.blockDim = dim3(p.G * 32);
+  // warps per query: up to 8, within 1024 threads
+  // (small CTAs co-reside with the next decode kernel's CTAs under PDL)
+  uint32_t ws_per_q = 1;
+  const uint32_t mt = p.merge_threads ? p.merge_threads : 512u;
+  while (ws_per_q < 8 && p.G * 32 * ws_per_q * 2 <= mt) ws_per_q *= 2;
+  mcfg.blockDim = dim3(p.G * 32 * ws_per_q);
   mcfg.dynamicSmemBytes = 0;
   return cudaLaunchKernelEx(&mcfg, merge_kernel, p, static_cast<uint32_t>(grid));
 }
