@@ -459,6 +459,7 @@ paged_decode_kernel(const DecodeParams p) {
   // PDL-enabled predecessor writes (ctx_lens, block tables, KV of other
   // layers); Q, new K/V, outputs and the workspace come after the wait.
   pdl_launch_dependents();
+  const uint64_t t0 = p.trace ? gtimer() : 0;
 
   // ---- per-CTA prefix of blocks over sequences (x NG head groups) ----
   uint32_t* pre = reinterpret_cast<uint32_t*>(smem + p.prefix_offset);
@@ -560,7 +561,9 @@ paged_decode_kernel(const DecodeParams p) {
     cursor_seek(pc, pre, p.batch, NG, cs);
     bool dep_ready = false;
     uint32_t ui = 0, st = 0, ph = 0;
+    uint64_t t_first = 0;
     for (uint32_t k = 0; k < n; ++k) {
+      if (k == 1 && p.trace) t_first = gtimer();
       if ((k & 31) == 0 && k > 0 && k + 32 < n) {
         if ((k >> 5) & 1) win0 = load_window(k + 32);
         else win1 = load_window(k + 32);
@@ -601,6 +604,13 @@ paged_decode_kernel(const DecodeParams p) {
         st = 0;
         ph ^= 1;
       }
+    }
+    if (p.trace && lane == 0) {
+      unsigned long long* tr = p.trace + static_cast<uint64_t>(blockIdx.x) * 8;
+      tr[0] = t0;
+      tr[1] = t_first;
+      tr[2] = gtimer();
+      tr[3] = n;
     }
     return;
   }
@@ -669,6 +679,7 @@ paged_decode_kernel(const DecodeParams p) {
     }
 
     mbar_wait(&full[st], ph);
+    if (p.trace && k == 0 && warp == 0 && lane == 0) p.trace[blockIdx.x * 8 + 4] = gtimer();
     if (p.k_new != nullptr && cc.b == cc.nblk - 1) {
       // Fused K1: the block holding the new token (position ctx-1) was copied
       // before the token existed.  Quantise it once (store_row, bit-identical
@@ -882,6 +893,7 @@ paged_decode_kernel(const DecodeParams p) {
     }
     cursor_next(cc, pre, p.batch, NG);
   }
+  if (p.trace && warp == 0 && lane == 0) p.trace[blockIdx.x * 8 + 5] = gtimer();
 }
 
 // Ring depth per format: ~150-200 KB in flight per SM with one CTA (HG
