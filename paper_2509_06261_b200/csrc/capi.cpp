@@ -698,7 +698,8 @@ ks_status ks_paged_decode_workspace_size(const ks_pool* pool, const ks_kv_format
   if (!pool || !fmt || !bytes) return fail(KS_INVALID_ARGUMENT, "null argument");
   const int sms = pool->num_sms > 0 ? pool->num_sms : 148;
   const size_t part = kvslab::decode_partials_bytes(sms, static_cast<int>(fmt->num_q_heads / std::max(1u, fmt->num_kv_heads)));
-  *bytes = part + (static_cast<size_t>(batch + 1) * 4 + 255) / 256 * 256;
+  (void)batch;  // the partials are sized per SM, not per sequence
+  *bytes = part;
   return KS_OK;
 }
 
@@ -746,7 +747,6 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
       return fail(KS_INVALID_ARGUMENT, "k_new and v_new must both be set or both be null");
     const size_t part = kvslab::decode_partials_bytes(pool->num_sms, static_cast<int>(p.G));
     p.partials = static_cast<float*>(d_workspace);
-    p.prefix_out = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_workspace) + part);
     p.max_ctas = 0;
     if (const char* dbg = std::getenv("KVSLAB_DECODE_DEBUG")) p.debug = std::atoi(dbg);
     {
@@ -757,6 +757,7 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
     if (const char* hg = std::getenv("KVSLAB_DECODE_HG")) p.hg_max = static_cast<uint32_t>(std::atoi(hg));
     if (const char* sb = std::getenv("KVSLAB_DECODE_SMEM")) p.smem_budget = static_cast<uint32_t>(std::atoi(sb));
     if (const char* mt = std::getenv("KVSLAB_MERGE_THREADS")) p.merge_threads = static_cast<uint32_t>(std::atoi(mt));
+    if (const char* bp = std::getenv("KVSLAB_DECODE_BPI")) p.bpi = std::atoi(bp);
     p.pdl = 1;
     if (const char* tr = std::getenv("KVSLAB_DECODE_TRACE"))
       p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(tr, nullptr, 0));

@@ -182,11 +182,14 @@ __device__ __forceinline__ void load_k_frags(uint32_t sK, const FragOff& o, uint
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         uint32_t* r = a[2 * i + e];
-        // exact fp16 n + 1024 (the bias is removed after the MMA)
-        r[0] = lop3_and_or(wl[i] >> (8 * e), 0x000F000Fu, 0x64006400u);
-        r[2] = lop3_and_or(wl[i] >> (8 * e + 4), 0x000F000Fu, 0x64006400u);
-        r[1] = lop3_and_or(wh[i] >> (8 * e), 0x000F000Fu, 0x64006400u);
-        r[3] = lop3_and_or(wh[i] >> (8 * e + 4), 0x000F000Fu, 0x64006400u);
+        const uint32_t xl = e ? wl[i] >> 8 : wl[i], xh = e ? wh[i] >> 8 : wh[i];
+        // exact fp16 1024 + n (low nibble, k-slots 2t, 2t+1) and 1024 + 16 n
+        // (high nibble in place, k-slots 2t+8, 2t+9: their Q entries carry
+        // the 1/16); the 1024 bias is removed after the MMA
+        r[0] = lop3_and_or(xl, 0x000F000Fu, 0x64006400u);
+        r[2] = lop3_and_or(xl, 0x00F000F0u, 0x64006400u);
+        r[1] = lop3_and_or(xh, 0x000F000Fu, 0x64006400u);
+        r[3] = lop3_and_or(xh, 0x00F000F0u, 0x64006400u);
       }
     }
   }
@@ -222,10 +225,12 @@ __device__ __forceinline__ void load_q_frags(uint32_t sQ, int g, int t, uint32_t
 #pragma unroll
       for (int i = 0; i < 4; ++i) {  // dims 32t + 8i .. +7: pairs (0,4),(1,5) | (2,6),(3,7)
         const uint4 v = ok ? lds128(row + 64 * t + 16 * i) : make_uint4(0, 0, 0, 0);
+        // high-nibble k-slots see K as 1024 + 16 n: their Q entries carry 1/16
+        // (a power of two: exact for normal fp16)
         qf[nt][2 * i][0] = __byte_perm(v.x, v.z, 0x5410);
-        qf[nt][2 * i][1] = __byte_perm(v.x, v.z, 0x7632);
+        qf[nt][2 * i][1] = hmul2_u32(__byte_perm(v.x, v.z, 0x7632), 0x2C002C00u);
         qf[nt][2 * i + 1][0] = __byte_perm(v.y, v.w, 0x5410);
-        qf[nt][2 * i + 1][1] = __byte_perm(v.y, v.w, 0x7632);
+        qf[nt][2 * i + 1][1] = hmul2_u32(__byte_perm(v.y, v.w, 0x7632), 0x2C002C00u);
       }
     }
   }
@@ -296,10 +301,12 @@ __device__ __forceinline__ void load_v_frags(uint32_t sV, const FragOff& o, uint
       const uint32_t ab = __byte_perm(A[w], B[w], sel);
       const uint32_t cd = __byte_perm(C[w], Dd[w], sel);
       uint32_t* r = a[i];
+      // rows g+8 (high nibbles, in place) enter as 1024 + 16 n: the epilogue
+      // divides those output dims by 16
       r[0] = lop3_and_or(ab, 0x000F000Fu, 0x64006400u);
-      r[1] = lop3_and_or(ab >> 4, 0x000F000Fu, 0x64006400u);
+      r[1] = lop3_and_or(ab, 0x00F000F0u, 0x64006400u);
       r[2] = lop3_and_or(cd, 0x000F000Fu, 0x64006400u);
-      r[3] = lop3_and_or(cd >> 4, 0x000F000Fu, 0x64006400u);
+      r[3] = lop3_and_or(cd, 0x00F000F0u, 0x64006400u);
     }
   }
 }
@@ -327,14 +334,10 @@ __device__ __forceinline__ CtaSplit make_split(uint32_t total, uint32_t C) {
 __device__ __forceinline__ uint32_t cta_start(uint32_t c, const CtaSplit& sp) {
   return c * sp.q0 + (c * sp.r0) / sp.C;
 }
-// CTA whose range contains flat index f: the largest c with start(c) <= f.
+// CTA whose range contains flat index f: the largest c with
+// floor(c*total/C) <= f, i.e. c*total < (f+1)*C.
 __device__ __forceinline__ uint32_t cta_of(uint32_t f, const CtaSplit& sp) {
-  uint32_t lo = 0, hi = sp.C;  // start(lo) <= f < start(hi) (start(C) = total > f)
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (cta_start(mid, sp) <= f) lo = mid; else hi = mid;
-  }
-  return lo;
+  return static_cast<uint32_t>(((static_cast<uint64_t>(f) + 1) * sp.C - 1) / sp.total);
 }
 
 constexpr uint32_t kMinBlocksPerCta = 4;
@@ -346,93 +349,138 @@ __device__ __forceinline__ uint32_t effective_ctas(uint32_t total, uint32_t grid
 // ------------------------------------------------------------ merge kernel
 // Combines the fp32 partials of every (sequence, head) unit that the decode
 // kernel's CTA ranges cut:  O = sum_j 2^(m_j-M) acc_j / sum_j 2^(m_j-M) l_j.
-// One CTA per unit; warp (q, w) merges segments j = w (mod WS) of query q
-// online (all loads of a batch issued before use, 4 dims per lane), then the
-// WS partial states of each query are combined through shared memory.
-// Launched right behind the decode kernel with programmatic dependent launch,
-// so it is resident when the decode grid ends.
-constexpr int kMergeThreads = 512;  // G <= 16 warps x up to 8 segment warps, capped
-__global__ void __launch_bounds__(kMergeThreads) merge_kernel(const DecodeParams p, uint32_t grid) {
+// One CTA per (sequence, head).  Before griddepcontrol.wait -- i.e. while the
+// decode grid still runs -- it recomputes the unit's CTA span from ctx_lens
+// (block prefix, the same equal-range split as the decode kernel), so after
+// the wait only the partial loads remain.  Warp (q, w) merges segments
+// c = ca + w (mod WS) of query q online (SB loads in flight, 4 dims per lane);
+// with WS > 1 the per-warp states are combined through shared memory.  The
+// CTAs are small (<= 56 registers, <= 4 KB shared) so they co-reside with the
+// running decode CTAs and with the next layer's.
+__global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS,
+                                                              uint32_t grid) {
   pdl_launch_dependents();
-  __shared__ float s_m[kMergeThreads / 32], s_l[kMergeThreads / 32];
-  __shared__ float4 s_o[kMergeThreads / 32][32];
+  const uint64_t tm0 = p.trace ? gtimer() : 0;
+  extern __shared__ float4 msm[];  // WS > 1: o[G*WS][32], then m[G*WS], l[G*WS]
+  __shared__ uint32_t red[2][32];
   const uint32_t unit = blockIdx.x;
   const uint32_t s = unit / p.H, h = unit % p.H;
   const uint32_t HG = p.hg, NG = p.H / p.hg, grp = h / HG, hw = h % HG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t G = p.G;
-  const uint32_t WS = blockDim.x / 32 / G;  // warps per query
   const uint32_t q = warp / WS, w = warp % WS;
-  pdl_wait();  // partials and the prefix come from the decode kernel
-  const uint32_t* pre = p.prefix_out;
-  const uint32_t total = pre[p.batch];
-  const uint32_t nblk = (pre[s + 1] - pre[s]) / NG;
-  if (nblk == 0) return;
-  const uint32_t C = effective_ctas(total, grid);
-  const CtaSplit sp = make_split(total, C);
-  const uint32_t U0 = pre[s] + grp * nblk;
+  const int ctx_s = p.ctx_lens[s];
+  if (ctx_s <= 0) return;  // empty sequence: written by decode CTA 0
+  // blocks before sequence s and in total (ctx_lens is not written by the
+  // PDL predecessor: same contract as the decode kernel's prologue)
+  uint32_t before = 0, all = 0;
+  for (uint32_t i = threadIdx.x; i < p.batch; i += blockDim.x) {
+    const int c = p.ctx_lens[i];
+    const uint32_t nb = c > 0 ? (static_cast<uint32_t>(c) + kTPB - 1) / kTPB : 0;
+    all += nb;
+    before += i < s ? nb : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    before += __shfl_xor_sync(0xffffffffu, before, o);
+    all += __shfl_xor_sync(0xffffffffu, all, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = before;
+    red[1][warp] = all;
+  }
+  __syncthreads();
+  before = all = 0;
+  for (uint32_t i = 0; i < blockDim.x / 32; ++i) {
+    before += red[0][i];
+    all += red[1][i];
+  }
+  const uint32_t nblk = (static_cast<uint32_t>(ctx_s) + kTPB - 1) / kTPB;
+  const uint32_t total = all * NG;
+  const uint32_t U0 = before * NG + grp * nblk;
+  const CtaSplit sp = make_split(total, effective_ctas(total, grid));
   const uint32_t ca = cta_of(U0, sp), cb = cta_of(U0 + nblk - 1, sp);
   if (ca == cb) return;  // whole unit: the decode kernel wrote it
+  // the unit is the last segment of CTA ca (its first if it starts there)
+  // and the first segment of every later CTA
+  const uint32_t slot_a = cta_start(ca, sp) < U0 ? 1u : 0u;
+  pdl_wait();  // partials come from the decode kernel
+  if (p.trace && threadIdx.x == 0) {  // probes: [2048] first merge CTA past the wait
+    const uint64_t tw = gtimer();
+    atomicMin(p.trace + 2048, static_cast<unsigned long long>(tw));
+    p.trace[2050 + 3 * blockIdx.x] = tm0;
+    p.trace[2051 + 3 * blockIdx.x] = tw;
+  }
   const uint32_t hdr = (2 * G + 3) & ~3u;
   const uint32_t slot_f = hdr + G * kD;
   constexpr int SB = 4;
   float M = -INFINITY, L = 0.f;
   float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (q < G) {
-    for (uint32_t c0 = ca + w; c0 <= cb; c0 += SB * WS) {
-      float mv[SB], lv[SB];
-      float4 av[SB];
+  for (uint32_t c0 = ca + w; c0 <= cb; c0 += SB * WS) {
+    float mv[SB], lv[SB];
+    float4 av[SB];
 #pragma unroll
-      for (int j = 0; j < SB; ++j) {
-        const uint32_t c = c0 + j * WS;
-        const bool inr = c <= cb;
-        const uint32_t c_lo = inr ? cta_start(c, sp) : 0, c_hi = inr ? cta_start(c + 1, sp) : 0;
-        const bool valid = inr && c_lo < c_hi;
-        const float* pp =
-            p.partials + ((2ull * c + (c_lo < U0 ? 1 : 0)) * HG + hw) * static_cast<uint64_t>(slot_f);
-        mv[j] = valid ? __ldcg(pp + q) : -INFINITY;
-        lv[j] = valid ? __ldcg(pp + G + q) : 0.f;
-        av[j] = valid ? __ldcg(reinterpret_cast<const float4*>(pp + hdr + q * kD) + lane)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      float Mb = M;
-#pragma unroll
-      for (int j = 0; j < SB; ++j) Mb = fmaxf(Mb, mv[j]);
-      const float a = M == -INFINITY ? 0.f : ex2(M - Mb);
-      L *= a;
-      o.x *= a; o.y *= a; o.z *= a; o.w *= a;
-#pragma unroll
-      for (int j = 0; j < SB; ++j) {
-        const float f = mv[j] == -INFINITY ? 0.f : ex2(mv[j] - Mb);
-        L += f * lv[j];
-        o.x += f * av[j].x; o.y += f * av[j].y; o.z += f * av[j].z; o.w += f * av[j].w;
-      }
-      M = Mb;
+    for (int j = 0; j < SB; ++j) {
+      const uint32_t c = c0 + j * WS;
+      const bool valid = c <= cb;
+      // the unit is the last segment of CTA ca (or its first, slot_a = 0)
+      // and the first segment of every later CTA
+      const float* pp = p.partials +
+                        ((2ull * c + (c == ca ? slot_a : 0u)) * HG + hw) * static_cast<uint64_t>(slot_f);
+      mv[j] = valid ? __ldcg(pp + q) : -INFINITY;
+      lv[j] = valid ? __ldcg(pp + G + q) : 0.f;
+      av[j] = valid ? __ldcg(reinterpret_cast<const float4*>(pp + hdr + q * kD) + lane)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    float Mb = M;
+#pragma unroll
+    for (int j = 0; j < SB; ++j) Mb = fmaxf(Mb, mv[j]);
+    const float a = M == -INFINITY ? 0.f : ex2(M - Mb);
+    L *= a;
+    o.x *= a; o.y *= a; o.z *= a; o.w *= a;
+#pragma unroll
+    for (int j = 0; j < SB; ++j) {
+      const float f = mv[j] == -INFINITY ? 0.f : ex2(mv[j] - Mb);
+      L += f * lv[j];
+      o.x += f * av[j].x; o.y += f * av[j].y; o.z += f * av[j].z; o.w += f * av[j].w;
+    }
+    M = Mb;
   }
-  s_m[warp] = M;
-  s_l[warp] = L;
-  s_o[warp][lane] = o;
-  __syncthreads();
-  if (q >= G || w != 0) return;
-  float Mq = -INFINITY;
-  for (uint32_t i = 0; i < WS; ++i) Mq = fmaxf(Mq, s_m[warp + i]);
-  float Lq = 0.f;
-  float4 oq = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (uint32_t i = 0; i < WS; ++i) {
-    const float mi = s_m[warp + i];
-    const float f = mi == -INFINITY ? 0.f : ex2(mi - Mq);
-    Lq += f * s_l[warp + i];
-    const float4 v = s_o[warp + i][lane];
-    oq.x += f * v.x; oq.y += f * v.y; oq.z += f * v.z; oq.w += f * v.w;
+  if (WS > 1) {
+    float* s_m = reinterpret_cast<float*>(msm + G * WS * 32);
+    float* s_l = s_m + G * WS;
+    s_m[warp] = M;
+    s_l[warp] = L;
+    msm[warp * 32 + lane] = o;
+    __syncthreads();
+    if (w != 0) return;
+    float Mq = -INFINITY;
+    for (uint32_t i = 0; i < WS; ++i) Mq = fmaxf(Mq, s_m[warp + i]);
+    float Lq = 0.f;
+    float4 oq = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t i = 0; i < WS; ++i) {
+      const float mi = s_m[warp + i];
+      const float f = mi == -INFINITY ? 0.f : ex2(mi - Mq);
+      Lq += f * s_l[warp + i];
+      const float4 v = msm[(warp + i) * 32 + lane];
+      oq.x += f * v.x; oq.y += f * v.y; oq.z += f * v.z; oq.w += f * v.w;
+    }
+    M = Mq;
+    L = Lq;
+    o = oq;
   }
   const uint32_t Hq = p.H * G;
-  const float inv = 1.f / Lq;
+  const float inv = 1.f / L;
   __half* orow = p.out + (static_cast<uint64_t>(s) * Hq + h * G + q) * kD + 4 * lane;
-  *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(oq.x * inv, oq.y * inv);
-  *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(oq.z * inv, oq.w * inv);
+  *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(o.x * inv, o.y * inv);
+  *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(o.z * inv, o.w * inv);
   if (p.lse && lane == 0)
-    p.lse[static_cast<uint64_t>(s) * Hq + h * G + q] = (Mq + __log2f(Lq)) * 0.69314718055994531f;
+    p.lse[static_cast<uint64_t>(s) * Hq + h * G + q] = (M + __log2f(L)) * 0.69314718055994531f;
+  if (p.trace && lane == 0) {
+    const uint64_t te = gtimer();
+    atomicMax(p.trace + 2049, static_cast<unsigned long long>(te));
+    p.trace[2052 + 3 * blockIdx.x] = te;
+  }
 }
 
 // ------------------------------------------------------------------ kernel
@@ -446,8 +494,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(const DecodeParams
 // each unit start.  Every consumer warp runs the tensor-core online softmax
 // for its head; a (sequence, head) cut by a CTA-range boundary leaves an fp32
 // partial that the warp finishing the unit last merges (per-unit counter).
-template <int FMT, int NT>
-__global__ void __launch_bounds__(NT == 1 ? 288 : 160, 1)
+// <= 152 registers for the 9-warp CTA: three warps on one SM sub-partition
+// then leave room for a merge warp (<= 56 registers) of a co-resident merge CTA
+template <int FMT, int NT, int BPI, int MINB = 1>
+__global__ void __maxnreg__(NT == 1 && MINB == 1 ? 152 : (MINB > 1 ? 128 : 255))
 paged_decode_kernel(const DecodeParams p) {
   using Gm = Geo<FMT>;
   constexpr float kRescaleSlack = 8.0f;  // log2 units: P <= 2^8 before a rescale
@@ -509,12 +559,10 @@ paged_decode_kernel(const DecodeParams p) {
   __syncthreads();
   const uint32_t total = pre[p.batch];
 
-  // CTA 0 publishes the prefix for the merge kernel and writes empty outputs
-  // for sequences with no context (both after the predecessor finished).
+  // CTA 0 writes empty outputs for sequences with no context (after the
+  // predecessor finished).
   if (blockIdx.x == 0) {
-    pdl_wait();
-    for (uint32_t s = threadIdx.x; s <= p.batch; s += blockDim.x) p.prefix_out[s] = pre[s];
-    bool waited = true;
+    bool waited = false;
     for (uint32_t s = threadIdx.x; s < p.batch; s += blockDim.x) {
       if (pre[s + 1] != pre[s]) continue;
       if (!waited) {
@@ -616,12 +664,15 @@ paged_decode_kernel(const DecodeParams p) {
   }
 
   // ============================ consumer warps ============================
+  // Each iteration consumes BPI consecutive blocks of one unit segment (two
+  // independent score tiles -> twice the ILP, one online-softmax update).
   const FragOff fo = make_offsets<FMT>(g, t);
   uint32_t qf[NT][8][2];
   float acc[8][NT][4];
-  float m_run[NT][2], l_run[NT][2], z_run[NT][2], qsum[NT][2];
+  // zb: -bias * sum(P') (biased integer formats), zz: sum(p * z_v) (INT4)
+  float m_run[NT][2], l_run[NT][2], zb_run[NT][2], zz_run[NT][2], qsb[NT][2], qst[NT][2];
   float kscale = 1.f, vscale = 1.f;
-  uint32_t seg_b0 = 0, ui = 0, st = 0, ph = 0;
+  uint32_t seg_b0 = 0, ui = 0, st = 0, ph = 0, app_b = 0xffffffffu;
   int ctx_cur = 0;
   Cursor cc;
   cursor_seek(cc, pre, p.batch, NG, cs);
@@ -629,8 +680,11 @@ paged_decode_kernel(const DecodeParams p) {
   int32_t new_gid = 0;
   const uint32_t slot_hdr = (2 * p.G + 3) & ~3u;  // m[G], l[G], padded to 16 B
   const uint32_t slot_f = slot_hdr + p.G * kD;
+  const float sml2 = p.sm_scale_log2;
+  const bool has_app = p.k_new != nullptr;
+  const uint32_t wK = warp * Gm::kChunk, wP = 2 * kvq + warp * Gm::kParam;
 
-  for (uint32_t k = 0; k < n; ++k) {
+  for (uint32_t k = 0; k < n;) {
     const uint32_t head = cc.h * HG + warp;
     if (k == 0 || cc.b == 0) {  // first block of a unit segment
       seg_b0 = cc.b;
@@ -644,21 +698,29 @@ paged_decode_kernel(const DecodeParams p) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         if constexpr (Gm::kBiased) {
-          float qsm = 0.f;
+          // lo: k-slots 2t, 2t+1; hi: 2t+8, 2t+9 (carry 1/16 for INT4)
+          float lo = 0.f, hi = 0.f;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][0]));
             const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][1]));
-            qsm += (f0.x + f0.y) + (f1.x + f1.y);
+            lo += f0.x + f0.y;
+            hi += f1.x + f1.y;
           }
-          qsm += __shfl_xor_sync(0xffffffffu, qsm, 1);
-          qsm += __shfl_xor_sync(0xffffffffu, qsm, 2);
-          qsum[nt][0] = __shfl_sync(0xffffffffu, qsm, (2 * t) * 4);
-          qsum[nt][1] = __shfl_sync(0xffffffffu, qsm, (2 * t + 1) * 4);
+          float sb = lo + hi, stt = FMT == kINT4 ? lo + 16.f * hi : sb;
+          sb += __shfl_xor_sync(0xffffffffu, sb, 1);
+          sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+          stt += __shfl_xor_sync(0xffffffffu, stt, 1);
+          stt += __shfl_xor_sync(0xffffffffu, stt, 2);
+          qsb[nt][0] = __shfl_sync(0xffffffffu, sb, (2 * t) * 4);
+          qsb[nt][1] = __shfl_sync(0xffffffffu, sb, (2 * t + 1) * 4);
+          qst[nt][0] = __shfl_sync(0xffffffffu, stt, (2 * t) * 4);
+          qst[nt][1] = __shfl_sync(0xffffffffu, stt, (2 * t + 1) * 4);
         }
         m_run[nt][0] = m_run[nt][1] = -INFINITY;
         l_run[nt][0] = l_run[nt][1] = 0.f;
-        z_run[nt][0] = z_run[nt][1] = 0.f;
+        zb_run[nt][0] = zb_run[nt][1] = 0.f;
+        zz_run[nt][0] = zz_run[nt][1] = 0.f;
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
       }
@@ -670,7 +732,8 @@ paged_decode_kernel(const DecodeParams p) {
       }
       // fused K1: if this CTA range reaches the unit's last block, fetch the
       // new token's K/V row now so the load latency is hidden
-      if (p.k_new != nullptr && k + (cc.nblk - 1 - cc.b) < n) {
+      app_b = (has_app && k + (cc.nblk - 1 - cc.b) < n) ? cc.nblk - 1 : 0xffffffffu;
+      if (app_b != 0xffffffffu) {
         const uint64_t row = (static_cast<uint64_t>(cc.s) * p.H + head) * kD + lane * 4;
         new_k = __ldg(reinterpret_cast<const uint2*>(p.k_new + row));
         new_v = __ldg(reinterpret_cast<const uint2*>(p.v_new + row));
@@ -678,13 +741,23 @@ paged_decode_kernel(const DecodeParams p) {
       }
     }
 
+    // blocks of this iteration: cc.b (stage st) and, if BPI == 2 and the
+    // segment continues, cc.b + 1 (stage st1); a lone block re-reads stage st
+    // as a fully masked second tile
+    const uint32_t nb = (BPI == 2 && k + 1 < n && cc.b + 1 < cc.nblk) ? 2u : 1u;
+    uint32_t st1 = st + 1, ph1 = ph;
+    if (st1 == S) {
+      st1 = 0;
+      ph1 ^= 1;
+    }
     mbar_wait(&full[st], ph);
-    if (p.trace && k == 0 && warp == 0 && lane == 0) p.trace[blockIdx.x * 8 + 4] = gtimer();
-    if (p.k_new != nullptr && cc.b == cc.nblk - 1) {
+    if (nb == 2) mbar_wait(&full[st1], ph1);
+    if (app_b == cc.b || (nb == 2 && app_b == cc.b + 1)) {
       // Fused K1: the block holding the new token (position ctx-1) was copied
       // before the token existed.  Quantise it once (store_row, bit-identical
       // to K1), write it to its slab block in HBM, and patch the staged copy
       // in shared memory so this step's attention includes it.
+      const uint32_t ast = app_b == cc.b ? st : st1;
       uint8_t* gblk = const_cast<uint8_t*>(p.pool) +
                       block_offset(p.geom, static_cast<uint32_t>(new_gid)) + p.layer_off;
       const uint32_t slot = static_cast<uint32_t>(ctx_cur - 1) % kTPB;
@@ -694,43 +767,37 @@ paged_decode_kernel(const DecodeParams p) {
                      head, p.H, kTPB, new_k, sck, p.fp8_inblock, lane);
       store_row<FMT>(gblk + static_cast<uint64_t>(p.H + head) * Gm::kChunk, gblk + p.params_off,
                      slot, 1, head, p.H, kTPB, new_v, scv, p.fp8_inblock, lane);
-      uint8_t* sst = ring + static_cast<size_t>(st) * p.stage_bytes;
+      uint8_t* sst = ring + static_cast<size_t>(ast) * p.stage_bytes;
       uint8_t* sprm = sst + 2 * kvq;  // [K params x HG][V params x HG]
       store_row<FMT>(sst + warp * Gm::kChunk, sprm, slot, 0, warp, HG, kTPB, new_k, sck, false, lane);
       store_row<FMT>(sst + kvq + warp * Gm::kChunk, sprm, slot, 1, warp, HG, kTPB, new_v, scv, false,
                      lane);
       __syncwarp();
     }
-    const uint32_t sb = smem_u32(ring + static_cast<size_t>(st) * p.stage_bytes);
-    const uint32_t sK = sb + warp * Gm::kChunk, sV = sb + kvq + warp * Gm::kChunk;
-    const uint32_t sKp = sb + 2 * kvq + warp * Gm::kParam, sVp = sb + 2 * kvq + pq + warp * Gm::kParam;
-    if (!(p.debug & 1)) {
-      // ---- S^T = K . Q^T (two accumulators halve the dependent MMA chain) ----
-      uint32_t ka[8][4];
-      load_k_frags<FMT>(sK, fo, ka);
-      float sacc[NT][4];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        float s2[4] = {0.f, 0.f, 0.f, 0.f};
-        sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
-#pragma unroll
-        for (int kk = 0; kk < 8; kk += 2) {
-          mma16816(sacc[nt], ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
-          mma16816(s2, ka[kk + 1][0], ka[kk + 1][1], ka[kk + 1][2], ka[kk + 1][3],
-                   qf[nt][kk + 1][0], qf[nt][kk + 1][1]);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) sacc[nt][e] += s2[e];
-      }
-      uint32_t va[8][4];
-      load_v_frags<FMT>(sV, fo, va);
+    uint32_t sbs[BPI];
+    int valid[BPI];
+    sbs[0] = smem_u32(ring + static_cast<size_t>(st) * p.stage_bytes);
+    valid[0] = min(kTPB, ctx_cur - static_cast<int>(cc.b) * kTPB);
+    if constexpr (BPI == 2) {
+      sbs[1] = nb == 2 ? smem_u32(ring + static_cast<size_t>(st1) * p.stage_bytes) : sbs[0];
+      valid[1] = nb == 2 ? min(kTPB, ctx_cur - static_cast<int>(cc.b + 1) * kTPB) : 0;
+    }
 
-      float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f}, sv[2] = {1.f, 1.f}, zv[2] = {0.f, 0.f};
+    // ---- S^T = K . Q^T per block (two accumulators halve the MMA chain) ----
+    float sc[BPI][NT][4], svv[BPI][2], zvv[BPI][2];
+#pragma unroll
+    for (int bi = 0; bi < BPI; ++bi) {
+      uint32_t ka[8][4];
+      load_k_frags<FMT>(sbs[bi] + wK, fo, ka);
+      float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f};
+      svv[bi][0] = svv[bi][1] = 1.f;
+      zvv[bi][0] = zvv[bi][1] = 0.f;
+      const uint32_t sKp = sbs[bi] + wP, sVp = sKp + pq;
       if constexpr (FMT == kINT8) {
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
-          sv[r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
+          svv[bi][r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
         }
       } else if constexpr (FMT == kINT4) {
 #pragma unroll
@@ -738,113 +805,154 @@ paged_decode_kernel(const DecodeParams p) {
           const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
           sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
           zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
-          sv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
-          zv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
+          svv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
+          zvv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
         }
       }
-      const int valid = min(kTPB, ctx_cur - static_cast<int>(cc.b) * kTPB);
-
-      uint32_t pb[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        float sc[4];
+        float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 2) {
+          mma16816(s1, ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
+          mma16816(s2, ka[kk + 1][0], ka[kk + 1][1], ka[kk + 1][2], ka[kk + 1][3],
+                   qf[nt][kk + 1][0], qf[nt][kk + 1][1]);
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int r = e >> 1, tok = g + 8 * r;
+          const int r = e >> 1;
+          const float dot = s1[e] + s2[e];
           float x;
-          if constexpr (Gm::kBiased)  // s * (dot' - bias*sum(q)) + z * sum(q)
-            x = sk[r] * (sacc[nt][e] - Gm::kBias * qsum[nt][e & 1]) + zk[r] * qsum[nt][e & 1];
+          if constexpr (Gm::kBiased)  // s * (dot' - bias*sum(q')) + z * sum(q)
+            x = sk[r] * (dot - Gm::kBias * qsb[nt][e & 1]) + zk[r] * qst[nt][e & 1];
           else
-            x = sacc[nt][e] * sk[r];
-          x *= p.sm_scale_log2;
-          sc[e] = tok < valid ? x : -INFINITY;
+            x = dot * sk[r];
+          sc[bi][nt][e] = g + 8 * r < valid[bi] ? x * sml2 : -INFINITY;
         }
-        float mx[2] = {fmaxf(sc[0], sc[2]), fmaxf(sc[1], sc[3])};
+      }
+    }
+
+    // ---- online softmax over the BPI tiles ----
+    // Lazy rescaling: the reference max m_run moves (and O is rescaled) only
+    // when a score exceeds it by kRescaleSlack; the common case costs one vote.
+    uint32_t pb[BPI][NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      bool grow = false;
+#pragma unroll
+      for (int bi = 0; bi < BPI; ++bi)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) grow |= sc[bi][nt][e] > m_run[nt][e & 1] + kRescaleSlack;
+      if (__any_sync(0xffffffffu, grow)) {
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int bi = 0; bi < BPI; ++bi) {
+          mx[0] = fmaxf(mx[0], fmaxf(sc[bi][nt][0], sc[bi][nt][2]));
+          mx[1] = fmaxf(mx[1], fmaxf(sc[bi][nt][1], sc[bi][nt][3]));
+        }
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
           mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
           mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
-        }
-        // Lazy rescaling: the reference max moves (and the accumulator is
-        // rescaled) only when a score exceeds it by kRescaleSlack.
-        const bool grow = (mx[0] > m_run[nt][0] + kRescaleSlack) ||
-                          (mx[1] > m_run[nt][1] + kRescaleSlack);
-        if (__any_sync(0xffffffffu, grow)) {
-          float alpha[2];
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const float mn = fmaxf(m_run[nt][c], mx[c]);
-            alpha[c] = ex2(m_run[nt][c] - mn);
-            m_run[nt][c] = mn;
-            l_run[nt][c] *= alpha[c];
-            z_run[nt][c] *= alpha[c];
-          }
+          const float mn = fmaxf(m_run[nt][c], mx[c]);
+          const float alpha = ex2(m_run[nt][c] - mn);
+          m_run[nt][c] = mn;
+          l_run[nt][c] *= alpha;
+          zb_run[nt][c] *= alpha;
+          zz_run[nt][c] *= alpha;
 #pragma unroll
           for (int mt = 0; mt < 8; ++mt) {
-            acc[mt][nt][0] *= alpha[0];
-            acc[mt][nt][1] *= alpha[1];
-            acc[mt][nt][2] *= alpha[0];
-            acc[mt][nt][3] *= alpha[1];
+            acc[mt][nt][c] *= alpha;
+            acc[mt][nt][2 + c] *= alpha;
           }
         }
+      }
+#pragma unroll
+      for (int bi = 0; bi < BPI; ++bi) {
         float pr[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[e] - m_run[nt][e & 1]);
-        const uint32_t plo = pack_h2(pr[0] * sv[0], pr[1] * sv[0]);
-        const uint32_t phi = pack_h2(pr[2] * sv[1], pr[3] * sv[1]);
+        for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[bi][nt][e] - m_run[nt][e & 1]);
+        const uint32_t plo = pack_h2(pr[0] * svv[bi][0], pr[1] * svv[bi][0]);
+        const uint32_t phi = pack_h2(pr[2] * svv[bi][1], pr[3] * svv[bi][1]);
 #pragma unroll
         for (int c = 0; c < 2; ++c) l_run[nt][c] += pr[c] + pr[c + 2];
         if constexpr (Gm::kBiased) {
-          // z_run collects the additive terms of O: sum p*z_v (INT4) minus
-          // bias * sum p' over the exact fp16 P' fed to the MMA
+          // the bias term uses the exact fp16 P' that the MMA consumes
           const float2 flo = __half22float2(*reinterpret_cast<const __half2*>(&plo));
           const float2 fhi = __half22float2(*reinterpret_cast<const __half2*>(&phi));
-          z_run[nt][0] += pr[0] * zv[0] + pr[2] * zv[1] - Gm::kBias * (flo.x + fhi.x);
-          z_run[nt][1] += pr[1] * zv[0] + pr[3] * zv[1] - Gm::kBias * (flo.y + fhi.y);
+          zb_run[nt][0] -= Gm::kBias * (flo.x + fhi.x);
+          zb_run[nt][1] -= Gm::kBias * (flo.y + fhi.y);
+          if constexpr (FMT == kINT4) {
+            zz_run[nt][0] += pr[0] * zvv[bi][0] + pr[2] * zvv[bi][1];
+            zz_run[nt][1] += pr[1] * zvv[bi][0] + pr[3] * zvv[bi][1];
+          }
         }
         const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
         const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
         const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
         const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
-        pb[nt][0] = __byte_perm(xa, xb, sel);
-        pb[nt][1] = __byte_perm(ya, yb, sel);
+        pb[bi][nt][0] = __byte_perm(xa, xb, sel);
+        pb[bi][nt][1] = __byte_perm(ya, yb, sel);
       }
-      // ---- O^T += V^T . P^T ----
+    }
+    // ---- O^T += V^T . P^T ----
+#pragma unroll
+    for (int bi = 0; bi < BPI; ++bi) {
+      uint32_t va[8][4];
+      load_v_frags<FMT>(sbs[bi] + kvq + wK, fo, va);
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
-          mma16816(acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[nt][0], pb[nt][1]);
+          mma16816(acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[bi][nt][0], pb[bi][nt][1]);
     }
-    // release the stage to the producer
+    // release the stage(s) to the producer
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-    if (++st == S) {
-      st = 0;
-      ph ^= 1;
+    if (lane == 0) {
+      mbar_arrive(&empty[st]);
+      if (nb == 2) mbar_arrive(&empty[st1]);
     }
+    st = st1;
+    ph = ph1;
+    if (nb == 2) {
+      if (++st == S) {
+        st = 0;
+        ph ^= 1;
+      }
+      ++cc.b;
+    }
+    const uint32_t kl = k + nb - 1;  // flat index of the last block consumed
 
     // ---- end of a unit segment ----
-    if (k == n - 1 || cc.b == cc.nblk - 1) {
+    if (kl == n - 1 || cc.b == cc.nblk - 1) {
       const bool whole = (seg_b0 == 0) && (cc.b == cc.nblk - 1);
-      float lf[NT][2], zf[NT][2];
+      const uint32_t nseg = cc.b - seg_b0 + 1;
+      const bool first_seg = (kl + 1 == nseg);
+      float lf[NT][2], zbf[NT][2], zzf[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          float l = l_run[nt][c], z = z_run[nt][c];
-          l += __shfl_xor_sync(0xffffffffu, l, 4);
-          l += __shfl_xor_sync(0xffffffffu, l, 8);
-          l += __shfl_xor_sync(0xffffffffu, l, 16);
-          if constexpr (Gm::kBiased) {
-            z += __shfl_xor_sync(0xffffffffu, z, 4);
-            z += __shfl_xor_sync(0xffffffffu, z, 8);
-            z += __shfl_xor_sync(0xffffffffu, z, 16);
+          float l = l_run[nt][c], zb = zb_run[nt][c], zz = zz_run[nt][c];
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) {
+            l += __shfl_xor_sync(0xffffffffu, l, o);
+            if constexpr (Gm::kBiased) zb += __shfl_xor_sync(0xffffffffu, zb, o);
+            if constexpr (FMT == kINT4) zz += __shfl_xor_sync(0xffffffffu, zz, o);
           }
           lf[nt][c] = l;
-          zf[nt][c] = z;
+          zbf[nt][c] = zb;
+          zzf[nt][c] = zz;
         }
+      // O rows g (lo) and g+8 (hi) of m-tile mt for query column c, unnormalised
+      auto o_lo = [&](int mt, int nt, int c) {
+        return acc[mt][nt][c] * vscale + zbf[nt][c] + zzf[nt][c];
+      };
+      auto o_hi = [&](int mt, int nt, int c) {
+        if constexpr (FMT == kINT4) return (acc[mt][nt][2 + c] + zbf[nt][c]) * 0.0625f + zzf[nt][c];
+        else return acc[mt][nt][2 + c] * vscale + zbf[nt][c] + zzf[nt][c];
+      };
       if (whole) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
@@ -857,9 +965,8 @@ paged_decode_kernel(const DecodeParams p) {
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
               const int d0 = vdim<FMT>(mt, g, 0);
-              const float o0 = (acc[mt][nt][c] * vscale + zf[nt][c]) * inv;
-              const float o1 = (acc[mt][nt][2 + c] * vscale + zf[nt][c]) * inv;
-              *reinterpret_cast<__half2*>(orow + d0) = __floats2half2_rn(o0, o1);
+              *reinterpret_cast<__half2*>(orow + d0) =
+                  __floats2half2_rn(o_lo(mt, nt, c) * inv, o_hi(mt, nt, c) * inv);
             }
             if (p.lse && g == 0)
               p.lse[static_cast<uint64_t>(cc.s) * Hq + head * p.G + q] =
@@ -867,8 +974,6 @@ paged_decode_kernel(const DecodeParams p) {
           }
       } else {
         // partial slot: (2*cta + [0 first | 1 last segment of the CTA]) * HG + warp
-        const uint32_t nseg = cc.b - seg_b0 + 1;
-        const bool first_seg = (k + 1 == nseg);
         float* ps = p.partials + ((2ull * blockIdx.x + (first_seg ? 0 : 1)) * HG + warp) * slot_f;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
@@ -883,26 +988,25 @@ paged_decode_kernel(const DecodeParams p) {
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
               const int d0 = vdim<FMT>(mt, g, 0);
-              float2 v;
-              v.x = acc[mt][nt][c] * vscale + zf[nt][c];
-              v.y = acc[mt][nt][2 + c] * vscale + zf[nt][c];
-              *reinterpret_cast<float2*>(ps + slot_hdr + q * kD + d0) = v;
+              *reinterpret_cast<float2*>(ps + slot_hdr + q * kD + d0) =
+                  make_float2(o_lo(mt, nt, c), o_hi(mt, nt, c));
             }
           }
       }
     }
     cursor_next(cc, pre, p.batch, NG);
+    k += nb;
   }
   if (p.trace && warp == 0 && lane == 0) p.trace[blockIdx.x * 8 + 5] = gtimer();
 }
 
 // Ring depth per format: ~150-200 KB in flight per SM with one CTA (HG
 // consumer warps + a producer) per SM.
-template <int FMT, int NT>
+template <int FMT, int NT, int BPI, int MINB = 1>
 static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t stream) {
   using Gm = Geo<FMT>;
   DecodeParams p = p0;
-  uint32_t hg_max = NT == 1 ? 8 : 4;
+  uint32_t hg_max = (NT == 1 && MINB == 1) ? 8 : 4;
   if (p.hg_max > 0 && p.hg_max < hg_max) hg_max = p.hg_max;
   uint32_t hg = 1;
   while (hg * 2 <= hg_max && p.H % (hg * 2) == 0) hg *= 2;
@@ -910,7 +1014,7 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   p.stage_bytes = (2 * hg * (Gm::kChunk + Gm::kParam) + 127) / 128 * 128;
   const uint32_t qbytes = hg * p.G * kD * 2;
   const size_t budget = p.smem_budget > 0 ? p.smem_budget
-                                          : 224 * 1024 - (p.batch + 1) * 4 - 2 * qbytes - 512;
+                                          : 220 * 1024 / MINB - (p.batch + 1) * 4 - 2 * qbytes - 512;
   uint32_t stages = static_cast<uint32_t>(budget / p.stage_bytes);
   if (stages > 16) stages = 16;
   if (stages < 2) stages = 2;
@@ -919,7 +1023,7 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   p.bar_offset = (p.qbuf_offset + 2 * qbytes + 15) / 16 * 16;
   p.prefix_offset = p.bar_offset + (2 * stages + 4) * 8;
   const size_t smem = p.prefix_offset + (p.batch + 1) * 4;
-  auto kern = paged_decode_kernel<FMT, NT>;
+  auto kern = paged_decode_kernel<FMT, NT, BPI, MINB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -928,7 +1032,7 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  if (per_sm > 2) per_sm = 2;  // workspace partials are sized for <= 2 CTAs per SM
+  if (per_sm > 4) per_sm = 4;  // workspace partials are sized for <= 4 CTAs per SM
   int grid = per_sm * num_sms;
   if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;
   cudaLaunchConfig_t cfg{};
@@ -943,17 +1047,20 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, kern, p);
   if (e != cudaSuccess) return e;
-  // merge the partials of units cut by CTA ranges (early-exits otherwise)
+  // merge the partials of units cut by CTA ranges (early-exits otherwise).
+  // Warps per query from the expected segments per unit (about grid / units,
+  // +1), SB = 4 loads in flight per warp; <= 128 threads (one warp per SM
+  // sub-partition) by default so a merge CTA fits beside a decode CTA.
+  const uint32_t units = p.batch * (p.H / hg);
+  const uint32_t segs = (static_cast<uint32_t>(grid) + units - 1) / units + 1;
+  const uint32_t mt = p.merge_threads ? p.merge_threads : 128u;
+  uint32_t ws = 1;
+  while (ws < 8 && ws * 4 < segs && p.G * 32 * ws * 2 <= mt) ws *= 2;
   cudaLaunchConfig_t mcfg = cfg;
   mcfg.gridDim = dim3(p.batch * p.H);
-  // warps per query: up to 8, within 1024 threads
-  // (small CTAs co-reside with the next decode kernel's CTAs under PDL)
-  uint32_t ws_per_q = 1;
-  const uint32_t mt = p.merge_threads ? p.merge_threads : 512u;
-  while (ws_per_q < 8 && p.G * 32 * ws_per_q * 2 <= mt) ws_per_q *= 2;
-  mcfg.blockDim = dim3(p.G * 32 * ws_per_q);
-  mcfg.dynamicSmemBytes = 0;
-  return cudaLaunchKernelEx(&mcfg, merge_kernel, p, static_cast<uint32_t>(grid));
+  mcfg.blockDim = dim3(p.G * 32 * ws);
+  mcfg.dynamicSmemBytes = ws > 1 ? p.G * ws * (32 * 16 + 8) : 0;
+  return cudaLaunchKernelEx(&mcfg, merge_kernel, p, ws, static_cast<uint32_t>(grid));
 }
 
 }  // namespace dev
@@ -962,19 +1069,35 @@ cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms
                                 cudaStream_t stream) {
   using namespace dev;
   const bool two = p.G > 8;
+  // one block per consumer iteration; two (probe: KVSLAB_DECODE_BPI=2) measured
+  // no faster on B200 (r01: the loop is latency-bound, not ILP-bound)
+  const bool b2 = p.bpi == 2;
+  if (p.bpi == 3 && !two) {  // probe: 3 CTAs of 4 heads per SM (<= 128 registers)
+    switch (kv_dtype) {
+      case kFP16: return launch_fmt<kFP16, 1, 1, 3>(p, num_sms, stream);
+      case kFP8: return launch_fmt<kFP8, 1, 1, 3>(p, num_sms, stream);
+      case kINT8: return launch_fmt<kINT8, 1, 1, 3>(p, num_sms, stream);
+      case kINT4: return launch_fmt<kINT4, 1, 1, 3>(p, num_sms, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+#define KS_DISPATCH(F)                                                              \
+  return two ? (b2 ? launch_fmt<F, 2, 2>(p, num_sms, stream) : launch_fmt<F, 2, 1>(p, num_sms, stream)) \
+             : (b2 ? launch_fmt<F, 1, 2>(p, num_sms, stream) : launch_fmt<F, 1, 1>(p, num_sms, stream))
   switch (kv_dtype) {
-    case kFP16: return two ? launch_fmt<kFP16, 2>(p, num_sms, stream) : launch_fmt<kFP16, 1>(p, num_sms, stream);
-    case kFP8: return two ? launch_fmt<kFP8, 2>(p, num_sms, stream) : launch_fmt<kFP8, 1>(p, num_sms, stream);
-    case kINT8: return two ? launch_fmt<kINT8, 2>(p, num_sms, stream) : launch_fmt<kINT8, 1>(p, num_sms, stream);
-    case kINT4: return two ? launch_fmt<kINT4, 2>(p, num_sms, stream) : launch_fmt<kINT4, 1>(p, num_sms, stream);
+    case kFP16: KS_DISPATCH(kFP16);
+    case kFP8: KS_DISPATCH(kFP8);
+    case kINT8: KS_DISPATCH(kINT8);
+    case kINT4: KS_DISPATCH(kINT4);
     default: return cudaErrorInvalidValue;
   }
+#undef KS_DISPATCH
 }
 
 size_t decode_partials_bytes(int num_sms, int G) {
-  // <= 2 CTAs per SM (smem) x 2 segments x (group heads x G) <= 64 query rows
+  // <= 4 CTAs per SM (smem) x 2 segments x (group heads x G) <= 64 query rows
   (void)G;
-  const size_t ctas = static_cast<size_t>(num_sms) * 2;
+  const size_t ctas = static_cast<size_t>(num_sms) * 4;
   return ctas * 2 * 64 * (dev::kD + 4) * sizeof(float);
 }
 

@@ -31,7 +31,6 @@ struct DecodeParams {
   uint32_t params_off;     // 2*H*chunk: quant params inside a layer sub-block
   bool fp8_inblock;
   float* partials;
-  uint32_t* prefix_out;  // [batch+1] block prefix published for the merge kernel
   // filled by the launcher
   uint32_t stage_bytes, bar_offset, qbuf_offset, prefix_offset, hg, stages;
   int max_ctas;  // 0 = persistent full machine
@@ -39,6 +38,7 @@ struct DecodeParams {
   uint32_t smem_budget;   // ring bytes per CTA; 0 = default
   uint32_t merge_threads; // merge CTA size cap; 0 = default (256)
   int debug;     // bit0: skip math, bit1: skip partial merge (probes only)
+  int bpi;       // blocks per consumer iteration (0 = per-format default, 1 or 2)
   int pdl;       // launch with programmatic stream serialization
   unsigned long long* trace;  // probes: per-warp globaltimer stamps (nullable)
 };

@@ -179,8 +179,9 @@ class SlabPool:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            L.lib.ks_pool_destroy(h)
+        lib = getattr(L, "lib", None)  # None during interpreter shutdown
+        if h is not None and h.value and lib is not None:
+            lib.ks_pool_destroy(h)
             self._h = C.c_void_p()
 
     def close(self) -> None:
