@@ -483,6 +483,154 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS,
   }
 }
 
+// Online-softmax state of one warp's (unit segment, head): O^T accumulator
+// tiles, reference max, row sums and the additive terms of biased formats
+// (zb: -bias * sum(P'), zz: sum(p * z_v) for INT4).
+template <int NT>
+struct UnitState {
+  float acc[8][NT][4];
+  float m[NT][2], l[NT][2], zb[NT][2], zz[NT][2];
+};
+
+constexpr float kRescaleSlack = 8.0f;  // log2 units: P <= 2^8 before a rescale
+
+// One consumer step: BPI staged blocks (shared-memory stage addresses sbs,
+// valid token counts) of one head attended by one warp -- S^T = K.Q^T on
+// tensor cores, lazy online softmax, O^T += V^T.P^T.
+template <int FMT, int NT, int BPI, bool MASK = true>
+__device__ __forceinline__ void attend(UnitState<NT>& u, const uint32_t (&sbs)[BPI],
+                                       const int (&valid)[BPI], uint32_t wK, uint32_t wP,
+                                       uint32_t kvq, uint32_t pq, const FragOff& fo,
+                                       const uint32_t (&qf)[NT][8][2], const float (&qsb)[NT][2],
+                                       const float (&qst)[NT][2], float kscale, float sml2, int g,
+                                       int t) {
+  using Gm = Geo<FMT>;
+  // ---- S^T = K . Q^T per block (two accumulators halve the MMA chain) ----
+  float sc[BPI][NT][4], svv[BPI][2], zvv[BPI][2];
+#pragma unroll
+  for (int bi = 0; bi < BPI; ++bi) {
+    uint32_t ka[8][4];
+    load_k_frags<FMT>(sbs[bi] + wK, fo, ka);
+    float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f};
+    svv[bi][0] = svv[bi][1] = 1.f;
+    zvv[bi][0] = zvv[bi][1] = 0.f;
+    const uint32_t sKp = sbs[bi] + wP, sVp = sKp + pq;
+    if constexpr (FMT == kINT8) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
+        svv[bi][r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
+      }
+    } else if constexpr (FMT == kINT4) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
+        sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
+        zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
+        svv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
+        zvv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 2) {
+        mma16816(s1, ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
+        mma16816(s2, ka[kk + 1][0], ka[kk + 1][1], ka[kk + 1][2], ka[kk + 1][3],
+                 qf[nt][kk + 1][0], qf[nt][kk + 1][1]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = e >> 1;
+        const float dot = s1[e] + s2[e];
+        float x;
+        if constexpr (Gm::kBiased)  // s * (dot' - bias*sum(q')) + z * sum(q)
+          x = sk[r] * (dot - Gm::kBias * qsb[nt][e & 1]) + zk[r] * qst[nt][e & 1];
+        else
+          x = dot * sk[r];
+        sc[bi][nt][e] = g + 8 * r < valid[bi] ? x * sml2 : -INFINITY;
+      }
+    }
+  }
+
+  // ---- online softmax over the BPI tiles ----
+  // Lazy rescaling: the reference max u.m moves (and O is rescaled) only
+  // when a score exceeds it by kRescaleSlack; the common case costs one vote.
+  uint32_t pb[BPI][NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    bool grow = false;
+#pragma unroll
+    for (int bi = 0; bi < BPI; ++bi)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) grow |= sc[bi][nt][e] > u.m[nt][e & 1] + kRescaleSlack;
+    if (__any_sync(0xffffffffu, grow)) {
+      float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int bi = 0; bi < BPI; ++bi) {
+        mx[0] = fmaxf(mx[0], fmaxf(sc[bi][nt][0], sc[bi][nt][2]));
+        mx[1] = fmaxf(mx[1], fmaxf(sc[bi][nt][1], sc[bi][nt][3]));
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
+        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
+        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
+        const float mn = fmaxf(u.m[nt][c], mx[c]);
+        const float alpha = ex2(u.m[nt][c] - mn);
+        u.m[nt][c] = mn;
+        u.l[nt][c] *= alpha;
+        u.zb[nt][c] *= alpha;
+        u.zz[nt][c] *= alpha;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          u.acc[mt][nt][c] *= alpha;
+          u.acc[mt][nt][2 + c] *= alpha;
+        }
+      }
+    }
+#pragma unroll
+    for (int bi = 0; bi < BPI; ++bi) {
+      float pr[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[bi][nt][e] - u.m[nt][e & 1]);
+      const uint32_t plo = pack_h2(pr[0] * svv[bi][0], pr[1] * svv[bi][0]);
+      const uint32_t phi = pack_h2(pr[2] * svv[bi][1], pr[3] * svv[bi][1]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) u.l[nt][c] += pr[c] + pr[c + 2];
+      if constexpr (Gm::kBiased) {
+        // the bias term uses the exact fp16 P' that the MMA consumes
+        const float2 flo = __half22float2(*reinterpret_cast<const __half2*>(&plo));
+        const float2 fhi = __half22float2(*reinterpret_cast<const __half2*>(&phi));
+        u.zb[nt][0] -= Gm::kBias * (flo.x + fhi.x);
+        u.zb[nt][1] -= Gm::kBias * (flo.y + fhi.y);
+        if constexpr (FMT == kINT4) {
+          u.zz[nt][0] += pr[0] * zvv[bi][0] + pr[2] * zvv[bi][1];
+          u.zz[nt][1] += pr[1] * zvv[bi][0] + pr[3] * zvv[bi][1];
+        }
+      }
+      const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
+      const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
+      const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
+      const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
+      pb[bi][nt][0] = __byte_perm(xa, xb, sel);
+      pb[bi][nt][1] = __byte_perm(ya, yb, sel);
+    }
+  }
+  // ---- O^T += V^T . P^T ----
+#pragma unroll
+  for (int bi = 0; bi < BPI; ++bi) {
+    uint32_t va[8][4];
+    load_v_frags<FMT>(sbs[bi] + kvq + wK, fo, va);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        mma16816(u.acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[bi][nt][0], pb[bi][nt][1]);
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 // CTA = HG consumer warps (one KV head each, a head group) + 1 producer warp.
 // Work = the flattened list of (sequence, head group, block) cut into one
@@ -496,11 +644,9 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS,
 // partial that the warp finishing the unit last merges (per-unit counter).
 // <= 152 registers for the 9-warp CTA: three warps on one SM sub-partition
 // then leave room for a merge warp (<= 56 registers) of a co-resident merge CTA
-template <int FMT, int NT, int BPI, int MINB = 1>
-__global__ void __maxnreg__(NT == 1 && MINB == 1 ? 152 : (MINB > 1 ? 128 : 255))
-paged_decode_kernel(const DecodeParams p) {
+template <int FMT, int NT>
+__global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const DecodeParams p) {
   using Gm = Geo<FMT>;
-  constexpr float kRescaleSlack = 8.0f;  // log2 units: P <= 2^8 before a rescale
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -591,63 +737,85 @@ paged_decode_kernel(const DecodeParams p) {
   uint8_t* ring = smem;
   uint8_t* qbuf = smem + p.qbuf_offset;
 
+  const bool compute_only = (p.debug & 4) != 0;  // probe: no copies; consumers reuse stage data
   if (warp == static_cast<int>(HG)) {
+    if (compute_only) return;
     // ============================ producer warp ============================
+    // Per-block work is precomputed 32 blocks at a time, one block per lane
+    // (cursor, block-table entry, slab address, unit start), so each stage
+    // costs a few shuffles and one bulk copy when the head group spans all
+    // kv heads (K, V and params of a layer sub-block are contiguous), else
+    // four.
     const uint64_t pol = policy_evict_first();
-    auto load_window = [&](uint32_t base) -> int32_t {
-      int32_t e = 0;
+    const bool one_copy = HG == p.H;
+    const uint32_t stage_tx = 2 * kvq + 2 * pq;
+    struct Win {
+      uint64_t src;  // K of head g0 in the block's layer sub-block (g0 = 0 if one_copy)
+      uint32_t g0;   // first head of the group
+      int32_t qrow;  // first Q row of the unit if the block opens a unit segment, else -1
+    };
+    auto load_window = [&](uint32_t base) -> Win {
+      Win w{0, 0, -1};
       if (base + lane < n) {
         Cursor c;
         cursor_seek(c, pre, p.batch, NG, cs + base + lane);
-        e = __ldg(p.block_table + static_cast<uint64_t>(c.s) * p.bt_stride + c.b);
+        const int32_t ent = __ldg(p.block_table + static_cast<uint64_t>(c.s) * p.bt_stride + c.b);
+        w.g0 = c.h * HG;
+        w.src = reinterpret_cast<uint64_t>(p.pool) + block_offset(p.geom, static_cast<uint32_t>(ent)) +
+                p.layer_off + static_cast<uint64_t>(w.g0) * Gm::kChunk;
+        if (c.b == 0 || base + lane == 0) w.qrow = static_cast<int32_t>(c.s * Hq + w.g0 * p.G);
       }
-      return e;
+      return w;
     };
-    int32_t win0 = load_window(0);
-    int32_t win1 = n > 32 ? load_window(32) : 0;
-    Cursor pc;
-    cursor_seek(pc, pre, p.batch, NG, cs);
+    Win win0 = load_window(0);
+    Win win1 = n > 32 ? load_window(32) : Win{0, 0, -1};
     bool dep_ready = false;
     uint32_t ui = 0, st = 0, ph = 0;
     uint64_t t_first = 0;
+    const uint32_t ring_u = smem_u32(ring);
     for (uint32_t k = 0; k < n; ++k) {
       if (k == 1 && p.trace) t_first = gtimer();
       if ((k & 31) == 0 && k > 0 && k + 32 < n) {
         if ((k >> 5) & 1) win0 = load_window(k + 32);
         else win1 = load_window(k + 32);
       }
-      const int32_t ent = __shfl_sync(0xffffffffu, ((k >> 5) & 1) ? win1 : win0, k & 31);
-      const uint32_t g0 = pc.h * HG;  // first head of the group (cursor field h = group)
-      const uint8_t* blk = p.pool + block_offset(p.geom, static_cast<uint32_t>(ent)) + p.layer_off;
-      const bool first_of_unit = (k == 0) || (pc.b == 0);
+      const Win& w = ((k >> 5) & 1) ? win1 : win0;
+      const uint32_t j = k & 31;
+      const uint64_t src = (static_cast<uint64_t>(__shfl_sync(0xffffffffu, static_cast<uint32_t>(w.src >> 32), j)) << 32) |
+                           __shfl_sync(0xffffffffu, static_cast<uint32_t>(w.src), j);
+      const int32_t qrow = __shfl_sync(0xffffffffu, w.qrow, j);
+      const uint32_t g0 = one_copy ? 0u : __shfl_sync(0xffffffffu, w.g0, j);
       mbar_wait(&empty[st], ph ^ 1);
       if (lane == 0) {
-        uint8_t* sb = ring + static_cast<size_t>(st) * p.stage_bytes;
-        mbar_expect_tx(&full[st], 2 * kvq + 2 * pq);
-        bulk_g2s(sb, blk + static_cast<uint64_t>(g0) * Gm::kChunk, kvq, &full[st], pol);
-        bulk_g2s(sb + kvq, blk + static_cast<uint64_t>(p.H + g0) * Gm::kChunk, kvq, &full[st], pol);
-        if constexpr (Gm::kParam > 0) {
-          const uint8_t* prm = blk + 2ull * p.H * Gm::kChunk;
-          bulk_g2s(sb + 2 * kvq, prm + static_cast<uint64_t>(g0) * Gm::kParam, pq, &full[st], pol);
-          bulk_g2s(sb + 2 * kvq + pq, prm + static_cast<uint64_t>(p.H + g0) * Gm::kParam, pq,
-                   &full[st], pol);
+        const uint32_t sb = ring_u + st * p.stage_bytes;
+        mbar_expect_tx(&full[st], stage_tx);
+        const uint8_t* blk = reinterpret_cast<const uint8_t*>(src);
+        if (one_copy) {
+          bulk_g2s_u32(sb, blk, stage_tx, &full[st], pol);
+        } else {
+          bulk_g2s_u32(sb, blk, kvq, &full[st], pol);
+          bulk_g2s_u32(sb + kvq, blk + static_cast<uint64_t>(p.H) * Gm::kChunk, kvq, &full[st], pol);
+          if constexpr (Gm::kParam > 0) {
+            const uint8_t* prm = blk + (2ull * p.H - g0) * Gm::kChunk + static_cast<uint64_t>(g0) * Gm::kParam;
+            bulk_g2s_u32(sb + 2 * kvq, prm, pq, &full[st], pol);
+            bulk_g2s_u32(sb + 2 * kvq + pq, prm + static_cast<uint64_t>(p.H) * Gm::kParam, pq, &full[st],
+                         pol);
+          }
         }
       }
-      if (first_of_unit && !dep_ready) {  // Q comes from the predecessor
-        pdl_wait();
-        dep_ready = true;
-      }
-      if (lane == 0) {
-        if (first_of_unit) {
+      if (qrow >= 0) {
+        if (!dep_ready) {  // Q comes from the predecessor
+          pdl_wait();
+          dep_ready = true;
+        }
+        if (lane == 0) {
           const uint32_t qs = ui & 1;
           mbar_wait(&qempty[qs], ((ui >> 1) & 1) ^ 1);
           mbar_expect_tx(&qfull[qs], qbytes);
-          bulk_g2s(qbuf + qs * qbytes, p.q + (static_cast<uint64_t>(pc.s) * Hq + g0 * p.G) * kD,
-                   qbytes, &qfull[qs], pol);
+          bulk_g2s(qbuf + qs * qbytes, p.q + static_cast<uint64_t>(qrow) * kD, qbytes, &qfull[qs], pol);
         }
+        ++ui;
       }
-      if (first_of_unit) ++ui;
-      cursor_next(pc, pre, p.batch, NG);
       if (++st == S) {
         st = 0;
         ph ^= 1;
@@ -664,36 +832,49 @@ paged_decode_kernel(const DecodeParams p) {
   }
 
   // ============================ consumer warps ============================
-  // Each iteration consumes BPI consecutive blocks of one unit segment (two
-  // independent score tiles -> twice the ILP, one online-softmax update).
+  // The CTA range is walked one unit segment at a time: the inner loop over
+  // a segment's full blocks is just wait -> attend -> release; the unit's last
+  // (partial, possibly freshly appended) block is peeled off.
   const FragOff fo = make_offsets<FMT>(g, t);
   uint32_t qf[NT][8][2];
-  float acc[8][NT][4];
-  // zb: -bias * sum(P') (biased integer formats), zz: sum(p * z_v) (INT4)
-  float m_run[NT][2], l_run[NT][2], zb_run[NT][2], zz_run[NT][2], qsb[NT][2], qst[NT][2];
+  UnitState<NT> us;
+  float qsb[NT][2], qst[NT][2];
   float kscale = 1.f, vscale = 1.f;
-  uint32_t seg_b0 = 0, ui = 0, st = 0, ph = 0, app_b = 0xffffffffu;
-  int ctx_cur = 0;
+  uint32_t ui = 0, st = 0, ph = 0;
+  const uint32_t ring_u32 = smem_u32(ring), ring_end = ring_u32 + S * p.stage_bytes;
+  uint32_t sb = ring_u32;  // shared address of stage st
   Cursor cc;
   cursor_seek(cc, pre, p.batch, NG, cs);
-  uint2 new_k = make_uint2(0, 0), new_v = make_uint2(0, 0);
-  int32_t new_gid = 0;
   const uint32_t slot_hdr = (2 * p.G + 3) & ~3u;  // m[G], l[G], padded to 16 B
   const uint32_t slot_f = slot_hdr + p.G * kD;
   const float sml2 = p.sm_scale_log2;
-  const bool has_app = p.k_new != nullptr;
   const uint32_t wK = warp * Gm::kChunk, wP = 2 * kvq + warp * Gm::kParam;
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0 && !compute_only) mbar_arrive(&empty[st]);
+    sb += p.stage_bytes;
+    if (++st == S) {
+      st = 0;
+      ph ^= 1;
+      sb = ring_u32;
+    }
+  };
+  (void)ring_end;
+  if (p.trace && warp == 0 && lane == 0) p.trace[blockIdx.x * 8 + 4] = gtimer();
+  const long long c_loop0 = clock64();
 
   for (uint32_t k = 0; k < n;) {
     const uint32_t head = cc.h * HG + warp;
-    if (k == 0 || cc.b == 0) {  // first block of a unit segment
-      seg_b0 = cc.b;
-      ctx_cur = p.ctx_lens[cc.s];
+    const uint32_t seg_b0 = cc.b;
+    const uint32_t seg_len = min(cc.nblk - cc.b, n - k);
+    const bool has_last = seg_b0 + seg_len == cc.nblk;  // holds the unit's last block
+    const int ctx_cur = p.ctx_lens[cc.s];
+    {  // ---- unit segment start: Q fragments, state ----
       const uint32_t qs = ui & 1;
-      mbar_wait(&qfull[qs], (ui >> 1) & 1);
+      if (!compute_only) mbar_wait(&qfull[qs], (ui >> 1) & 1);
       load_q_frags<FMT, NT>(smem_u32(qbuf + qs * qbytes) + warp * p.G * kD * 2, g, t, p.G, qf);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&qempty[qs]);
+      if (lane == 0 && !compute_only) mbar_arrive(&qempty[qs]);
       ++ui;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
@@ -707,22 +888,23 @@ paged_decode_kernel(const DecodeParams p) {
             lo += f0.x + f0.y;
             hi += f1.x + f1.y;
           }
-          float sb = lo + hi, stt = FMT == kINT4 ? lo + 16.f * hi : sb;
-          sb += __shfl_xor_sync(0xffffffffu, sb, 1);
-          sb += __shfl_xor_sync(0xffffffffu, sb, 2);
-          stt += __shfl_xor_sync(0xffffffffu, stt, 1);
-          stt += __shfl_xor_sync(0xffffffffu, stt, 2);
-          qsb[nt][0] = __shfl_sync(0xffffffffu, sb, (2 * t) * 4);
-          qsb[nt][1] = __shfl_sync(0xffffffffu, sb, (2 * t + 1) * 4);
-          qst[nt][0] = __shfl_sync(0xffffffffu, stt, (2 * t) * 4);
-          qst[nt][1] = __shfl_sync(0xffffffffu, stt, (2 * t + 1) * 4);
+          float sbq = lo + hi, stq = FMT == kINT4 ? lo + 16.f * hi : sbq;
+          sbq += __shfl_xor_sync(0xffffffffu, sbq, 1);
+          sbq += __shfl_xor_sync(0xffffffffu, sbq, 2);
+          stq += __shfl_xor_sync(0xffffffffu, stq, 1);
+          stq += __shfl_xor_sync(0xffffffffu, stq, 2);
+          qsb[nt][0] = __shfl_sync(0xffffffffu, sbq, (2 * t) * 4);
+          qsb[nt][1] = __shfl_sync(0xffffffffu, sbq, (2 * t + 1) * 4);
+          qst[nt][0] = __shfl_sync(0xffffffffu, stq, (2 * t) * 4);
+          qst[nt][1] = __shfl_sync(0xffffffffu, stq, (2 * t + 1) * 4);
         }
-        m_run[nt][0] = m_run[nt][1] = -INFINITY;
-        l_run[nt][0] = l_run[nt][1] = 0.f;
-        zb_run[nt][0] = zb_run[nt][1] = 0.f;
-        zz_run[nt][0] = zz_run[nt][1] = 0.f;
+        us.m[nt][0] = us.m[nt][1] = -INFINITY;
+        us.l[nt][0] = us.l[nt][1] = 0.f;
+        us.zb[nt][0] = us.zb[nt][1] = 0.f;
+        us.zz[nt][0] = us.zz[nt][1] = 0.f;
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
+        for (int mt = 0; mt < 8; ++mt)
+          us.acc[mt][nt][0] = us.acc[mt][nt][1] = us.acc[mt][nt][2] = us.acc[mt][nt][3] = 0.f;
       }
       if constexpr (FMT == kFP8) {
         if (p.kv_scales) {
@@ -730,211 +912,71 @@ paged_decode_kernel(const DecodeParams p) {
           vscale = p.kv_scales[p.H + head];
         }
       }
-      // fused K1: if this CTA range reaches the unit's last block, fetch the
-      // new token's K/V row now so the load latency is hidden
-      app_b = (has_app && k + (cc.nblk - 1 - cc.b) < n) ? cc.nblk - 1 : 0xffffffffu;
-      if (app_b != 0xffffffffu) {
-        const uint64_t row = (static_cast<uint64_t>(cc.s) * p.H + head) * kD + lane * 4;
-        new_k = __ldg(reinterpret_cast<const uint2*>(p.k_new + row));
-        new_v = __ldg(reinterpret_cast<const uint2*>(p.v_new + row));
-        new_gid = __ldg(p.block_table + static_cast<uint64_t>(cc.s) * p.bt_stride + cc.nblk - 1);
-      }
+    }
+    // fused K1: the new token lands in the unit's last block; fetch its K/V
+    // row now so the load latency is hidden behind the full blocks
+    const bool app = p.k_new != nullptr && has_last;
+    uint2 new_k = make_uint2(0, 0), new_v = make_uint2(0, 0);
+    int32_t new_gid = 0;
+    if (app) {
+      const uint64_t row = (static_cast<uint64_t>(cc.s) * p.H + head) * kD + lane * 4;
+      new_k = __ldg(reinterpret_cast<const uint2*>(p.k_new + row));
+      new_v = __ldg(reinterpret_cast<const uint2*>(p.v_new + row));
+      new_gid = __ldg(p.block_table + static_cast<uint64_t>(cc.s) * p.bt_stride + cc.nblk - 1);
     }
 
-    // blocks of this iteration: cc.b (stage st) and, if BPI == 2 and the
-    // segment continues, cc.b + 1 (stage st1); a lone block re-reads stage st
-    // as a fully masked second tile
-    const uint32_t nb = (BPI == 2 && k + 1 < n && cc.b + 1 < cc.nblk) ? 2u : 1u;
-    uint32_t st1 = st + 1, ph1 = ph;
-    if (st1 == S) {
-      st1 = 0;
-      ph1 ^= 1;
+    // ---- full blocks: all 16 tokens valid ----
+    const uint32_t nfull = seg_len - (has_last ? 1u : 0u);
+    for (uint32_t i = 0; i < nfull; ++i) {
+      if (!compute_only) mbar_wait(&full[st], ph);
+      const uint32_t sbs[1] = {sb};
+      const int valid[1] = {kTPB};
+      if (!(p.debug & 8))  // probe: stream only
+        attend<FMT, NT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+      release();
     }
-    mbar_wait(&full[st], ph);
-    if (nb == 2) mbar_wait(&full[st1], ph1);
-    if (app_b == cc.b || (nb == 2 && app_b == cc.b + 1)) {
-      // Fused K1: the block holding the new token (position ctx-1) was copied
-      // before the token existed.  Quantise it once (store_row, bit-identical
-      // to K1), write it to its slab block in HBM, and patch the staged copy
-      // in shared memory so this step's attention includes it.
-      const uint32_t ast = app_b == cc.b ? st : st1;
-      uint8_t* gblk = const_cast<uint8_t*>(p.pool) +
-                      block_offset(p.geom, static_cast<uint32_t>(new_gid)) + p.layer_off;
-      const uint32_t slot = static_cast<uint32_t>(ctx_cur - 1) % kTPB;
-      const float sck = (FMT == kFP8 && p.kv_scales) ? kscale : 1.0f;
-      const float scv = (FMT == kFP8 && p.kv_scales) ? vscale : 1.0f;
-      store_row<FMT>(gblk + static_cast<uint64_t>(head) * Gm::kChunk, gblk + p.params_off, slot, 0,
-                     head, p.H, kTPB, new_k, sck, p.fp8_inblock, lane);
-      store_row<FMT>(gblk + static_cast<uint64_t>(p.H + head) * Gm::kChunk, gblk + p.params_off,
-                     slot, 1, head, p.H, kTPB, new_v, scv, p.fp8_inblock, lane);
-      uint8_t* sst = ring + static_cast<size_t>(ast) * p.stage_bytes;
-      uint8_t* sprm = sst + 2 * kvq;  // [K params x HG][V params x HG]
-      store_row<FMT>(sst + warp * Gm::kChunk, sprm, slot, 0, warp, HG, kTPB, new_k, sck, false, lane);
-      store_row<FMT>(sst + kvq + warp * Gm::kChunk, sprm, slot, 1, warp, HG, kTPB, new_v, scv, false,
-                     lane);
-      __syncwarp();
+    // ---- the unit's last block (partial; holds the appended token) ----
+    if (has_last) {
+      if (!compute_only) mbar_wait(&full[st], ph);
+      if (app) {
+        // Fused K1: the block holding the new token (position ctx-1) was
+        // copied before the token existed.  Quantise it once (store_row,
+        // bit-identical to K1), write it to its slab block in HBM, and patch
+        // the staged copy so this step's attention includes it.
+        uint8_t* gblk = const_cast<uint8_t*>(p.pool) +
+                        block_offset(p.geom, static_cast<uint32_t>(new_gid)) + p.layer_off;
+        const uint32_t slot = static_cast<uint32_t>(ctx_cur - 1) % kTPB;
+        const float sck = (FMT == kFP8 && p.kv_scales) ? kscale : 1.0f;
+        const float scv = (FMT == kFP8 && p.kv_scales) ? vscale : 1.0f;
+        store_row<FMT>(gblk + static_cast<uint64_t>(head) * Gm::kChunk, gblk + p.params_off, slot, 0,
+                       head, p.H, kTPB, new_k, sck, p.fp8_inblock, lane);
+        store_row<FMT>(gblk + static_cast<uint64_t>(p.H + head) * Gm::kChunk, gblk + p.params_off,
+                       slot, 1, head, p.H, kTPB, new_v, scv, p.fp8_inblock, lane);
+        uint8_t* sst = ring + (sb - ring_u32);
+        uint8_t* sprm = sst + 2 * kvq;  // [K params x HG][V params x HG]
+        store_row<FMT>(sst + warp * Gm::kChunk, sprm, slot, 0, warp, HG, kTPB, new_k, sck, false, lane);
+        store_row<FMT>(sst + kvq + warp * Gm::kChunk, sprm, slot, 1, warp, HG, kTPB, new_v, scv, false,
+                       lane);
+        __syncwarp();
+      }
+      const uint32_t sbs[1] = {sb};
+      const int valid[1] = {ctx_cur - static_cast<int>(cc.nblk - 1) * kTPB};
+      attend<FMT, NT, 1, true>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+      release();
     }
-    uint32_t sbs[BPI];
-    int valid[BPI];
-    sbs[0] = smem_u32(ring + static_cast<size_t>(st) * p.stage_bytes);
-    valid[0] = min(kTPB, ctx_cur - static_cast<int>(cc.b) * kTPB);
-    if constexpr (BPI == 2) {
-      sbs[1] = nb == 2 ? smem_u32(ring + static_cast<size_t>(st1) * p.stage_bytes) : sbs[0];
-      valid[1] = nb == 2 ? min(kTPB, ctx_cur - static_cast<int>(cc.b + 1) * kTPB) : 0;
-    }
+    const bool first_seg = k == 0;  // the segment opens this CTA's range
+    k += seg_len;
+    cc.b = seg_b0 + seg_len - 1;  // last block consumed
 
-    // ---- S^T = K . Q^T per block (two accumulators halve the MMA chain) ----
-    float sc[BPI][NT][4], svv[BPI][2], zvv[BPI][2];
-#pragma unroll
-    for (int bi = 0; bi < BPI; ++bi) {
-      uint32_t ka[8][4];
-      load_k_frags<FMT>(sbs[bi] + wK, fo, ka);
-      float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f};
-      svv[bi][0] = svv[bi][1] = 1.f;
-      zvv[bi][0] = zvv[bi][1] = 0.f;
-      const uint32_t sKp = sbs[bi] + wP, sVp = sKp + pq;
-      if constexpr (FMT == kINT8) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
-          svv[bi][r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
-        }
-      } else if constexpr (FMT == kINT4) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
-          sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
-          zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
-          svv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
-          zvv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
-        }
-      }
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int kk = 0; kk < 8; kk += 2) {
-          mma16816(s1, ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
-          mma16816(s2, ka[kk + 1][0], ka[kk + 1][1], ka[kk + 1][2], ka[kk + 1][3],
-                   qf[nt][kk + 1][0], qf[nt][kk + 1][1]);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = e >> 1;
-          const float dot = s1[e] + s2[e];
-          float x;
-          if constexpr (Gm::kBiased)  // s * (dot' - bias*sum(q')) + z * sum(q)
-            x = sk[r] * (dot - Gm::kBias * qsb[nt][e & 1]) + zk[r] * qst[nt][e & 1];
-          else
-            x = dot * sk[r];
-          sc[bi][nt][e] = g + 8 * r < valid[bi] ? x * sml2 : -INFINITY;
-        }
-      }
-    }
-
-    // ---- online softmax over the BPI tiles ----
-    // Lazy rescaling: the reference max m_run moves (and O is rescaled) only
-    // when a score exceeds it by kRescaleSlack; the common case costs one vote.
-    uint32_t pb[BPI][NT][2];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      bool grow = false;
-#pragma unroll
-      for (int bi = 0; bi < BPI; ++bi)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) grow |= sc[bi][nt][e] > m_run[nt][e & 1] + kRescaleSlack;
-      if (__any_sync(0xffffffffu, grow)) {
-        float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-        for (int bi = 0; bi < BPI; ++bi) {
-          mx[0] = fmaxf(mx[0], fmaxf(sc[bi][nt][0], sc[bi][nt][2]));
-          mx[1] = fmaxf(mx[1], fmaxf(sc[bi][nt][1], sc[bi][nt][3]));
-        }
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
-          mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
-          mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
-          const float mn = fmaxf(m_run[nt][c], mx[c]);
-          const float alpha = ex2(m_run[nt][c] - mn);
-          m_run[nt][c] = mn;
-          l_run[nt][c] *= alpha;
-          zb_run[nt][c] *= alpha;
-          zz_run[nt][c] *= alpha;
-#pragma unroll
-          for (int mt = 0; mt < 8; ++mt) {
-            acc[mt][nt][c] *= alpha;
-            acc[mt][nt][2 + c] *= alpha;
-          }
-        }
-      }
-#pragma unroll
-      for (int bi = 0; bi < BPI; ++bi) {
-        float pr[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[bi][nt][e] - m_run[nt][e & 1]);
-        const uint32_t plo = pack_h2(pr[0] * svv[bi][0], pr[1] * svv[bi][0]);
-        const uint32_t phi = pack_h2(pr[2] * svv[bi][1], pr[3] * svv[bi][1]);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) l_run[nt][c] += pr[c] + pr[c + 2];
-        if constexpr (Gm::kBiased) {
-          // the bias term uses the exact fp16 P' that the MMA consumes
-          const float2 flo = __half22float2(*reinterpret_cast<const __half2*>(&plo));
-          const float2 fhi = __half22float2(*reinterpret_cast<const __half2*>(&phi));
-          zb_run[nt][0] -= Gm::kBias * (flo.x + fhi.x);
-          zb_run[nt][1] -= Gm::kBias * (flo.y + fhi.y);
-          if constexpr (FMT == kINT4) {
-            zz_run[nt][0] += pr[0] * zvv[bi][0] + pr[2] * zvv[bi][1];
-            zz_run[nt][1] += pr[1] * zvv[bi][0] + pr[3] * zvv[bi][1];
-          }
-        }
-        const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
-        const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
-        const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
-        const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
-        pb[bi][nt][0] = __byte_perm(xa, xb, sel);
-        pb[bi][nt][1] = __byte_perm(ya, yb, sel);
-      }
-    }
-    // ---- O^T += V^T . P^T ----
-#pragma unroll
-    for (int bi = 0; bi < BPI; ++bi) {
-      uint32_t va[8][4];
-      load_v_frags<FMT>(sbs[bi] + kvq + wK, fo, va);
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          mma16816(acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[bi][nt][0], pb[bi][nt][1]);
-    }
-    // release the stage(s) to the producer
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&empty[st]);
-      if (nb == 2) mbar_arrive(&empty[st1]);
-    }
-    st = st1;
-    ph = ph1;
-    if (nb == 2) {
-      if (++st == S) {
-        st = 0;
-        ph ^= 1;
-      }
-      ++cc.b;
-    }
-    const uint32_t kl = k + nb - 1;  // flat index of the last block consumed
-
-    // ---- end of a unit segment ----
-    if (kl == n - 1 || cc.b == cc.nblk - 1) {
-      const bool whole = (seg_b0 == 0) && (cc.b == cc.nblk - 1);
-      const uint32_t nseg = cc.b - seg_b0 + 1;
-      const bool first_seg = (kl + 1 == nseg);
+    // ---- end of the unit segment: output or fp32 partial ----
+    {
+      const bool whole = (seg_b0 == 0) && has_last;
       float lf[NT][2], zbf[NT][2], zzf[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          float l = l_run[nt][c], zb = zb_run[nt][c], zz = zz_run[nt][c];
+          float l = us.l[nt][c], zb = us.zb[nt][c], zz = us.zz[nt][c];
 #pragma unroll
           for (int o = 4; o < 32; o <<= 1) {
             l += __shfl_xor_sync(0xffffffffu, l, o);
@@ -947,11 +989,11 @@ paged_decode_kernel(const DecodeParams p) {
         }
       // O rows g (lo) and g+8 (hi) of m-tile mt for query column c, unnormalised
       auto o_lo = [&](int mt, int nt, int c) {
-        return acc[mt][nt][c] * vscale + zbf[nt][c] + zzf[nt][c];
+        return us.acc[mt][nt][c] * vscale + zbf[nt][c] + zzf[nt][c];
       };
       auto o_hi = [&](int mt, int nt, int c) {
-        if constexpr (FMT == kINT4) return (acc[mt][nt][2 + c] + zbf[nt][c]) * 0.0625f + zzf[nt][c];
-        else return acc[mt][nt][2 + c] * vscale + zbf[nt][c] + zzf[nt][c];
+        if constexpr (FMT == kINT4) return (us.acc[mt][nt][2 + c] + zbf[nt][c]) * 0.0625f + zzf[nt][c];
+        else return us.acc[mt][nt][2 + c] * vscale + zbf[nt][c] + zzf[nt][c];
       };
       if (whole) {
 #pragma unroll
@@ -970,7 +1012,7 @@ paged_decode_kernel(const DecodeParams p) {
             }
             if (p.lse && g == 0)
               p.lse[static_cast<uint64_t>(cc.s) * Hq + head * p.G + q] =
-                  (m_run[nt][c] + __log2f(lf[nt][c])) * 0.69314718055994531f;
+                  (us.m[nt][c] + __log2f(lf[nt][c])) * 0.69314718055994531f;
           }
       } else {
         // partial slot: (2*cta + [0 first | 1 last segment of the CTA]) * HG + warp
@@ -982,7 +1024,7 @@ paged_decode_kernel(const DecodeParams p) {
             const int q = nt * 8 + 2 * t + c;
             if (q >= static_cast<int>(p.G)) continue;
             if (g == 0) {
-              ps[q] = m_run[nt][c];
+              ps[q] = us.m[nt][c];
               ps[p.G + q] = lf[nt][c];
             }
 #pragma unroll
@@ -995,18 +1037,21 @@ paged_decode_kernel(const DecodeParams p) {
       }
     }
     cursor_next(cc, pre, p.batch, NG);
-    k += nb;
   }
-  if (p.trace && warp == 0 && lane == 0) p.trace[blockIdx.x * 8 + 5] = gtimer();
+  if (p.trace && warp == 0 && lane == 0) {
+    p.trace[blockIdx.x * 8 + 5] = gtimer();
+    p.trace[blockIdx.x * 8 + 6] = static_cast<unsigned long long>(clock64() - c_loop0);
+    p.trace[blockIdx.x * 8 + 7] = n;
+  }
 }
 
 // Ring depth per format: ~150-200 KB in flight per SM with one CTA (HG
 // consumer warps + a producer) per SM.
-template <int FMT, int NT, int BPI, int MINB = 1>
+template <int FMT, int NT>
 static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t stream) {
   using Gm = Geo<FMT>;
   DecodeParams p = p0;
-  uint32_t hg_max = (NT == 1 && MINB == 1) ? 8 : 4;
+  uint32_t hg_max = NT == 1 ? 8 : 4;
   if (p.hg_max > 0 && p.hg_max < hg_max) hg_max = p.hg_max;
   uint32_t hg = 1;
   while (hg * 2 <= hg_max && p.H % (hg * 2) == 0) hg *= 2;
@@ -1014,7 +1059,7 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   p.stage_bytes = (2 * hg * (Gm::kChunk + Gm::kParam) + 127) / 128 * 128;
   const uint32_t qbytes = hg * p.G * kD * 2;
   const size_t budget = p.smem_budget > 0 ? p.smem_budget
-                                          : 220 * 1024 / MINB - (p.batch + 1) * 4 - 2 * qbytes - 512;
+                                          : 220 * 1024 - (p.batch + 1) * 4 - 2 * qbytes - 512;
   uint32_t stages = static_cast<uint32_t>(budget / p.stage_bytes);
   if (stages > 16) stages = 16;
   if (stages < 2) stages = 2;
@@ -1023,7 +1068,7 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   p.bar_offset = (p.qbuf_offset + 2 * qbytes + 15) / 16 * 16;
   p.prefix_offset = p.bar_offset + (2 * stages + 4) * 8;
   const size_t smem = p.prefix_offset + (p.batch + 1) * 4;
-  auto kern = paged_decode_kernel<FMT, NT, BPI, MINB>;
+  auto kern = paged_decode_kernel<FMT, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -1069,29 +1114,13 @@ cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms
                                 cudaStream_t stream) {
   using namespace dev;
   const bool two = p.G > 8;
-  // one block per consumer iteration; two (probe: KVSLAB_DECODE_BPI=2) measured
-  // no faster on B200 (r01: the loop is latency-bound, not ILP-bound)
-  const bool b2 = p.bpi == 2;
-  if (p.bpi == 3 && !two) {  // probe: 3 CTAs of 4 heads per SM (<= 128 registers)
-    switch (kv_dtype) {
-      case kFP16: return launch_fmt<kFP16, 1, 1, 3>(p, num_sms, stream);
-      case kFP8: return launch_fmt<kFP8, 1, 1, 3>(p, num_sms, stream);
-      case kINT8: return launch_fmt<kINT8, 1, 1, 3>(p, num_sms, stream);
-      case kINT4: return launch_fmt<kINT4, 1, 1, 3>(p, num_sms, stream);
-      default: return cudaErrorInvalidValue;
-    }
-  }
-#define KS_DISPATCH(F)                                                              \
-  return two ? (b2 ? launch_fmt<F, 2, 2>(p, num_sms, stream) : launch_fmt<F, 2, 1>(p, num_sms, stream)) \
-             : (b2 ? launch_fmt<F, 1, 2>(p, num_sms, stream) : launch_fmt<F, 1, 1>(p, num_sms, stream))
   switch (kv_dtype) {
-    case kFP16: KS_DISPATCH(kFP16);
-    case kFP8: KS_DISPATCH(kFP8);
-    case kINT8: KS_DISPATCH(kINT8);
-    case kINT4: KS_DISPATCH(kINT4);
+    case kFP16: return two ? launch_fmt<kFP16, 2>(p, num_sms, stream) : launch_fmt<kFP16, 1>(p, num_sms, stream);
+    case kFP8: return two ? launch_fmt<kFP8, 2>(p, num_sms, stream) : launch_fmt<kFP8, 1>(p, num_sms, stream);
+    case kINT8: return two ? launch_fmt<kINT8, 2>(p, num_sms, stream) : launch_fmt<kINT8, 1>(p, num_sms, stream);
+    case kINT4: return two ? launch_fmt<kINT4, 2>(p, num_sms, stream) : launch_fmt<kINT4, 1>(p, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
-#undef KS_DISPATCH
 }
 
 size_t decode_partials_bytes(int num_sms, int G) {

@@ -38,7 +38,6 @@ struct DecodeParams {
   uint32_t smem_budget;   // ring bytes per CTA; 0 = default
   uint32_t merge_threads; // merge CTA size cap; 0 = default (256)
   int debug;     // bit0: skip math, bit1: skip partial merge (probes only)
-  int bpi;       // blocks per consumer iteration (0 = per-format default, 1 or 2)
   int pdl;       // launch with programmatic stream serialization
   unsigned long long* trace;  // probes: per-warp globaltimer stamps (nullable)
 };

@@ -50,6 +50,7 @@ for spec in os.environ.get("CASES", "FP8_E4M3:16:2048,INT4:8:8192").split(","):
         torch.cuda.synchronize()
     t = tr.cpu().numpy()
     cta = t[:, :2048].reshape(L, -1, 8)
+    cta[:, :, 0] = np.where(cta[:, :, 0] > 0, cta[:, :, 0], cta[:, :, 4])  # compute-only probes: no producer stamps
     live = cta[:, :, 0] > 0
     base = cta[:, :, 0][live].min()
     us = lambda x: (x - base) / 1e3
@@ -67,6 +68,9 @@ for spec in os.environ.get("CASES", "FP8_E4M3:16:2048,INT4:8:8192").split(","):
     pc4 = lambda x: "/".join("%.2f" % np.percentile(x, q) for q in (0, 10, 50, 90, 100))
     print(f"  L1 CTA start pct(0/10/50/90/100) {pc4(st_)}  done {pc4(dn_)}  corr {np.corrcoef(st_, dn_)[0,1]:.2f}")
     late = dn_ > np.percentile(dn_, 90)
+    print(f"  L1 consumer loop: {np.median(c[:,6] / np.maximum(c[:,7],1)):.0f} cycles/iteration (warp 0), "
+          f"{np.median((c[:,5]-c[:,4]) / np.maximum(c[:,7],1)):.0f} ns/iteration, clock "
+          f"{np.median(c[:,6] / np.maximum(c[:,5]-c[:,4],1)):.2f} GHz")
     print(f"  L1 late finishers: start {pc4(st_[late])}  blocks/cta {np.median(c[:,3]):.0f}  late ids {np.nonzero(live[1])[0][late][:12]}")
     for l in (1, L - 1):
         mm = t[l, 2050:2050 + 3 * B * 8].reshape(-1, 3)
