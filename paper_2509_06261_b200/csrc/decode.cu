@@ -357,13 +357,14 @@ __device__ __forceinline__ uint32_t effective_ctas(uint32_t total, uint32_t grid
 // with WS > 1 the per-warp states are combined through shared memory.  The
 // CTAs are small (<= 56 registers, <= 4 KB shared) so they co-reside with the
 // running decode CTAs and with the next layer's.
-__global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS,
-                                                              uint32_t grid) {
+template <int DC>  // dims split over DC CTAs per (sequence, head) (small batches)
+__global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, uint32_t grid) {
+  constexpr int VW = 4 / DC;  // floats per lane
   pdl_launch_dependents();
   const uint64_t tm0 = p.trace ? gtimer() : 0;
   extern __shared__ float4 msm[];  // WS > 1: o[G*WS][32], then m[G*WS], l[G*WS]
   __shared__ uint32_t red[2][32];
-  const uint32_t unit = blockIdx.x;
+  const uint32_t unit = blockIdx.x / DC, dc = blockIdx.x % DC;
   const uint32_t s = unit / p.H, h = unit % p.H;
   const uint32_t HG = p.hg, NG = p.H / p.hg, grp = h / HG, hw = h % HG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -413,36 +414,51 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS,
   }
   const uint32_t hdr = (2 * G + 3) & ~3u;
   const uint32_t slot_f = hdr + G * kD;
-  constexpr int SB = 4;
+  constexpr int SB = DC == 1 ? 4 : (DC == 2 ? 6 : 8);
+  const uint32_t d0 = dc * (kD / DC) + lane * VW;  // first dim of this lane
   float M = -INFINITY, L = 0.f;
-  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+  float o[VW];
+#pragma unroll
+  for (int v = 0; v < VW; ++v) o[v] = 0.f;
+  // slot of CTA c: (2c + [c == ca ? slot_a : 0]) * HG + hw; header (m, l) pairs
+  const uint32_t cstride = 2 * HG * slot_f;  // floats between consecutive CTAs' slots
+  const float* pbase = p.partials + static_cast<uint64_t>(hw) * slot_f;
+  const uint32_t a_off = slot_a * HG * slot_f;
   for (uint32_t c0 = ca + w; c0 <= cb; c0 += SB * WS) {
     float mv[SB], lv[SB];
-    float4 av[SB];
+    float av[SB][VW];
 #pragma unroll
     for (int j = 0; j < SB; ++j) {
       const uint32_t c = c0 + j * WS;
       const bool valid = c <= cb;
-      // the unit is the last segment of CTA ca (or its first, slot_a = 0)
-      // and the first segment of every later CTA
-      const float* pp = p.partials +
-                        ((2ull * c + (c == ca ? slot_a : 0u)) * HG + hw) * static_cast<uint64_t>(slot_f);
-      mv[j] = valid ? __ldcg(pp + q) : -INFINITY;
-      lv[j] = valid ? __ldcg(pp + G + q) : 0.f;
-      av[j] = valid ? __ldcg(reinterpret_cast<const float4*>(pp + hdr + q * kD) + lane)
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float* pp = pbase + (c * cstride + (c == ca ? a_off : 0u));
+      const float2 ml = valid ? __ldcg(reinterpret_cast<const float2*>(pp) + q) : make_float2(-INFINITY, 0.f);
+      mv[j] = ml.x;
+      lv[j] = ml.y;
+      const float* pa = pp + hdr + q * kD + d0;
+      if constexpr (VW == 4) {
+        const float4 x = valid ? __ldcg(reinterpret_cast<const float4*>(pa)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        av[j][0] = x.x; av[j][1] = x.y; av[j][2] = x.z; av[j][3] = x.w;
+      } else if constexpr (VW == 2) {
+        const float2 x = valid ? __ldcg(reinterpret_cast<const float2*>(pa)) : make_float2(0.f, 0.f);
+        av[j][0] = x.x; av[j][1] = x.y;
+      } else {
+        av[j][0] = valid ? __ldcg(pa) : 0.f;
+      }
     }
     float Mb = M;
 #pragma unroll
     for (int j = 0; j < SB; ++j) Mb = fmaxf(Mb, mv[j]);
     const float a = M == -INFINITY ? 0.f : ex2(M - Mb);
     L *= a;
-    o.x *= a; o.y *= a; o.z *= a; o.w *= a;
+#pragma unroll
+    for (int v = 0; v < VW; ++v) o[v] *= a;
 #pragma unroll
     for (int j = 0; j < SB; ++j) {
       const float f = mv[j] == -INFINITY ? 0.f : ex2(mv[j] - Mb);
       L += f * lv[j];
-      o.x += f * av[j].x; o.y += f * av[j].y; o.z += f * av[j].z; o.w += f * av[j].w;
+#pragma unroll
+      for (int v = 0; v < VW; ++v) o[v] += f * av[j][v];
     }
     M = Mb;
   }
@@ -451,30 +467,41 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS,
     float* s_l = s_m + G * WS;
     s_m[warp] = M;
     s_l[warp] = L;
-    msm[warp * 32 + lane] = o;
+    float* mo = reinterpret_cast<float*>(msm + warp * 32 + lane);
+#pragma unroll
+    for (int v = 0; v < VW; ++v) mo[v] = o[v];
     __syncthreads();
     if (w != 0) return;
     float Mq = -INFINITY;
     for (uint32_t i = 0; i < WS; ++i) Mq = fmaxf(Mq, s_m[warp + i]);
     float Lq = 0.f;
-    float4 oq = make_float4(0.f, 0.f, 0.f, 0.f);
+    float oq[VW];
+#pragma unroll
+    for (int v = 0; v < VW; ++v) oq[v] = 0.f;
     for (uint32_t i = 0; i < WS; ++i) {
       const float mi = s_m[warp + i];
       const float f = mi == -INFINITY ? 0.f : ex2(mi - Mq);
       Lq += f * s_l[warp + i];
-      const float4 v = msm[(warp + i) * 32 + lane];
-      oq.x += f * v.x; oq.y += f * v.y; oq.z += f * v.z; oq.w += f * v.w;
+      const float* vi = reinterpret_cast<const float*>(msm + (warp + i) * 32 + lane);
+#pragma unroll
+      for (int v = 0; v < VW; ++v) oq[v] += f * vi[v];
     }
     M = Mq;
     L = Lq;
-    o = oq;
+#pragma unroll
+    for (int v = 0; v < VW; ++v) o[v] = oq[v];
   }
   const uint32_t Hq = p.H * G;
   const float inv = 1.f / L;
-  __half* orow = p.out + (static_cast<uint64_t>(s) * Hq + h * G + q) * kD + 4 * lane;
-  *reinterpret_cast<__half2*>(orow) = __floats2half2_rn(o.x * inv, o.y * inv);
-  *reinterpret_cast<__half2*>(orow + 2) = __floats2half2_rn(o.z * inv, o.w * inv);
-  if (p.lse && lane == 0)
+  __half* orow = p.out + (static_cast<uint64_t>(s) * Hq + h * G + q) * kD + d0;
+  if constexpr (VW == 1) {
+    *orow = __float2half_rn(o[0] * inv);
+  } else {
+#pragma unroll
+    for (int v = 0; v < VW; v += 2)
+      *reinterpret_cast<__half2*>(orow + v) = __floats2half2_rn(o[v] * inv, o[v + 1] * inv);
+  }
+  if (p.lse && lane == 0 && dc == 0)
     p.lse[static_cast<uint64_t>(s) * Hq + h * G + q] = (M + __log2f(L)) * 0.69314718055994531f;
   if (p.trace && lane == 0) {
     const uint64_t te = gtimer();
@@ -845,7 +872,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
   uint32_t sb = ring_u32;  // shared address of stage st
   Cursor cc;
   cursor_seek(cc, pre, p.batch, NG, cs);
-  const uint32_t slot_hdr = (2 * p.G + 3) & ~3u;  // m[G], l[G], padded to 16 B
+  const uint32_t slot_hdr = (2 * p.G + 3) & ~3u;  // (m, l)[G], padded to 16 B
   const uint32_t slot_f = slot_hdr + p.G * kD;
   const float sml2 = p.sm_scale_log2;
   const uint32_t wK = warp * Gm::kChunk, wP = 2 * kvq + warp * Gm::kParam;
@@ -1023,10 +1050,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
           for (int c = 0; c < 2; ++c) {
             const int q = nt * 8 + 2 * t + c;
             if (q >= static_cast<int>(p.G)) continue;
-            if (g == 0) {
-              ps[q] = us.m[nt][c];
-              ps[p.G + q] = lf[nt][c];
-            }
+            if (g == 0) *reinterpret_cast<float2*>(ps + 2 * q) = make_float2(us.m[nt][c], lf[nt][c]);
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
               const int d0 = vdim<FMT>(mt, g, 0);
@@ -1098,14 +1122,23 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   // sub-partition) by default so a merge CTA fits beside a decode CTA.
   const uint32_t units = p.batch * (p.H / hg);
   const uint32_t segs = (static_cast<uint32_t>(grid) + units - 1) / units + 1;
-  const uint32_t mt = p.merge_threads ? p.merge_threads : 128u;
+  // Many merge CTAs (>= 64): <= 128 threads each, so they co-reside with the
+  // decode CTAs.  Few (small batch, long context: many segments per unit):
+  // up to 1024 threads, so each warp merges <= 2 batches of SB segments.
+  const uint32_t mt = p.merge_threads ? p.merge_threads : (p.batch * p.H >= 64 ? 128u : 1024u);
   uint32_t ws = 1;
-  while (ws < 8 && ws * 4 < segs && p.G * 32 * ws * 2 <= mt) ws *= 2;
+  while (ws < 32 && ws * 4 * 2 < segs && p.G * 32 * ws * 2 <= mt) ws *= 2;
+  // and few (sequence, head) merges are spread over DC CTAs each (dims split)
+  const uint32_t heads = p.batch * p.H;
+  const int DC = heads >= 64 ? 1 : (heads >= 32 ? 2 : 4);
   cudaLaunchConfig_t mcfg = cfg;
-  mcfg.gridDim = dim3(p.batch * p.H);
+  mcfg.gridDim = dim3(heads * DC);
   mcfg.blockDim = dim3(p.G * 32 * ws);
   mcfg.dynamicSmemBytes = ws > 1 ? p.G * ws * (32 * 16 + 8) : 0;
-  return cudaLaunchKernelEx(&mcfg, merge_kernel, p, ws, static_cast<uint32_t>(grid));
+  const uint32_t g32 = static_cast<uint32_t>(grid);
+  if (DC == 1) return cudaLaunchKernelEx(&mcfg, merge_kernel<1>, p, ws, g32);
+  if (DC == 2) return cudaLaunchKernelEx(&mcfg, merge_kernel<2>, p, ws, g32);
+  return cudaLaunchKernelEx(&mcfg, merge_kernel<4>, p, ws, g32);
 }
 
 }  // namespace dev
