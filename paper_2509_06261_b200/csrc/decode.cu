@@ -761,6 +761,10 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
   const uint32_t kvq = HG * Gm::kChunk;          // bytes of the group's K (or V) chunks
   const uint32_t pq = HG * Gm::kParam;           // bytes of the group's K (or V) params
   const uint32_t qbytes = HG * p.G * kD * 2;
+  // a Q slot also carries the group's new K/V rows when the step appends
+  const uint32_t nbytes = HG * kD * 2;
+  const uint32_t qslot = qbytes + (p.k_new != nullptr ? 2 * nbytes : 0u);
+  uint64_t* meta = reinterpret_cast<uint64_t*>(smem + p.bar_offset) + 2 * S + 4;  // [S] stage block address
   uint8_t* ring = smem;
   uint8_t* qbuf = smem + p.qbuf_offset;
 
@@ -778,7 +782,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     const uint32_t stage_tx = 2 * kvq + 2 * pq;
     struct Win {
       uint64_t src;  // K of head g0 in the block's layer sub-block (g0 = 0 if one_copy)
-      uint32_t g0;   // first head of the group
+      uint32_t g0;   // first head of the group; bit 31: the segment it opens holds the unit's last block
       int32_t qrow;  // first Q row of the unit if the block opens a unit segment, else -1
     };
     auto load_window = [&](uint32_t base) -> Win {
@@ -790,7 +794,10 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         w.g0 = c.h * HG;
         w.src = reinterpret_cast<uint64_t>(p.pool) + block_offset(p.geom, static_cast<uint32_t>(ent)) +
                 p.layer_off + static_cast<uint64_t>(w.g0) * Gm::kChunk;
-        if (c.b == 0 || base + lane == 0) w.qrow = static_cast<int32_t>(c.s * Hq + w.g0 * p.G);
+        if (c.b == 0 || base + lane == 0) {
+          w.qrow = static_cast<int32_t>(c.s * Hq + w.g0 * p.G);
+          if (n - (base + lane) >= c.nblk - c.b) w.g0 |= 0x80000000u;
+        }
       }
       return w;
     };
@@ -811,10 +818,12 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       const uint64_t src = (static_cast<uint64_t>(__shfl_sync(0xffffffffu, static_cast<uint32_t>(w.src >> 32), j)) << 32) |
                            __shfl_sync(0xffffffffu, static_cast<uint32_t>(w.src), j);
       const int32_t qrow = __shfl_sync(0xffffffffu, w.qrow, j);
-      const uint32_t g0 = one_copy ? 0u : __shfl_sync(0xffffffffu, w.g0, j);
+      const uint32_t gw = __shfl_sync(0xffffffffu, w.g0, j);
+      const uint32_t g0 = gw & 0x7fffffffu;
       mbar_wait(&empty[st], ph ^ 1);
       if (lane == 0) {
         const uint32_t sb = ring_u + st * p.stage_bytes;
+        meta[st] = src - static_cast<uint64_t>(g0) * Gm::kChunk;  // layer sub-block (fused append)
         mbar_expect_tx(&full[st], stage_tx);
         const uint8_t* blk = reinterpret_cast<const uint8_t*>(src);
         if (one_copy) {
@@ -837,9 +846,16 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         }
         if (lane == 0) {
           const uint32_t qs = ui & 1;
+          const bool app = p.k_new != nullptr && (gw >> 31);
           mbar_wait(&qempty[qs], ((ui >> 1) & 1) ^ 1);
-          mbar_expect_tx(&qfull[qs], qbytes);
-          bulk_g2s(qbuf + qs * qbytes, p.q + static_cast<uint64_t>(qrow) * kD, qbytes, &qfull[qs], pol);
+          mbar_expect_tx(&qfull[qs], qbytes + (app ? 2 * nbytes : 0u));
+          uint8_t* qd = qbuf + qs * qslot;
+          bulk_g2s(qd, p.q + static_cast<uint64_t>(qrow) * kD, qbytes, &qfull[qs], pol);
+          if (app) {  // the new token's K and V rows of the group (fused K1)
+            const uint64_t nrow = static_cast<uint64_t>(qrow / static_cast<int32_t>(Hq)) * p.H + g0;
+            bulk_g2s(qd + qbytes, p.k_new + nrow * kD, nbytes, &qfull[qs], pol);
+            bulk_g2s(qd + qbytes + nbytes, p.v_new + nrow * kD, nbytes, &qfull[qs], pol);
+          }
         }
         ++ui;
       }
@@ -896,10 +912,16 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     const uint32_t seg_len = min(cc.nblk - cc.b, n - k);
     const bool has_last = seg_b0 + seg_len == cc.nblk;  // holds the unit's last block
     const int ctx_cur = p.ctx_lens[cc.s];
+    uint2 new_k = make_uint2(0, 0), new_v = make_uint2(0, 0);  // fused K1: this lane's 4 values
     {  // ---- unit segment start: Q fragments, state ----
       const uint32_t qs = ui & 1;
       if (!compute_only) mbar_wait(&qfull[qs], (ui >> 1) & 1);
-      load_q_frags<FMT, NT>(smem_u32(qbuf + qs * qbytes) + warp * p.G * kD * 2, g, t, p.G, qf);
+      load_q_frags<FMT, NT>(smem_u32(qbuf + qs * qslot) + warp * p.G * kD * 2, g, t, p.G, qf);
+      if (p.k_new != nullptr && has_last) {  // staged with Q by the producer
+        const uint32_t nk = smem_u32(qbuf + qs * qslot + qbytes) + warp * kD * 2 + lane * 8;
+        new_k = lds64(nk);
+        new_v = lds64(nk + nbytes);
+      }
       __syncwarp();
       if (lane == 0 && !compute_only) mbar_arrive(&qempty[qs]);
       ++ui;
@@ -943,14 +965,6 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     // fused K1: the new token lands in the unit's last block; fetch its K/V
     // row now so the load latency is hidden behind the full blocks
     const bool app = p.k_new != nullptr && has_last;
-    uint2 new_k = make_uint2(0, 0), new_v = make_uint2(0, 0);
-    int32_t new_gid = 0;
-    if (app) {
-      const uint64_t row = (static_cast<uint64_t>(cc.s) * p.H + head) * kD + lane * 4;
-      new_k = __ldg(reinterpret_cast<const uint2*>(p.k_new + row));
-      new_v = __ldg(reinterpret_cast<const uint2*>(p.v_new + row));
-      new_gid = __ldg(p.block_table + static_cast<uint64_t>(cc.s) * p.bt_stride + cc.nblk - 1);
-    }
 
     // ---- full blocks: all 16 tokens valid ----
     const uint32_t nfull = seg_len - (has_last ? 1u : 0u);
@@ -967,23 +981,22 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       if (!compute_only) mbar_wait(&full[st], ph);
       if (app) {
         // Fused K1: the block holding the new token (position ctx-1) was
-        // copied before the token existed.  Quantise it once (store_row,
+        // copied before the token existed.  Quantise it once (quant_row,
         // bit-identical to K1), write it to its slab block in HBM, and patch
         // the staged copy so this step's attention includes it.
-        uint8_t* gblk = const_cast<uint8_t*>(p.pool) +
-                        block_offset(p.geom, static_cast<uint32_t>(new_gid)) + p.layer_off;
+        uint8_t* gblk = reinterpret_cast<uint8_t*>(meta[st]);  // the block's layer sub-block
         const uint32_t slot = static_cast<uint32_t>(ctx_cur - 1) % kTPB;
         const float sck = (FMT == kFP8 && p.kv_scales) ? kscale : 1.0f;
         const float scv = (FMT == kFP8 && p.kv_scales) ? vscale : 1.0f;
-        store_row<FMT>(gblk + static_cast<uint64_t>(head) * Gm::kChunk, gblk + p.params_off, slot, 0,
-                       head, p.H, kTPB, new_k, sck, p.fp8_inblock, lane);
-        store_row<FMT>(gblk + static_cast<uint64_t>(p.H + head) * Gm::kChunk, gblk + p.params_off,
-                       slot, 1, head, p.H, kTPB, new_v, scv, p.fp8_inblock, lane);
+        const QRow rk = quant_row<FMT>(new_k, sck), rv = quant_row<FMT>(new_v, scv);
+        put_row<FMT>(gblk + static_cast<uint64_t>(head) * Gm::kChunk, gblk + p.params_off, slot, 0, head,
+                     p.H, kTPB, rk, sck, p.fp8_inblock, lane);
+        put_row<FMT>(gblk + static_cast<uint64_t>(p.H + head) * Gm::kChunk, gblk + p.params_off, slot, 1,
+                     head, p.H, kTPB, rv, scv, p.fp8_inblock, lane);
         uint8_t* sst = ring + (sb - ring_u32);
         uint8_t* sprm = sst + 2 * kvq;  // [K params x HG][V params x HG]
-        store_row<FMT>(sst + warp * Gm::kChunk, sprm, slot, 0, warp, HG, kTPB, new_k, sck, false, lane);
-        store_row<FMT>(sst + kvq + warp * Gm::kChunk, sprm, slot, 1, warp, HG, kTPB, new_v, scv, false,
-                       lane);
+        put_row<FMT>(sst + warp * Gm::kChunk, sprm, slot, 0, warp, HG, kTPB, rk, sck, false, lane);
+        put_row<FMT>(sst + kvq + warp * Gm::kChunk, sprm, slot, 1, warp, HG, kTPB, rv, scv, false, lane);
         __syncwarp();
       }
       const uint32_t sbs[1] = {sb};
@@ -1081,7 +1094,7 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   while (hg * 2 <= hg_max && p.H % (hg * 2) == 0) hg *= 2;
   p.hg = hg;
   p.stage_bytes = (2 * hg * (Gm::kChunk + Gm::kParam) + 127) / 128 * 128;
-  const uint32_t qbytes = hg * p.G * kD * 2;
+  const uint32_t qbytes = hg * p.G * kD * 2 + (p.k_new != nullptr ? 2 * hg * kD * 2 : 0);  // Q slot
   const size_t budget = p.smem_budget > 0 ? p.smem_budget
                                           : 220 * 1024 - (p.batch + 1) * 4 - 2 * qbytes - 512;
   uint32_t stages = static_cast<uint32_t>(budget / p.stage_bytes);
@@ -1090,7 +1103,7 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   p.stages = stages;
   p.qbuf_offset = stages * p.stage_bytes;
   p.bar_offset = (p.qbuf_offset + 2 * qbytes + 15) / 16 * 16;
-  p.prefix_offset = p.bar_offset + (2 * stages + 4) * 8;
+  p.prefix_offset = p.bar_offset + (2 * stages + 4) * 8 + stages * 8;  // + stage block addresses
   const size_t smem = p.prefix_offset + (p.batch + 1) * 4;
   auto kern = paged_decode_kernel<FMT, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -34,8 +34,9 @@ for spec in os.environ.get("CASES", "FP8_E4M3:16:2048,INT4:8:8192").split(","):
     def step():
         for l in range(L):
             os.environ["KVSLAB_DECODE_TRACE"] = str(tr[l].data_ptr())
+            app = os.environ.get("APPEND", "1") == "1"
             kv.paged_decode(pool, fmt, l, qs[l], m.table, ctx, kv_scales=sc, workspace=ws,
-                            k_new=kn, v_new=kn)
+                            k_new=kn if app else None, v_new=kn if app else None)
         del os.environ["KVSLAB_DECODE_TRACE"]
     with torch.cuda.stream(st):
         step(); torch.cuda.synchronize()
