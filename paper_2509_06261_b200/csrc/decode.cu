@@ -658,6 +658,11 @@ __device__ __forceinline__ void attend(UnitState<NT>& u, const uint32_t (&sbs)[B
   }
 }
 
+// Formats whose consumer step runs two full blocks at a time (measured per format
+// with scripts/microbench_consumer.cu and in the kernel).
+template <int FMT, int NT>
+constexpr bool kPairs = NT == 1 && FMT != kFP16;  // FP16: no gain, spills
+
 // ------------------------------------------------------------------ kernel
 // CTA = HG consumer warps (one KV head each, a head group) + 1 producer warp.
 // Work = the flattened list of (sequence, head group, block) cut into one
@@ -902,7 +907,6 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       sb = ring_u32;
     }
   };
-  (void)ring_end;
   if (p.trace && warp == 0 && lane == 0) p.trace[blockIdx.x * 8 + 4] = gtimer();
   const long long c_loop0 = clock64();
 
@@ -968,7 +972,25 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
 
     // ---- full blocks: all 16 tokens valid ----
     const uint32_t nfull = seg_len - (has_last ? 1u : 0u);
-    for (uint32_t i = 0; i < nfull; ++i) {
+    uint32_t i = 0;
+    if constexpr (kPairs<FMT, NT>) {
+      // two full blocks per step: two independent score tiles, one softmax
+      // update (INT4: the dequant-heavy step gains from the extra ILP)
+      for (; i + 1 < nfull; i += 2) {
+        const uint32_t sb1 = sb + p.stage_bytes == ring_end ? ring_u32 : sb + p.stage_bytes;
+        const uint32_t st1 = st + 1 == S ? 0 : st + 1, ph1 = st + 1 == S ? ph ^ 1 : ph;
+        if (!compute_only) {
+          mbar_wait(&full[st], ph);
+          mbar_wait(&full[st1], ph1);
+        }
+        const uint32_t sbs[2] = {sb, sb1};
+        const int valid[2] = {kTPB, kTPB};
+        attend<FMT, NT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+        release();
+        release();
+      }
+    }
+    for (; i < nfull; ++i) {
       if (!compute_only) mbar_wait(&full[st], ph);
       const uint32_t sbs[1] = {sb};
       const int valid[1] = {kTPB};
