@@ -8,6 +8,7 @@ device tensor and calls a CUDA kernel.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import enum
 import math
 from dataclasses import dataclass
@@ -76,6 +77,25 @@ class KvFormat:
     def to_c(self) -> L.ks_kv_format:
         return L.ks_kv_format(int(self.kv_dtype), self.num_kv_heads, self.num_q_heads,
                               self.head_dim, self.num_layers, self.tokens_per_block, self.qparams)
+
+    def shard(self, tp: int) -> "KvFormat":
+        """Format of one tensor-parallel shard: KV and Q
+        heads split over `tp` GPUs, each shard an ordinary pool over its heads.
+        Rejects heads % tp != 0 like token_size (precision.cpp:80-83); the
+        shard's key equals kv_block_size(profile with tp_degree=tp)."""
+        if tp < 1 or self.num_kv_heads % tp or self.num_q_heads % tp:
+            raise ValueError(f"kv heads {self.num_kv_heads} / q heads {self.num_q_heads} "
+                             f"not divisible by tp {tp}")
+        qp = self.quant_param_bytes_per_block
+        return dataclasses.replace(self, num_kv_heads=self.num_kv_heads // tp,
+                                   num_q_heads=self.num_q_heads // tp,
+                                   quant_param_bytes_per_block=None if qp is None else qp // tp)
+
+    def head_slices(self, tp: int, rank: int) -> Tuple[slice, slice]:
+        """(kv-head slice, q-head slice) of shard `rank`: contiguous head ranges,
+        so every q head stays with its kv head (GQA groups are never split)."""
+        kv, q = self.num_kv_heads // tp, self.num_q_heads // tp
+        return slice(rank * kv, (rank + 1) * kv), slice(rank * q, (rank + 1) * q)
 
     def decode_bytes(self, ctx_lens: Sequence[int]) -> int:
         """Algorithmic bytes of one K2 launch: every cached K/V
