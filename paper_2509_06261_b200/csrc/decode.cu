@@ -510,6 +510,13 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, 
   }
 }
 
+// Probe stamps (p.trace only): per CTA, the time the producer issues stage k
+// (k < 32) and the time consumer warp 0 sees it full.
+constexpr uint32_t kTrStage = 12288, kTrReady = kTrStage + 148 * 4 * 32;
+__device__ __forceinline__ void trace_ready(const DecodeParams& p, int warp, int lane, uint32_t k) {
+  if (p.trace && warp == 0 && lane == 0 && k < 32) p.trace[kTrReady + blockIdx.x * 32 + k] = gtimer();
+}
+
 // Online-softmax state of one warp's (unit segment, head): O^T accumulator
 // tiles, reference max, row sums and the additive terms of biased formats
 // (zb: -bias * sum(P'), zz: sum(p * z_v) for INT4).
@@ -826,6 +833,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       const uint32_t gw = __shfl_sync(0xffffffffu, w.g0, j);
       const uint32_t g0 = gw & 0x7fffffffu;
       mbar_wait(&empty[st], ph ^ 1);
+      if (p.trace && lane == 0 && k < 32) p.trace[kTrStage + blockIdx.x * 32 + k] = gtimer();
       if (lane == 0) {
         const uint32_t sb = ring_u + st * p.stage_bytes;
         meta[st] = src - static_cast<uint64_t>(g0) * Gm::kChunk;  // layer sub-block (fused append)
@@ -983,6 +991,8 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
           mbar_wait(&full[st], ph);
           mbar_wait(&full[st1], ph1);
         }
+        trace_ready(p, warp, lane, k + i);
+        trace_ready(p, warp, lane, k + i + 1);
         const uint32_t sbs[2] = {sb, sb1};
         const int valid[2] = {kTPB, kTPB};
         attend<FMT, NT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
@@ -992,6 +1002,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     }
     for (; i < nfull; ++i) {
       if (!compute_only) mbar_wait(&full[st], ph);
+      trace_ready(p, warp, lane, k + i);
       const uint32_t sbs[1] = {sb};
       const int valid[1] = {kTPB};
       if (!(p.debug & 8))  // probe: stream only
@@ -1001,6 +1012,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     // ---- the unit's last block (partial; holds the appended token) ----
     if (has_last) {
       if (!compute_only) mbar_wait(&full[st], ph);
+      trace_ready(p, warp, lane, k + nfull);
       if (app) {
         // Fused K1: the block holding the new token (position ctx-1) was
         // copied before the token existed.  Quantise it once (quant_row,
