@@ -260,6 +260,21 @@ ks_status ks_paged_decode_append(ks_pool* pool, const ks_kv_format* fmt, uint32_
                                  float sm_scale, const float* d_kv_scales, void* d_workspace,
                                  size_t workspace_bytes, void* stream);
 
+/* K4 -- chunked-prefill attention over slab blocks (the
+ * prefill block claim is simulator.cpp:500-526).  The chunk's K/V must
+ * already be in the blocks (ks_kv_append).  d_q, d_out: fp16
+ * [T_total][Hq][d], the rows of sequence s being d_cu_q[s]..d_cu_q[s+1]-1
+ * (int32 [batch+1], device), at positions d_ctx_lens[s]-n_s..d_ctx_lens[s]-1
+ * (so d_ctx_lens[s] >= n_s); each query attends causally to keys 0..its
+ * position.  max_q_len >= every n_s (sizes the grid).  d_lse: fp32
+ * [T_total][Hq] natural-log LSE (nullable).  GQA group must divide 8.
+ * No workspace; no host synchronisation. */
+ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
+                           void* d_out, float* d_lse, const int32_t* d_block_table,
+                           uint32_t bt_stride, const int32_t* d_cu_q, const int32_t* d_ctx_lens,
+                           uint32_t batch, uint32_t max_q_len, float sm_scale,
+                           const float* d_kv_scales, void* stream);
+
 /* Spatial sharing between co-located models (MPS-style SM partitioning,
  * PAPER.md section 2.4): cap the persistent K2 grid of the model with slab
  * key `key` at max_ctas CTAs (one CTA per SM), so co-located models' decode

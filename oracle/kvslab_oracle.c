@@ -558,6 +558,65 @@ void orc_paged_decode(const uint8_t* pool, uint64_t slab_size, uint64_t bps, con
   }
 }
 
+/* Chunked-prefill attention over slab blocks (the
+ * prefill claim of simulator.cpp:500-526 reserves the blocks, K1 writes the
+ * chunk's K/V).  Sequence s contributes n_s = cu_q[s+1]-cu_q[s] query tokens
+ * at positions ctx_lens[s]-n_s .. ctx_lens[s]-1; the query at position p
+ * attends keys 0..p (causal).  fp64 softmax over the dequantised bytes. */
+void orc_paged_prefill(const uint8_t* pool, uint64_t slab_size, uint64_t bps, const orc_fmt* f,
+                       uint32_t layer, const uint16_t* q, const int32_t* block_table,
+                       uint32_t bt_stride, const int32_t* cu_q, const int32_t* ctx_lens,
+                       uint32_t batch, double sm_scale, const float* kv_scales, double* out,
+                       double* lse, int nthreads) {
+  const uint32_t H = f->num_kv_heads, Hq = f->num_q_heads, d = f->head_dim,
+                 T = f->tokens_per_block, G = Hq / H;
+  const int64_t units = (int64_t)batch * H;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+  for (int64_t u = 0; u < units; ++u) {
+    uint32_t s = (uint32_t)(u / H), h = (uint32_t)(u % H);
+    int32_t n = ctx_lens[s], nq = cu_q[s + 1] - cu_q[s];
+    if (nq <= 0) continue;
+    double* kk = (double*)malloc(sizeof(double) * (size_t)n * d);
+    double* vv = (double*)malloc(sizeof(double) * (size_t)n * d);
+    double* sc = (double*)malloc(sizeof(double) * (size_t)n);
+    double* qd = (double*)malloc(sizeof(double) * d);
+    for (int32_t t = 0; t < n; ++t) {
+      uint64_t gid = (uint64_t)block_table[(uint64_t)s * bt_stride + (uint32_t)t / T];
+      orc_dequant(pool, slab_size, bps, f, layer, gid, 0, h, (uint32_t)t % T, kv_scales, kk + (size_t)t * d);
+      orc_dequant(pool, slab_size, bps, f, layer, gid, 1, h, (uint32_t)t % T, kv_scales, vv + (size_t)t * d);
+    }
+    for (int32_t i = 0; i < nq; ++i) {
+      const int32_t pos = n - nq + i;
+      const uint64_t row0 = (uint64_t)(cu_q[s] + i) * Hq + h * G;
+      for (uint32_t g = 0; g < G; ++g) {
+        for (uint32_t e = 0; e < d; ++e) qd[e] = orc_f16_to_f32(q[(row0 + g) * d + e]);
+        double m = -INFINITY, l = 0.0;
+        for (int32_t t = 0; t <= pos; ++t) {
+          double dot = 0.0;
+          for (uint32_t e = 0; e < d; ++e) dot += qd[e] * kk[(size_t)t * d + e];
+          sc[t] = dot * sm_scale;
+          m = fmax(m, sc[t]);
+        }
+        for (int32_t t = 0; t <= pos; ++t) {
+          sc[t] = exp(sc[t] - m);
+          l += sc[t];
+        }
+        if (lse) lse[row0 + g] = m + log(l);
+        double* o = out + (row0 + g) * d;
+        for (uint32_t e = 0; e < d; ++e) o[e] = 0.0;
+        for (int32_t t = 0; t <= pos; ++t) {
+          const double p = sc[t] / l;
+          for (uint32_t e = 0; e < d; ++e) o[e] += p * vv[(size_t)t * d + e];
+        }
+      }
+    }
+    free(kk);
+    free(vv);
+    free(sc);
+    free(qd);
+  }
+}
+
 uint64_t orc_decode_bytes(const orc_fmt* f, const int32_t* ctx_lens, uint32_t batch) {
   uint64_t ts = orc_fmt_token_size(f), T = f->tokens_per_block, total = 0;
   for (uint32_t s = 0; s < batch; ++s) {

@@ -118,6 +118,13 @@ void orc_paged_decode(const uint8_t* pool, uint64_t slab_size, uint64_t bps, con
                       int nthreads);
 
 /* algorithmic bytes of one decode launch */
+/* chunked prefill: queries of sequence s are rows cu_q[s]..cu_q[s+1]-1 of q,
+ * at positions ctx_lens[s]-n_s..ctx_lens[s]-1, causal over keys 0..pos */
+void orc_paged_prefill(const uint8_t* pool, uint64_t slab_size, uint64_t bps, const orc_fmt* f,
+                       uint32_t layer, const uint16_t* q, const int32_t* block_table,
+                       uint32_t bt_stride, const int32_t* cu_q, const int32_t* ctx_lens,
+                       uint32_t batch, double sm_scale, const float* kv_scales, double* out,
+                       double* lse, int nthreads);
 uint64_t orc_decode_bytes(const orc_fmt* f, const int32_t* ctx_lens, uint32_t batch);
 
 /* ---------------- compaction plan (K3 restated; new, no reference) --------- */

@@ -71,6 +71,8 @@ lib.orc_append.argtypes = [P, C.c_uint64, C.c_uint64, C.POINTER(orc_fmt), C.c_ui
                            C.c_uint32, P, P, P, C.c_uint32, P]
 lib.orc_paged_decode.argtypes = [P, C.c_uint64, C.c_uint64, C.POINTER(orc_fmt), C.c_uint32, P,
                                  P, C.c_uint32, P, C.c_uint32, C.c_double, P, P, P, C.c_int]
+lib.orc_paged_prefill.argtypes = [P, C.c_uint64, C.c_uint64, C.POINTER(orc_fmt), C.c_uint32, P,
+                                  P, C.c_uint32, P, P, C.c_uint32, C.c_double, P, P, P, C.c_int]
 lib.orc_decode_bytes.argtypes = [C.POINTER(orc_fmt), P, C.c_uint32]
 lib.orc_decode_bytes.restype = C.c_uint64
 for _n in ("orc_fmt_token_size", "orc_fmt_chunk_bytes", "orc_fmt_layer_bytes", "orc_fmt_key",
@@ -125,6 +127,23 @@ def paged_decode(pool_bytes, slab_size, bps, f, layer, q16, table, ctx_lens, sm_
     lib.orc_paged_decode(pool_bytes.ctypes.data, slab_size, bps, C.byref(f), layer,
                          q16.ctypes.data, tb.ctypes.data, tb.shape[1], cl.ctypes.data, B,
                          sm_scale, _p(sc), out.ctypes.data, lse.ctypes.data, nthreads)
+    return out, lse
+
+
+def paged_prefill(pool_bytes, slab_size, bps, f, layer, q16, table, cu_q, ctx_lens, sm_scale,
+                  kv_scales=None, nthreads=1):
+    """Causal chunked-prefill attention (fp64): q16 [T_total, Hq, d] as uint16."""
+    q16 = np.ascontiguousarray(q16, dtype=np.uint16)
+    tb = np.ascontiguousarray(table, dtype=np.int32)
+    cq = np.ascontiguousarray(cu_q, dtype=np.int32)
+    cl = np.ascontiguousarray(ctx_lens, dtype=np.int32)
+    sc = None if kv_scales is None else np.ascontiguousarray(kv_scales, dtype=np.float32)
+    out = np.zeros(q16.shape, dtype=np.float64)
+    lse = np.zeros(q16.shape[:2], dtype=np.float64)
+    lib.orc_paged_prefill(pool_bytes.ctypes.data, slab_size, bps, C.byref(f), layer,
+                          q16.ctypes.data, tb.ctypes.data, tb.shape[1], cq.ctypes.data,
+                          cl.ctypes.data, cl.shape[0], sm_scale, _p(sc), out.ctypes.data,
+                          lse.ctypes.data, nthreads)
     return out, lse
 
 

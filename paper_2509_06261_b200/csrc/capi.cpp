@@ -791,6 +791,52 @@ ks_status ks_paged_decode_append(ks_pool* pool, const ks_kv_format* fmt, uint32_
                      workspace_bytes, stream);
 }
 
+ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
+                           void* d_out, float* d_lse, const int32_t* d_block_table,
+                           uint32_t bt_stride, const int32_t* d_cu_q, const int32_t* d_ctx_lens,
+                           uint32_t batch, uint32_t max_q_len, float sm_scale,
+                           const float* d_kv_scales, void* stream) {
+  return guarded([&] {
+    FmtInfo fi;
+    ks_status st = check_kernel_format(pool, fmt, &fi);
+    if (st != KS_OK) return st;
+    if (layer >= fmt->num_layers) return fail(KS_INVALID_ARGUMENT, "layer out of range");
+    const uint32_t G = fmt->num_q_heads / fmt->num_kv_heads;
+    if (G == 0 || 8 % G != 0) return fail(KS_NOT_SUPPORTED, "prefill needs a GQA group dividing 8");
+    if (batch == 0 || max_q_len == 0) return KS_OK;
+    if (!d_q || !d_out || !d_block_table || !d_cu_q || !d_ctx_lens)
+      return fail(KS_INVALID_ARGUMENT, "null device pointer");
+    if (static_cast<uint64_t>(batch) * fmt->num_kv_heads > 0x7fffffffULL)
+      return fail(KS_NOT_SUPPORTED, "batch x kv heads too large");
+    DeviceGuard g(pool->device);
+    kvslab::PrefillParams p{};
+    p.pool = pool->d_base;
+    p.geom.slab_size = pool->pool->slab_size();
+    p.geom.key = fi.key;
+    p.geom.bps = kvslab::dev::make_fastdiv(static_cast<uint32_t>(pool->pool->blocks_per_slab(fi.key)));
+    p.layer_off = static_cast<uint64_t>(layer) * fi.layer_bytes;
+    p.H = fmt->num_kv_heads;
+    p.G = G;
+    p.q = static_cast<const __half*>(d_q);
+    p.out = static_cast<__half*>(d_out);
+    p.lse = d_lse;
+    p.block_table = d_block_table;
+    p.bt_stride = bt_stride;
+    p.cu_q = d_cu_q;
+    p.ctx_lens = d_ctx_lens;
+    p.batch = batch;
+    p.max_q_len = max_q_len;
+    const float scale = sm_scale > 0.f ? sm_scale : 1.0f / std::sqrt(static_cast<float>(fmt->head_dim));
+    p.sm_scale_log2 = scale * 1.4426950408889634f;
+    p.kv_scales = fmt->kv_dtype == KS_KV_FP8_E4M3 ? d_kv_scales : nullptr;
+    cudaError_t e = kvslab::launch_paged_prefill(p, static_cast<int>(fmt->kv_dtype),
+                                                 static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "paged_prefill launch");
+    ++g_launches;
+    return KS_OK;
+  });
+}
+
 ks_status ks_set_decode_sm_share(ks_pool* pool, uint64_t key, uint32_t max_ctas) {
   return guarded([&] {
     if (!pool) return fail(KS_INVALID_ARGUMENT, "null pool");

@@ -26,26 +26,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "attend.cuh"
 #include "kvslab_device.cuh"
 #include "launch.hpp"
 
 namespace kvslab {
 namespace dev {
-
-constexpr int kD = 128;   // head dim
-constexpr int kTPB = 16;  // tokens per block
-constexpr float kLog2e = 1.4426950408889634f;
-
-template <int FMT>
-struct Geo {
-  static constexpr int kRow = kD * Fmt<FMT>::kBits / 8;  // bytes per token row
-  static constexpr int kChunk = kTPB * kRow;              // bytes per (K|V, head) chunk
-  static constexpr int kParam = FMT == kINT8 ? kTPB * 2 : (FMT == kINT4 ? kTPB * 4 : 0);
-  // integer formats enter the MMA as exact fp16 (q + kBias); the bias is
-  // removed from the 16x8 score tile (kBias * sum(q)) and from O (kBias * sum(p'))
-  static constexpr float kBias = FMT == kINT8 ? 1152.f : (FMT == kINT4 ? 1024.f : 0.f);
-  static constexpr bool kBiased = FMT == kINT8 || FMT == kINT4;
-};
 
 // ------------------------------------------------------------------ cursor
 // Walks the flattened (seq, head, block) space using the per-CTA prefix.
@@ -79,248 +65,6 @@ __device__ __forceinline__ void cursor_next(Cursor& c, const uint32_t* pre, uint
     ++c.s;
   } while (c.s < batch && pre[c.s + 1] == pre[c.s]);
   if (c.s < batch) c.nblk = nblk_of(pre, c.s, H);
-}
-
-// ------------------------------------------------------ fragment loaders
-// Per-thread byte offsets (inside a K or V chunk) of the fragment loads; they
-// only depend on (g, t) so they are computed once per kernel.
-struct FragOff {
-  uint32_t k[4];
-  uint32_t v[4];
-};
-
-// token held in PV k-slot: slot 2t -> ta(t), 2t+1 -> tb(t), +8 for 2t+8/2t+9
-template <int FMT>
-__device__ __forceinline__ int tok_a(int t) {
-  if constexpr (FMT == kFP16) return t;
-  else if constexpr (FMT == kINT4) return (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}
-  else return 2 * t;
-}
-template <int FMT>
-__device__ __forceinline__ int tok_b(int t) {
-  if constexpr (FMT == kFP16) return t + 4;
-  else if constexpr (FMT == kINT4) return 2 + (t & 1) + ((t >> 1) << 2);  // {2,3,6,7}
-  else return 2 * t + 1;
-}
-
-template <int FMT>
-__device__ __forceinline__ FragOff make_offsets(int g, int t) {
-  FragOff o;
-  const int ta = tok_a<FMT>(t), tb = tok_b<FMT>(t);
-  if constexpr (FMT == kFP16) {
-    const int gt = (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}[t]
-#pragma unroll
-    for (int c = 0; c < 4; ++c) o.k[c] = swz(g * 256 + 16 * (8 * (c >> 1) + gt + 2 * (c & 1)));
-    o.v[0] = swz(ta * 256 + 16 * g);
-    o.v[1] = swz(ta * 256 + 16 * (g + 8));
-    o.v[2] = swz(tb * 256 + 16 * g);
-    o.v[3] = swz(tb * 256 + 16 * (g + 8));
-  } else if constexpr (FMT == kFP8 || FMT == kINT8) {
-    o.k[0] = swz(g * 128 + 16 * (2 * t));
-    o.k[1] = swz(g * 128 + 16 * (2 * t + 1));
-    o.k[2] = o.k[3] = 0;
-    o.v[0] = swz(ta * 128 + 16 * g);
-    o.v[1] = swz(tb * 128 + 16 * g);
-    o.v[2] = o.v[3] = 0;
-  } else {
-    o.k[0] = swz(g * 64 + 16 * t);
-    o.k[1] = swz((g + 8) * 64 + 16 * t);
-    o.k[2] = o.k[3] = 0;
-    o.v[0] = swz(ta * 64 + 8 * g);
-    o.v[1] = swz(tb * 64 + 8 * g);
-    o.v[2] = swz((ta + 8) * 64 + 8 * g);
-    o.v[3] = swz((tb + 8) * 64 + 8 * g);
-  }
-  return o;
-}
-
-// K tile as the MMA A operand (rows = tokens g, g+8; k = dims permuted per
-// format).  a[kk][0..3] for k-step kk.  Row g+8 sits 8 rows further, which is
-// a constant (swizzle-preserving) offset for 256- and 128-byte rows.
-template <int FMT>
-__device__ __forceinline__ void load_k_frags(uint32_t sK, const FragOff& o, uint32_t (&a)[8][4]) {
-  if constexpr (FMT == kFP16) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint4 lo = lds128(sK + o.k[c]);
-      const uint4 hi = lds128(sK + o.k[c] + 2048);
-      a[2 * c][0] = lo.x; a[2 * c][1] = hi.x; a[2 * c][2] = lo.y; a[2 * c][3] = hi.y;
-      a[2 * c + 1][0] = lo.z; a[2 * c + 1][1] = hi.z; a[2 * c + 1][2] = lo.w; a[2 * c + 1][3] = hi.w;
-    }
-  } else if constexpr (FMT == kFP8 || FMT == kINT8) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const uint4 lo = lds128(sK + o.k[c]);
-      const uint4 hi = lds128(sK + o.k[c] + 1024);
-      const uint32_t wl[4] = {lo.x, lo.y, lo.z, lo.w};
-      const uint32_t wh[4] = {hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        uint32_t* r = a[4 * c + e];
-        if constexpr (FMT == kFP8) {
-          r[0] = e4m3x2_to_f16x2(static_cast<uint16_t>(wl[e] & 0xffff));
-          r[2] = e4m3x2_to_f16x2(static_cast<uint16_t>(wl[e] >> 16));
-          r[1] = e4m3x2_to_f16x2(static_cast<uint16_t>(wh[e] & 0xffff));
-          r[3] = e4m3x2_to_f16x2(static_cast<uint16_t>(wh[e] >> 16));
-        } else {
-          const uint32_t xl = wl[e] ^ 0x80808080u, xh = wh[e] ^ 0x80808080u;
-          // exact fp16 b + 1152 (the bias is removed after the MMA)
-          r[0] = __byte_perm(xl, 0x64646464u, 0x4140);
-          r[2] = __byte_perm(xl, 0x64646464u, 0x4342);
-          r[1] = __byte_perm(xh, 0x64646464u, 0x4140);
-          r[3] = __byte_perm(xh, 0x64646464u, 0x4342);
-        }
-      }
-    }
-  } else {  // INT4: one granule (32 dims) per row per thread
-    const uint4 lo = lds128(sK + o.k[0]);
-    const uint4 hi = lds128(sK + o.k[1]);
-    const uint32_t wl[4] = {lo.x, lo.y, lo.z, lo.w};
-    const uint32_t wh[4] = {hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        uint32_t* r = a[2 * i + e];
-        const uint32_t xl = e ? wl[i] >> 8 : wl[i], xh = e ? wh[i] >> 8 : wh[i];
-        // exact fp16 1024 + n (low nibble, k-slots 2t, 2t+1) and 1024 + 16 n
-        // (high nibble in place, k-slots 2t+8, 2t+9: their Q entries carry
-        // the 1/16); the 1024 bias is removed after the MMA
-        r[0] = lop3_and_or(xl, 0x000F000Fu, 0x64006400u);
-        r[2] = lop3_and_or(xl, 0x00F000F0u, 0x64006400u);
-        r[1] = lop3_and_or(xh, 0x000F000Fu, 0x64006400u);
-        r[3] = lop3_and_or(xh, 0x00F000F0u, 0x64006400u);
-      }
-    }
-  }
-}
-
-// Q rows of the unit -> MMA B fragments for query g of each n-tile, with the
-// K dims permuted exactly like load_k_frags (the reduction order is free).
-template <int FMT, int NT>
-__device__ __forceinline__ void load_q_frags(uint32_t sQ, int g, int t, uint32_t G,
-                                             uint32_t (&qf)[NT][8][2]) {
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int qrow = nt * 8 + g;
-    const bool ok = qrow < static_cast<int>(G);
-    const uint32_t row = sQ + qrow * kD * 2;
-    if constexpr (FMT == kFP16) {
-      const int gt = (t & 1) + ((t >> 1) << 2);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int gr = 8 * (c >> 1) + gt + 2 * (c & 1);
-        const uint4 v = ok ? lds128(row + 16 * gr) : make_uint4(0, 0, 0, 0);
-        qf[nt][2 * c][0] = v.x; qf[nt][2 * c][1] = v.y;
-        qf[nt][2 * c + 1][0] = v.z; qf[nt][2 * c + 1][1] = v.w;
-      }
-    } else if constexpr (FMT == kFP8 || FMT == kINT8) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {  // dims 32t + 8c .. +7 -> k-steps 2c, 2c+1
-        const uint4 v = ok ? lds128(row + 64 * t + 16 * c) : make_uint4(0, 0, 0, 0);
-        qf[nt][2 * c][0] = v.x; qf[nt][2 * c][1] = v.y;
-        qf[nt][2 * c + 1][0] = v.z; qf[nt][2 * c + 1][1] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {  // dims 32t + 8i .. +7: pairs (0,4),(1,5) | (2,6),(3,7)
-        const uint4 v = ok ? lds128(row + 64 * t + 16 * i) : make_uint4(0, 0, 0, 0);
-        // high-nibble k-slots see K as 1024 + 16 n: their Q entries carry 1/16
-        // (a power of two: exact for normal fp16)
-        qf[nt][2 * i][0] = __byte_perm(v.x, v.z, 0x5410);
-        qf[nt][2 * i][1] = hmul2_u32(__byte_perm(v.x, v.z, 0x7632), 0x2C002C00u);
-        qf[nt][2 * i + 1][0] = __byte_perm(v.y, v.w, 0x5410);
-        qf[nt][2 * i + 1][1] = hmul2_u32(__byte_perm(v.y, v.w, 0x7632), 0x2C002C00u);
-      }
-    }
-  }
-}
-
-// V tile as the MMA A operand of O^T = V^T P^T (rows = dims, k = tokens).
-template <int FMT>
-__device__ __forceinline__ void load_v_frags(uint32_t sV, const FragOff& o, uint32_t (&a)[8][4]) {
-  if constexpr (FMT == kFP16) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint4 va = lds128(sV + o.v[h]);
-      const uint4 vb = lds128(sV + o.v[2 + h]);
-      const uint4 vc = lds128(sV + o.v[h] + 2048);
-      const uint4 vd = lds128(sV + o.v[2 + h] + 2048);
-      const uint32_t A[4] = {va.x, va.y, va.z, va.w}, B[4] = {vb.x, vb.y, vb.z, vb.w};
-      const uint32_t C[4] = {vc.x, vc.y, vc.z, vc.w}, Dd[4] = {vd.x, vd.y, vd.z, vd.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint32_t* r = a[4 * h + i];
-        r[0] = __byte_perm(A[i], B[i], 0x5410);
-        r[1] = __byte_perm(A[i], B[i], 0x7632);
-        r[2] = __byte_perm(C[i], Dd[i], 0x5410);
-        r[3] = __byte_perm(C[i], Dd[i], 0x7632);
-      }
-    }
-  } else if constexpr (FMT == kFP8 || FMT == kINT8) {
-    const uint4 va = lds128(sV + o.v[0]);
-    const uint4 vb = lds128(sV + o.v[1]);
-    const uint4 vc = lds128(sV + o.v[0] + 1024);
-    const uint4 vd = lds128(sV + o.v[1] + 1024);
-    const uint32_t A[4] = {va.x, va.y, va.z, va.w}, B[4] = {vb.x, vb.y, vb.z, vb.w};
-    const uint32_t C[4] = {vc.x, vc.y, vc.z, vc.w}, Dd[4] = {vd.x, vd.y, vd.z, vd.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const uint32_t sel = e == 0 ? 0x5140u : 0x7362u;
-        uint32_t* r = a[2 * j + e];
-        if constexpr (FMT == kFP8) {
-          const uint32_t ab = __byte_perm(A[j], B[j], sel), cd = __byte_perm(C[j], Dd[j], sel);
-          r[0] = e4m3x2_to_f16x2(static_cast<uint16_t>(ab & 0xffff));
-          r[1] = e4m3x2_to_f16x2(static_cast<uint16_t>(ab >> 16));
-          r[2] = e4m3x2_to_f16x2(static_cast<uint16_t>(cd & 0xffff));
-          r[3] = e4m3x2_to_f16x2(static_cast<uint16_t>(cd >> 16));
-        } else {
-          const uint32_t ab = __byte_perm(A[j] ^ 0x80808080u, B[j] ^ 0x80808080u, sel);
-          const uint32_t cd = __byte_perm(C[j] ^ 0x80808080u, Dd[j] ^ 0x80808080u, sel);
-          r[0] = __byte_perm(ab, 0x64646464u, 0x4140);
-          r[1] = __byte_perm(ab, 0x64646464u, 0x4342);
-          r[2] = __byte_perm(cd, 0x64646464u, 0x4140);
-          r[3] = __byte_perm(cd, 0x64646464u, 0x4342);
-        }
-      }
-    }
-  } else {  // INT4: 8 bytes (16 dims) per token per thread
-    const uint2 va = lds64(sV + o.v[0]);
-    const uint2 vb = lds64(sV + o.v[1]);
-    const uint2 vc = lds64(sV + o.v[2]);
-    const uint2 vd = lds64(sV + o.v[3]);
-    const uint32_t A[2] = {va.x, va.y}, B[2] = {vb.x, vb.y}, C[2] = {vc.x, vc.y},
-                   Dd[2] = {vd.x, vd.y};
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int w = i >> 2, k = i & 3;
-      // bytes [A.k, A.k, B.k, B.k]: A.k in the low half, B.k in the high half
-      const uint32_t sel = k | (k << 4) | ((4 + k) << 8) | ((4 + k) << 12);
-      const uint32_t ab = __byte_perm(A[w], B[w], sel);
-      const uint32_t cd = __byte_perm(C[w], Dd[w], sel);
-      uint32_t* r = a[i];
-      // rows g+8 (high nibbles, in place) enter as 1024 + 16 n: the epilogue
-      // divides those output dims by 16
-      r[0] = lop3_and_or(ab, 0x000F000Fu, 0x64006400u);
-      r[1] = lop3_and_or(ab, 0x00F000F0u, 0x64006400u);
-      r[2] = lop3_and_or(cd, 0x000F000Fu, 0x64006400u);
-      r[3] = lop3_and_or(cd, 0x00F000F0u, 0x64006400u);
-    }
-  }
-}
-// output dim of V m-tile mt, row half r8 (0: row g, 1: row g+8)
-template <int FMT>
-__device__ __forceinline__ int vdim(int mt, int g, int r8) {
-  if constexpr (FMT == kFP16) return 64 * (mt >> 2) + 8 * g + 2 * (mt & 3) + r8;
-  else return 16 * g + 2 * mt + r8;
-}
-
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
 }
 
 // First flat index (CTA range start) of CTA c: floor(c * total / C), with
@@ -515,154 +259,6 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, 
 constexpr uint32_t kTrStage = 12288, kTrReady = kTrStage + 148 * 4 * 32;
 __device__ __forceinline__ void trace_ready(const DecodeParams& p, int warp, int lane, uint32_t k) {
   if (p.trace && warp == 0 && lane == 0 && k < 32) p.trace[kTrReady + blockIdx.x * 32 + k] = gtimer();
-}
-
-// Online-softmax state of one warp's (unit segment, head): O^T accumulator
-// tiles, reference max, row sums and the additive terms of biased formats
-// (zb: -bias * sum(P'), zz: sum(p * z_v) for INT4).
-template <int NT>
-struct UnitState {
-  float acc[8][NT][4];
-  float m[NT][2], l[NT][2], zb[NT][2], zz[NT][2];
-};
-
-constexpr float kRescaleSlack = 8.0f;  // log2 units: P <= 2^8 before a rescale
-
-// One consumer step: BPI staged blocks (shared-memory stage addresses sbs,
-// valid token counts) of one head attended by one warp -- S^T = K.Q^T on
-// tensor cores, lazy online softmax, O^T += V^T.P^T.
-template <int FMT, int NT, int BPI, bool MASK = true>
-__device__ __forceinline__ void attend(UnitState<NT>& u, const uint32_t (&sbs)[BPI],
-                                       const int (&valid)[BPI], uint32_t wK, uint32_t wP,
-                                       uint32_t kvq, uint32_t pq, const FragOff& fo,
-                                       const uint32_t (&qf)[NT][8][2], const float (&qsb)[NT][2],
-                                       const float (&qst)[NT][2], float kscale, float sml2, int g,
-                                       int t) {
-  using Gm = Geo<FMT>;
-  // ---- S^T = K . Q^T per block (two accumulators halve the MMA chain) ----
-  float sc[BPI][NT][4], svv[BPI][2], zvv[BPI][2];
-#pragma unroll
-  for (int bi = 0; bi < BPI; ++bi) {
-    uint32_t ka[8][4];
-    load_k_frags<FMT>(sbs[bi] + wK, fo, ka);
-    float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f};
-    svv[bi][0] = svv[bi][1] = 1.f;
-    zvv[bi][0] = zvv[bi][1] = 0.f;
-    const uint32_t sKp = sbs[bi] + wP, sVp = sKp + pq;
-    if constexpr (FMT == kINT8) {
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
-        svv[bi][r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
-      }
-    } else if constexpr (FMT == kINT4) {
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
-        sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
-        zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
-        svv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
-        zvv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
-      }
-    }
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int kk = 0; kk < 8; kk += 2) {
-        mma16816(s1, ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[nt][kk][0], qf[nt][kk][1]);
-        mma16816(s2, ka[kk + 1][0], ka[kk + 1][1], ka[kk + 1][2], ka[kk + 1][3],
-                 qf[nt][kk + 1][0], qf[nt][kk + 1][1]);
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = e >> 1;
-        const float dot = s1[e] + s2[e];
-        float x;
-        if constexpr (Gm::kBiased)  // s * (dot' - bias*sum(q')) + z * sum(q)
-          x = sk[r] * (dot - Gm::kBias * qsb[nt][e & 1]) + zk[r] * qst[nt][e & 1];
-        else
-          x = dot * sk[r];
-        sc[bi][nt][e] = g + 8 * r < valid[bi] ? x * sml2 : -INFINITY;
-      }
-    }
-  }
-
-  // ---- online softmax over the BPI tiles ----
-  // Lazy rescaling: the reference max u.m moves (and O is rescaled) only
-  // when a score exceeds it by kRescaleSlack; the common case costs one vote.
-  uint32_t pb[BPI][NT][2];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    bool grow = false;
-#pragma unroll
-    for (int bi = 0; bi < BPI; ++bi)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) grow |= sc[bi][nt][e] > u.m[nt][e & 1] + kRescaleSlack;
-    if (__any_sync(0xffffffffu, grow)) {
-      float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-      for (int bi = 0; bi < BPI; ++bi) {
-        mx[0] = fmaxf(mx[0], fmaxf(sc[bi][nt][0], sc[bi][nt][2]));
-        mx[1] = fmaxf(mx[1], fmaxf(sc[bi][nt][1], sc[bi][nt][3]));
-      }
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
-        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
-        mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
-        const float mn = fmaxf(u.m[nt][c], mx[c]);
-        const float alpha = ex2(u.m[nt][c] - mn);
-        u.m[nt][c] = mn;
-        u.l[nt][c] *= alpha;
-        u.zb[nt][c] *= alpha;
-        u.zz[nt][c] *= alpha;
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          u.acc[mt][nt][c] *= alpha;
-          u.acc[mt][nt][2 + c] *= alpha;
-        }
-      }
-    }
-#pragma unroll
-    for (int bi = 0; bi < BPI; ++bi) {
-      float pr[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[bi][nt][e] - u.m[nt][e & 1]);
-      const uint32_t plo = pack_h2(pr[0] * svv[bi][0], pr[1] * svv[bi][0]);
-      const uint32_t phi = pack_h2(pr[2] * svv[bi][1], pr[3] * svv[bi][1]);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) u.l[nt][c] += pr[c] + pr[c + 2];
-      if constexpr (Gm::kBiased) {
-        // the bias term uses the exact fp16 P' that the MMA consumes
-        const float2 flo = __half22float2(*reinterpret_cast<const __half2*>(&plo));
-        const float2 fhi = __half22float2(*reinterpret_cast<const __half2*>(&phi));
-        u.zb[nt][0] -= Gm::kBias * (flo.x + fhi.x);
-        u.zb[nt][1] -= Gm::kBias * (flo.y + fhi.y);
-        if constexpr (FMT == kINT4) {
-          u.zz[nt][0] += pr[0] * zvv[bi][0] + pr[2] * zvv[bi][1];
-          u.zz[nt][1] += pr[1] * zvv[bi][0] + pr[3] * zvv[bi][1];
-        }
-      }
-      const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
-      const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
-      const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
-      const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
-      pb[bi][nt][0] = __byte_perm(xa, xb, sel);
-      pb[bi][nt][1] = __byte_perm(ya, yb, sel);
-    }
-  }
-  // ---- O^T += V^T . P^T ----
-#pragma unroll
-  for (int bi = 0; bi < BPI; ++bi) {
-    uint32_t va[8][4];
-    load_v_frags<FMT>(sbs[bi] + kvq + wK, fo, va);
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        mma16816(u.acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[bi][nt][0], pb[bi][nt][1]);
-  }
 }
 
 // Formats whose consumer step runs two full blocks at a time (measured per format
@@ -998,6 +594,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         attend<FMT, NT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
         release();
         release();
+        if ((i & 3) == 2) flush_bias<FMT, NT>(us);  // every kBiasFlush blocks
       }
     }
     for (; i < nfull; ++i) {
@@ -1008,6 +605,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       if (!(p.debug & 8))  // probe: stream only
         attend<FMT, NT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
       release();
+      if (i % kBiasFlush == kBiasFlush - 1) flush_bias<FMT, NT>(us);
     }
     // ---- the unit's last block (partial; holds the appended token) ----
     if (has_last) {

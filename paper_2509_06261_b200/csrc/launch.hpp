@@ -42,6 +42,25 @@ struct DecodeParams {
   unsigned long long* trace;  // probes: per-warp globaltimer stamps (nullable)
 };
 
+struct PrefillParams {
+  const uint8_t* pool;
+  dev::SlabGeom geom;
+  uint64_t layer_off;
+  uint32_t H, G;
+  const __half* q;         // [T_total][H*G][d]
+  __half* out;
+  float* lse;
+  const int32_t* block_table;
+  uint32_t bt_stride;
+  const int32_t* cu_q;     // [batch+1] query-row offsets
+  const int32_t* ctx_lens; // [batch] cached tokens including the chunk
+  uint32_t batch, max_q_len;
+  float sm_scale_log2;
+  const float* kv_scales;  // FP8 [2][H]
+  // filled by the launcher
+  uint32_t tiles, stages, stage_bytes, qbuf_offset, bar_offset;
+};
+
 struct AppendParams {
   uint8_t* pool;
   dev::SlabGeom geom;
@@ -70,6 +89,7 @@ struct CompactParams {
 cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms,
                                 cudaStream_t stream);
 size_t decode_partials_bytes(int num_sms, int G);
+cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStream_t stream);
 cudaError_t launch_kv_append(const AppendParams& p, int kv_dtype, cudaStream_t stream);
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_table_scatter(int32_t* table, uint32_t row_stride, const int32_t* triples,

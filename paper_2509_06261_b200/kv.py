@@ -251,6 +251,32 @@ def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
     return out
 
 
+def paged_prefill(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
+                  block_table: torch.Tensor, cu_q: torch.Tensor, ctx_lens: torch.Tensor,
+                  max_q_len: int, out: Optional[torch.Tensor] = None,
+                  lse: Optional[torch.Tensor] = None, sm_scale: Optional[float] = None,
+                  kv_scales: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """K4: causal chunked-prefill attention over slab blocks.
+
+    q: fp16 [T, Hq, d], the rows of sequence s being cu_q[s]..cu_q[s+1]-1
+    (int32 [B+1], device) at positions ctx_lens[s]-n_s..ctx_lens[s]-1 (int32
+    [B], device; the chunk's K/V already appended with kv_append).  Each query
+    attends keys 0..its position.  max_q_len >= every n_s.  Returns out fp16
+    [T, Hq, d]."""
+    assert q.dtype == torch.float16 and q.is_contiguous()
+    assert block_table.dtype == torch.int32 and ctx_lens.dtype == torch.int32
+    assert cu_q.dtype == torch.int32
+    if out is None:
+        out = torch.empty_like(q)
+    f = fmt.to_c()
+    scale = 0.0 if sm_scale is None else float(sm_scale)
+    check(L.lib.ks_paged_prefill(pool.handle, C.byref(f), layer, _ptr(q), _ptr(out), _ptr(lse),
+                                 _ptr(block_table), block_table.stride(0), _ptr(cu_q),
+                                 _ptr(ctx_lens), ctx_lens.shape[0], int(max_q_len), scale,
+                                 _ptr(kv_scales), _stream(stream)))
+    return out
+
+
 def compact(pool: SlabPool, key: int, max_moves: int = 1 << 20,
             tables: Sequence[torch.Tensor] = (), stream=None) -> Tuple[List[Tuple[int, int]], int]:
     """K3: plan (host, applied to the slab table), move the bytes on the GPU,

@@ -156,6 +156,9 @@ CASES = [
     (KvDtype.INT4, 8, 32, [8192, 17]),
     (KvDtype.INT4, 8, 8, [1, 2, 3, 4, 50, 129]),
     (KvDtype.INT4, 4, 40, [333]),
+    # long contexts: the biased-V accumulator must not lose the signal's low bits
+    (KvDtype.INT4, 8, 32, [16384, 4000, 700, 9000]),
+    (KvDtype.INT8, 2, 16, [16384, 5000]),
 ]
 
 

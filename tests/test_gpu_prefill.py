@@ -1,0 +1,97 @@
+"""GPU parity of K4 chunked-prefill attention against the
+fp64 oracle (oracle/kvslab_oracle.c orc_paged_prefill), through the C ABI.
+
+Sequences mix whole prompts (chunk = context), chunks at the end of an
+existing context, single-token chunks and empty chunks; blocks are scattered
+by allocator churn.  Tolerance as K2: max|o-r| / max|r| per (query token,
+query head) <= 1e-3 (FP16/FP8) or 1e-2 (INT8/INT4); LSE within 1e-3.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2509_06261_b200 import kv
+from paper_2509_06261_b200.kv import KvDtype, KvFormat
+import oracle
+from test_gpu_kernels import FORMATS, TOL, append_gpu, dev, make_world
+
+pytestmark = pytest.mark.gpu
+
+# (context incl. the chunk, chunk length)
+CASES = [(1, 1), (37, 37), (300, 45), (16, 16), (17, 1), (129, 0), (700, 161), (64, 33)]
+
+
+def run_prefill(dt, H, Hq, cases, seed, layers=1, layer=0):
+    fmt = KvFormat(dt, H, Hq, num_layers=layers)
+    ctx = [c for c, _ in cases]
+    nq = [n for _, n in cases]
+    w = make_world(fmt, ctx, seed=seed,
+                   fp8_scale=np.linspace(0.5, 2.0, 2 * H).astype(np.float32)
+                   if dt == KvDtype.FP8_E4M3 else None)
+    append_gpu(w, fmt, layer)
+    cu = np.concatenate([[0], np.cumsum(nq)]).astype(np.int32)
+    q = w["rng"].standard_normal((int(cu[-1]), Hq, 128)).astype(np.float16)
+    lse = torch.zeros((int(cu[-1]), Hq), dtype=torch.float32, device="cuda")
+    out = kv.paged_prefill(w["pool"], fmt, layer, dev(q), dev(w["table"]), dev(cu),
+                           dev(w["ctx"]), max(nq), lse=lse,
+                           kv_scales=None if w["scales"] is None else dev(w["scales"]))
+    torch.cuda.synchronize()
+    img = kv.kv_tensor(w["pool"]).cpu().numpy()
+    f = oracle.fmt(int(dt), H, Hq, 128, layers, 16, fmt.qparams)
+    ref, ref_lse = oracle.paged_prefill(img, w["pool"].slab_size(), w["pool"].blocks_per_slab(fmt.key),
+                                        f, layer, q.view(np.uint16), w["table"], cu, w["ctx"],
+                                        1 / math.sqrt(128), w["scales"], nthreads=8)
+    return w, fmt, q, cu, out.cpu().numpy().astype(np.float64), lse.cpu().numpy(), ref, ref_lse
+
+
+def rel_err(o, r):
+    o = o.reshape(-1, 128)
+    r = r.reshape(-1, 128)
+    return (np.abs(o - r).max(1) / np.maximum(np.abs(r).max(1), 1e-30)).max() if len(r) else 0.0
+
+
+@pytest.mark.parametrize("dt", FORMATS, ids=[d.name for d in FORMATS])
+@pytest.mark.parametrize("H,Hq", [(2, 2), (2, 8), (2, 16)], ids=["mha", "gqa4", "gqa8"])
+def test_prefill_matches_oracle(dt, H, Hq):
+    _, _, _, _, o, lse, r, rl = run_prefill(dt, H, Hq, CASES, seed=11 * int(dt) + Hq)
+    err = rel_err(o, r)
+    assert err <= TOL[dt], f"{dt.name} H={H} Hq={Hq}: rel err {err:.3e}"
+    assert np.abs(lse - rl).max() <= 1e-3
+
+
+def test_prefill_layer_offset_int4():
+    """A non-zero layer of a multi-layer key reads its own sub-blocks."""
+    _, _, _, _, o, _, r, _ = run_prefill(KvDtype.INT4, 2, 8, [(200, 77), (33, 33)], seed=5,
+                                         layers=3, layer=2)
+    assert rel_err(o, r) <= 1e-2
+
+
+@pytest.mark.parametrize("dt", [KvDtype.FP16, KvDtype.INT8], ids=["FP16", "INT8"])
+def test_prefill_last_token_equals_decode(dt):
+    """A one-token chunk at the end of the context is a decode step: K4 and K2
+    see the same bytes and must agree to fp16-rounding level."""
+    H, Hq = 2, 8
+    cases = [(513, 1), (40, 1), (1, 1), (1000, 1)]
+    w, fmt, q, cu, o, _, _, _ = run_prefill(dt, H, Hq, cases, seed=3)
+    dec = kv.paged_decode(w["pool"], fmt, 0, dev(q.reshape(len(cases), Hq, 128)), dev(w["table"]),
+                          dev(w["ctx"]))
+    torch.cuda.synchronize()
+    d = dec.cpu().numpy().astype(np.float64)
+    assert rel_err(o, d) <= 2e-3
+
+
+def test_prefill_long_chunk_fp8():
+    """A 2k-token whole-prompt chunk (many tiles, heaviest first)."""
+    _, _, _, _, o, _, r, _ = run_prefill(KvDtype.FP8_E4M3, 2, 8, [(2048, 2048), (900, 300)], seed=9)
+    assert rel_err(o, r) <= 1e-3
+
+
+def test_prefill_rejects_bad_group():
+    fmt = KvFormat(KvDtype.FP16, 1, 16)
+    w = make_world(fmt, [16], churn=False)
+    q = torch.zeros((16, 16, 128), dtype=torch.float16, device="cuda")
+    cu = dev(np.array([0, 16], np.int32))
+    with pytest.raises(Exception, match="GQA"):
+        kv.paged_prefill(w["pool"], fmt, 0, q, dev(w["table"]), cu, dev(w["ctx"]), 16)
