@@ -802,7 +802,7 @@ ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t laye
     if (st != KS_OK) return st;
     if (layer >= fmt->num_layers) return fail(KS_INVALID_ARGUMENT, "layer out of range");
     const uint32_t G = fmt->num_q_heads / fmt->num_kv_heads;
-    if (G == 0 || 8 % G != 0) return fail(KS_NOT_SUPPORTED, "prefill needs a GQA group dividing 8");
+    if (G == 0 || 16 % G != 0) return fail(KS_NOT_SUPPORTED, "prefill needs a GQA group dividing 16");
     if (batch == 0 || max_q_len == 0) return KS_OK;
     if (!d_q || !d_out || !d_block_table || !d_cu_q || !d_ctx_lens)
       return fail(KS_INVALID_ARGUMENT, "null device pointer");
@@ -829,6 +829,7 @@ ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t laye
     const float scale = sm_scale > 0.f ? sm_scale : 1.0f / std::sqrt(static_cast<float>(fmt->head_dim));
     p.sm_scale_log2 = scale * 1.4426950408889634f;
     p.kv_scales = fmt->kv_dtype == KS_KV_FP8_E4M3 ? d_kv_scales : nullptr;
+    if (const char* nt = std::getenv("KVSLAB_PREFILL_NT")) p.nt = static_cast<uint32_t>(std::atoi(nt));
     cudaError_t e = kvslab::launch_paged_prefill(p, static_cast<int>(fmt->kv_dtype),
                                                  static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "paged_prefill launch");

@@ -26,19 +26,23 @@
 namespace kvslab {
 namespace dev {
 
-constexpr int kPrefillWarps = 8;  // consumer warps per CTA (8 query rows each)
+// consumer warps per CTA: 8*NT query rows each; the CTA (W+1 warps) fits one
+// SM's register file per sub-partition (NT=1: <= 152 regs, NT=2: <= 240)
+template <int NT>
+constexpr int kPrefillWarps = NT == 1 ? 11 : 6;
 
-template <int FMT>
-__global__ void __launch_bounds__((kPrefillWarps + 1) * 32, 1) prefill_kernel(const PrefillParams p) {
+template <int FMT, int NT>
+__global__ void __maxnreg__(NT == 1 ? 152 : 240) prefill_kernel(const PrefillParams p) {
   using Gm = Geo<FMT>;
-  constexpr int W = kPrefillWarps;
+  constexpr int W = kPrefillWarps<NT>;
+  constexpr int R = 8 * NT;  // query rows per consumer warp
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const uint32_t s = blockIdx.x / p.H, h = blockIdx.x % p.H;
   const uint32_t tile = p.tiles - 1 - blockIdx.y;  // heaviest (latest) tiles first
   const int q0 = p.cu_q[s], nq = p.cu_q[s + 1] - q0;
-  const uint32_t G = p.G, TPW = 8 / G;             // tokens per consumer warp
+  const uint32_t G = p.G, TPW = R / G;             // tokens per consumer warp
   const int QT = static_cast<int>(W * TPW);       // tokens per tile
   const int tok0 = static_cast<int>(tile) * QT;
   if (tok0 >= nq) return;  // uniform across the CTA
@@ -98,53 +102,53 @@ __global__ void __launch_bounds__((kPrefillWarps + 1) * 32, 1) prefill_kernel(co
   const int wtok0 = tok0 + warp * static_cast<int>(TPW);
   const int wtok_end = min(tok_end, wtok0 + static_cast<int>(TPW));  // may be <= wtok0
   const uint32_t Hq = p.H * G;
-  uint8_t* sq = smem + p.qbuf_offset + warp * 8 * kD * 2;
-  {
-    // stage the 8 rows (2 KB) in shared memory: lane -> row lane/4, 64 bytes
-    const int r = lane >> 2, part = lane & 3;
+  uint8_t* sq = smem + p.qbuf_offset + warp * R * kD * 2;
+  // stage the warp's R query rows in shared memory (row r = token r/G x head r%G)
+  for (int i = lane; i < R * 16; i += 32) {
+    const int r = i >> 4, part = i & 15;
     const int tok = wtok0 + r / static_cast<int>(G);
-    uint4 v[4] = {};
-    if (tok < wtok_end) {
-      const uint4* src = reinterpret_cast<const uint4*>(
-          p.q + (static_cast<uint64_t>(q0 + tok) * Hq + h * G + r % G) * kD) + part * 4;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = __ldg(src + i);
-    }
-    uint4* dst = reinterpret_cast<uint4*>(sq + r * kD * 2) + part * 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) dst[i] = v[i];
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (tok < wtok_end)
+      v = __ldg(reinterpret_cast<const uint4*>(p.q + (static_cast<uint64_t>(q0 + tok) * Hq + h * G + r % G) * kD) +
+                part);
+    reinterpret_cast<uint4*>(sq + r * kD * 2)[part] = v;
   }
   __syncwarp();
   const FragOff fo = make_offsets<FMT>(g, t);
-  uint32_t qf[1][8][2];
-  load_q_frags<FMT, 1>(smem_u32(sq), g, t, 8, qf);
-  float qsb[1][2] = {{0.f, 0.f}}, qst[1][2] = {{0.f, 0.f}};
-  if constexpr (Gm::kBiased) {
-    float lo = 0.f, hi = 0.f;
+  uint32_t qf[NT][8][2];
+  load_q_frags<FMT, NT>(smem_u32(sq), g, t, R, qf);
+  float qsb[NT][2], qst[NT][2];
+  UnitState<NT> us;
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&qf[0][kk][0]));
-      const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&qf[0][kk][1]));
-      lo += f0.x + f0.y;
-      hi += f1.x + f1.y;
+  for (int nt = 0; nt < NT; ++nt) {
+    qsb[nt][0] = qsb[nt][1] = qst[nt][0] = qst[nt][1] = 0.f;
+    if constexpr (Gm::kBiased) {
+      float lo = 0.f, hi = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const float2 f0 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][0]));
+        const float2 f1 = __half22float2(*reinterpret_cast<__half2*>(&qf[nt][kk][1]));
+        lo += f0.x + f0.y;
+        hi += f1.x + f1.y;
+      }
+      float sbq = lo + hi, stq = FMT == kINT4 ? lo + 16.f * hi : sbq;
+      sbq += __shfl_xor_sync(0xffffffffu, sbq, 1);
+      sbq += __shfl_xor_sync(0xffffffffu, sbq, 2);
+      stq += __shfl_xor_sync(0xffffffffu, stq, 1);
+      stq += __shfl_xor_sync(0xffffffffu, stq, 2);
+      qsb[nt][0] = __shfl_sync(0xffffffffu, sbq, (2 * t) * 4);
+      qsb[nt][1] = __shfl_sync(0xffffffffu, sbq, (2 * t + 1) * 4);
+      qst[nt][0] = __shfl_sync(0xffffffffu, stq, (2 * t) * 4);
+      qst[nt][1] = __shfl_sync(0xffffffffu, stq, (2 * t + 1) * 4);
     }
-    float sbq = lo + hi, stq = FMT == kINT4 ? lo + 16.f * hi : sbq;
-    sbq += __shfl_xor_sync(0xffffffffu, sbq, 1);
-    sbq += __shfl_xor_sync(0xffffffffu, sbq, 2);
-    stq += __shfl_xor_sync(0xffffffffu, stq, 1);
-    stq += __shfl_xor_sync(0xffffffffu, stq, 2);
-    qsb[0][0] = __shfl_sync(0xffffffffu, sbq, (2 * t) * 4);
-    qsb[0][1] = __shfl_sync(0xffffffffu, sbq, (2 * t + 1) * 4);
-    qst[0][0] = __shfl_sync(0xffffffffu, stq, (2 * t) * 4);
-    qst[0][1] = __shfl_sync(0xffffffffu, stq, (2 * t + 1) * 4);
-  }
-  UnitState<1> us;
-  us.m[0][0] = us.m[0][1] = -INFINITY;
-  us.l[0][0] = us.l[0][1] = 0.f;
-  us.zb[0][0] = us.zb[0][1] = 0.f;
-  us.zz[0][0] = us.zz[0][1] = 0.f;
+    us.m[nt][0] = us.m[nt][1] = -INFINITY;
+    us.l[nt][0] = us.l[nt][1] = 0.f;
+    us.zb[nt][0] = us.zb[nt][1] = 0.f;
+    us.zz[nt][0] = us.zz[nt][1] = 0.f;
 #pragma unroll
-  for (int mt = 0; mt < 8; ++mt) us.acc[mt][0][0] = us.acc[mt][0][1] = us.acc[mt][0][2] = us.acc[mt][0][3] = 0.f;
+    for (int mt = 0; mt < 8; ++mt)
+      us.acc[mt][nt][0] = us.acc[mt][nt][1] = us.acc[mt][nt][2] = us.acc[mt][nt][3] = 0.f;
+  }
   float kscale = 1.f, vscale = 1.f;
   if constexpr (FMT == kFP8) {
     if (p.kv_scales) {
@@ -155,12 +159,14 @@ __global__ void __launch_bounds__((kPrefillWarps + 1) * 32, 1) prefill_kernel(co
   // positions of this lane's two query columns (2t, 2t+1); padding columns
   // reuse the warp's last valid position (computed, never stored)
   const int wlast = wtok_end > wtok0 ? pos0 + wtok_end - 1 : pos0;
-  int qpos[2];
+  int qpos[NT][2];
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const int tok = wtok0 + (2 * t + c) / static_cast<int>(G);
-    qpos[c] = tok < wtok_end ? pos0 + tok : wlast;
-  }
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int tok = wtok0 + (nt * 8 + 2 * t + c) / static_cast<int>(G);
+      qpos[nt][c] = tok < wtok_end ? pos0 + tok : wlast;
+    }
   const int wfirst = wtok_end > wtok0 ? pos0 + wtok0 : pos0;
   const uint32_t nb_w = wtok_end > wtok0 ? static_cast<uint32_t>(wlast) / kTPB + 1 : 0u;
   const float sml2 = p.sm_scale_log2;
@@ -173,14 +179,19 @@ __global__ void __launch_bounds__((kPrefillWarps + 1) * 32, 1) prefill_kernel(co
       const int valid[1] = {kTPB};
       const int bstart = static_cast<int>(b) * kTPB;
       if (bstart + kTPB - 1 <= wfirst) {  // every row of the warp sees the whole block
-        attend<FMT, 1, 1, false, false>(us, sbs, valid, 0u, 2 * chunk, chunk, prm, fo, qf, qsb, qst, kscale,
-                                        sml2, g, t);
+        attend<FMT, NT, 1, false, false>(us, sbs, valid, 0u, 2 * chunk, chunk, prm, fo, qf, qsb, qst, kscale,
+                                         sml2, g, t);
       } else {  // diagonal block: causal mask per query column
-        const int lim[1][2] = {{qpos[0] - bstart + 1, qpos[1] - bstart + 1}};
-        attend<FMT, 1, 1, true, true>(us, sbs, valid, 0u, 2 * chunk, chunk, prm, fo, qf, qsb, qst, kscale,
-                                      sml2, g, t, lim);
+        int lim[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          lim[nt][0] = qpos[nt][0] - bstart + 1;
+          lim[nt][1] = qpos[nt][1] - bstart + 1;
+        }
+        attend<FMT, NT, 1, true, true>(us, sbs, valid, 0u, 2 * chunk, chunk, prm, fo, qf, qsb, qst, kscale,
+                                       sml2, g, t, lim);
       }
-      if (b % kBiasFlush == kBiasFlush - 1) flush_bias<FMT, 1>(us);
+      if (b % kBiasFlush == kBiasFlush - 1) flush_bias<FMT, NT>(us);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -191,62 +202,57 @@ __global__ void __launch_bounds__((kPrefillWarps + 1) * 32, 1) prefill_kernel(co
   }
   if (nb_w == 0) return;
   // ---- epilogue: normalise and store the warp's valid rows ----
-  float lf[2], zbf[2], zzf[2];
 #pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    float l = us.l[0][c], zb = us.zb[0][c], zz = us.zz[0][c];
+  for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      l += __shfl_xor_sync(0xffffffffu, l, o);
-      if constexpr (Gm::kBiased) zb += __shfl_xor_sync(0xffffffffu, zb, o);
-      if constexpr (FMT == kINT4) zz += __shfl_xor_sync(0xffffffffu, zz, o);
+    for (int c = 0; c < 2; ++c) {
+      float l = us.l[nt][c], zb = us.zb[nt][c], zz = us.zz[nt][c];
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+        if constexpr (Gm::kBiased) zb += __shfl_xor_sync(0xffffffffu, zb, o);
+        if constexpr (FMT == kINT4) zz += __shfl_xor_sync(0xffffffffu, zz, o);
+      }
+      const int col = nt * 8 + 2 * t + c;
+      const int tok = wtok0 + col / static_cast<int>(G);
+      if (tok >= wtok_end) continue;
+      const float inv = 1.f / l;
+      const uint64_t row = static_cast<uint64_t>(q0 + tok) * Hq + h * G + col % G;
+      __half* orow = p.out + row * kD;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        const int d0 = vdim<FMT>(mt, g, 0);
+        const float lo = us.acc[mt][nt][c] * vscale + zb + zz;
+        float hi;
+        if constexpr (FMT == kINT4) hi = (us.acc[mt][nt][2 + c] + zb) * 0.0625f + zz;
+        else hi = us.acc[mt][nt][2 + c] * vscale + zb + zz;
+        *reinterpret_cast<__half2*>(orow + d0) = __floats2half2_rn(lo * inv, hi * inv);
+      }
+      if (p.lse && g == 0) p.lse[row] = (us.m[nt][c] + __log2f(l)) * 0.69314718055994531f;
     }
-    lf[c] = l;
-    zbf[c] = zb;
-    zzf[c] = zz;
-  }
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const int col = 2 * t + c;
-    const int tok = wtok0 + col / static_cast<int>(G);
-    if (tok >= wtok_end) continue;
-    const float inv = 1.f / lf[c];
-    const uint64_t row = static_cast<uint64_t>(q0 + tok) * Hq + h * G + col % G;
-    __half* orow = p.out + row * kD;
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int d0 = vdim<FMT>(mt, g, 0);
-      const float lo = us.acc[mt][0][c] * vscale + zbf[c] + zzf[c];
-      float hi;
-      if constexpr (FMT == kINT4) hi = (us.acc[mt][0][2 + c] + zbf[c]) * 0.0625f + zzf[c];
-      else hi = us.acc[mt][0][2 + c] * vscale + zbf[c] + zzf[c];
-      *reinterpret_cast<__half2*>(orow + d0) = __floats2half2_rn(lo * inv, hi * inv);
-    }
-    if (p.lse && g == 0) p.lse[row] = (us.m[0][c] + __log2f(lf[c])) * 0.69314718055994531f;
-  }
 }
 
-template <int FMT>
+template <int FMT, int NT>
 static cudaError_t launch_prefill_fmt(const PrefillParams& p0, cudaStream_t stream) {
   using Gm = Geo<FMT>;
+  constexpr int W = kPrefillWarps<NT>;
   PrefillParams p = p0;
   p.stage_bytes = (2 * (Gm::kChunk + Gm::kParam) + 127) / 128 * 128;
-  const uint32_t qbytes = kPrefillWarps * 8 * kD * 2;
+  const uint32_t qbytes = W * 8 * NT * kD * 2;
   uint32_t stages = (200 * 1024 - qbytes) / p.stage_bytes;
   if (stages > 16) stages = 16;
   p.stages = stages;
   p.qbuf_offset = stages * p.stage_bytes;
   p.bar_offset = p.qbuf_offset + qbytes;
   const size_t smem = p.bar_offset + 2 * stages * 8;
-  auto kern = prefill_kernel<FMT>;
+  auto kern = prefill_kernel<FMT, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  const uint32_t tpw = 8 / p.G;
-  const uint32_t qt = kPrefillWarps * tpw;
+  const uint32_t qt = W * (8 * NT / p.G);  // tokens per tile
   p.tiles = (p.max_q_len + qt - 1) / qt;
   if (p.tiles == 0) return cudaSuccess;
-  kern<<<dim3(p.batch * p.H, p.tiles), (kPrefillWarps + 1) * 32, smem, stream>>>(p);
+  kern<<<dim3(p.batch * p.H, p.tiles), (W + 1) * 32, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -254,11 +260,12 @@ static cudaError_t launch_prefill_fmt(const PrefillParams& p0, cudaStream_t stre
 
 cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStream_t stream) {
   using namespace dev;
+  const bool two = p.nt != 1;  // 16 query rows per warp (default); 8 when p.nt == 1
   switch (kv_dtype) {
-    case kFP16: return launch_prefill_fmt<kFP16>(p, stream);
-    case kFP8: return launch_prefill_fmt<kFP8>(p, stream);
-    case kINT8: return launch_prefill_fmt<kINT8>(p, stream);
-    case kINT4: return launch_prefill_fmt<kINT4>(p, stream);
+    case kFP16: return two ? launch_prefill_fmt<kFP16, 2>(p, stream) : launch_prefill_fmt<kFP16, 1>(p, stream);
+    case kFP8: return two ? launch_prefill_fmt<kFP8, 2>(p, stream) : launch_prefill_fmt<kFP8, 1>(p, stream);
+    case kINT8: return two ? launch_prefill_fmt<kINT8, 2>(p, stream) : launch_prefill_fmt<kINT8, 1>(p, stream);
+    case kINT4: return two ? launch_prefill_fmt<kINT4, 2>(p, stream) : launch_prefill_fmt<kINT4, 1>(p, stream);
     default: return cudaErrorInvalidValue;
   }
 }

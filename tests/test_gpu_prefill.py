@@ -53,7 +53,7 @@ def rel_err(o, r):
 
 
 @pytest.mark.parametrize("dt", FORMATS, ids=[d.name for d in FORMATS])
-@pytest.mark.parametrize("H,Hq", [(2, 2), (2, 8), (2, 16)], ids=["mha", "gqa4", "gqa8"])
+@pytest.mark.parametrize("H,Hq", [(2, 2), (2, 8), (2, 16), (2, 32)], ids=["mha", "gqa4", "gqa8", "gqa16"])
 def test_prefill_matches_oracle(dt, H, Hq):
     _, _, _, _, o, lse, r, rl = run_prefill(dt, H, Hq, CASES, seed=11 * int(dt) + Hq)
     err = rel_err(o, r)
@@ -82,6 +82,14 @@ def test_prefill_last_token_equals_decode(dt):
     assert rel_err(o, d) <= 2e-3
 
 
+@pytest.mark.parametrize("nt", ["1", "2"])
+def test_prefill_row_tiling_variants(nt, monkeypatch):
+    """Both warp tilings (8 or 16 query rows per warp) agree with the oracle."""
+    monkeypatch.setenv("KVSLAB_PREFILL_NT", nt)
+    _, _, _, _, o, _, r, _ = run_prefill(KvDtype.INT8, 2, 8, [(300, 45), (700, 161), (5, 5)], seed=21)
+    assert rel_err(o, r) <= 1e-2
+
+
 def test_prefill_long_chunk_fp8():
     """A 2k-token whole-prompt chunk (many tiles, heaviest first)."""
     _, _, _, _, o, _, r, _ = run_prefill(KvDtype.FP8_E4M3, 2, 8, [(2048, 2048), (900, 300)], seed=9)
@@ -89,9 +97,9 @@ def test_prefill_long_chunk_fp8():
 
 
 def test_prefill_rejects_bad_group():
-    fmt = KvFormat(KvDtype.FP16, 1, 16)
+    fmt = KvFormat(KvDtype.FP16, 1, 32)
     w = make_world(fmt, [16], churn=False)
-    q = torch.zeros((16, 16, 128), dtype=torch.float16, device="cuda")
+    q = torch.zeros((16, 32, 128), dtype=torch.float16, device="cuda")
     cu = dev(np.array([0, 16], np.int32))
     with pytest.raises(Exception, match="GQA"):
         kv.paged_prefill(w["pool"], fmt, 0, q, dev(w["table"]), cu, dev(w["ctx"]), 16)
