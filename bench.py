@@ -47,6 +47,7 @@ P.add_argument("--layers", type=int, default=32)
 P.add_argument("--batch", type=int, default=16)
 P.add_argument("--ctx", type=int, default=2048)
 P.add_argument("--no-cpu-baseline", action="store_true")
+P.add_argument("--no-sweep", action="store_true", help="skip the per-format K2 / K4 sweep")
 P.add_argument("--profile", action="store_true", help="one eager step, no timing (for ncu)")
 ARGS = P.parse_args()
 
@@ -266,6 +267,93 @@ class Clocks:
                           if s[2 + i].lower().startswith("active")})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+def format_sweep(peak):
+    """K2 decode of each KV precision alone (Llama-3-8B shape, 8-layer CUDA
+    graph of fused append+decode launches, per-launch average, algorithmic
+    bytes) and K4 chunked prefill (whole 4k prompt, causal FLOPs vs the
+    measured dense fp16/bf16 tensor peak).  Reported beside the headline; not
+    part of the timed step."""
+    import torch
+    import paper_2509_06261_b200 as ks
+    from paper_2509_06261_b200 import kv
+    from paper_2509_06261_b200.engine import SlabModel
+    from paper_2509_06261_b200.kv import KvDtype, KvFormat
+    pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    tpeak = pk.get("bf16_tflops", 2250.0)
+    Ls = 8
+    res = {"decode": {}, "prefill": {}}
+
+    def world(dt, B, ctx0):
+        fmt = KvFormat(dt, HKV, HQ, D, Ls)
+        slab = fmt.key * 16
+        nb = (ctx0 + 15) // 16 + 1
+        pool = ks.SlabPool(ks.SlabPoolConfig((B * nb // 16 + 4) * slab, slab, [fmt.key]), device=0)
+        m = SlabModel(pool, fmt, B, nb)
+        for s_ in range(B):
+            assert m.admit(s_, ctx0)
+        m.sync()
+        return fmt, pool, m
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    for B, ctx0 in ((16, 2048), (64, 4096)):
+        row = {}
+        for dt in (KvDtype.FP16, KvDtype.FP8_E4M3, KvDtype.INT8, KvDtype.INT4):
+            fmt, pool, m = world(dt, B, ctx0)
+            ctx = torch.full((B,), ctx0, dtype=torch.int32, device="cuda")
+            qs = [torch.randn(B, HQ, D, dtype=torch.float16, device="cuda") for _ in range(Ls)]
+            kn = torch.randn(B, HKV, D, dtype=torch.float16, device="cuda")
+            sc = torch.ones(2 * HKV, device="cuda")
+            ws = kv.DecodeWorkspace(pool, fmt, B)
+            g = torch.cuda.CUDAGraph()
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for layer in range(Ls):
+                    kv.paged_decode(pool, fmt, layer, qs[layer], m.table, ctx, kv_scales=sc,
+                                    workspace=ws, k_new=kn, v_new=kn)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=st):
+                    for layer in range(Ls):
+                        kv.paged_decode(pool, fmt, layer, qs[layer], m.table, ctx, kv_scales=sc,
+                                        workspace=ws, k_new=kn, v_new=kn)
+            ms = timed(g.replay, 10) / Ls
+            by = fmt.decode_bytes([ctx0] * B)
+            gbs = by / (ms / 1e3) / 1e9
+            row[dt.name.lower()] = {"us": round(ms * 1e3, 2), "gbs": round(gbs, 1),
+                                    "frac": round(gbs / peak, 4)}
+            del g, pool
+        res["decode"][f"B{B}_ctx{ctx0}"] = row
+    nq = 4096
+    for dt in (KvDtype.FP16, KvDtype.INT4):
+        fmt, pool, m = world(dt, 1, nq)
+        ctx = torch.full((1,), nq, dtype=torch.int32, device="cuda")
+        cu = torch.tensor([0, nq], dtype=torch.int32, device="cuda")
+        q = torch.randn(nq, HQ, D, dtype=torch.float16, device="cuda")
+        out = torch.empty_like(q)
+        sc = torch.ones(2 * HKV, device="cuda")
+        ms = timed(lambda: kv.paged_prefill(pool, fmt, 0, q, m.table, cu, ctx, nq, out=out,
+                                            kv_scales=sc), 10)
+        flops = 4.0 * D * HQ * nq * (nq + 1) / 2
+        tf = flops / (ms / 1e3) / 1e12
+        res["prefill"][dt.name.lower()] = {"workload": "1 seq, whole 4096-token prompt, causal",
+                                           "us": round(ms * 1e3, 1), "tflops": round(tf, 1),
+                                           "frac": round(tf / tpeak, 4), "bound": "tensor"}
+        del pool
+    res["decode"]["note"] = ("K2 alone per KV precision: 8-layer graph of fused append+decode, "
+                             "per-launch average, algorithmic bytes / measured HBM copy peak")
+    return res
 
 
 def run_ours():
@@ -551,6 +639,11 @@ def run_ours():
         by = m.fmt.decode_bytes(cl)
         rl[["fp16", "fp8"][mi]] = (by, per_launch_ms)
 
+    # every KV precision's K2 alone (outside the timed region, rank 0 / N=1
+    # only): the bench shape and a large batch, 8-layer graphs
+    sweep = format_sweep(peaks()[0]) if (RANK == 0 and WORLD == 1 and not ARGS.no_sweep) else None
+    del pool
+
     # ---- reduce over ranks (max time) ----
     from paper_2509_06261_b200.placement import reduce_max
     ms, e2e_ms = reduce_max(ms), reduce_max(e2e_ms)
@@ -594,6 +687,7 @@ def run_ours():
         "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(gpu_launches),
+        **({"formats": sweep["decode"], "prefill": sweep["prefill"]} if sweep else {}),
         "clocks": clk.summary(),
     }
     if not ARGS.no_cpu_baseline:
