@@ -158,7 +158,7 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, 
   }
   const uint32_t hdr = (2 * G + 3) & ~3u;
   const uint32_t slot_f = hdr + G * kD;
-  constexpr int SB = DC == 1 ? 4 : (DC == 2 ? 6 : 8);
+  constexpr int SB = DC == 1 ? 4 : (DC == 2 ? 8 : 10);  // loads in flight (<= 56 registers)
   const uint32_t d0 = dc * (kD / DC) + lane * VW;  // first dim of this lane
   float M = -INFINITY, L = 0.f;
   float o[VW];
@@ -775,7 +775,8 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   while (ws < 32 && ws * 4 * 2 < segs && p.G * 32 * ws * 2 <= mt) ws *= 2;
   // and few (sequence, head) merges are spread over DC CTAs each (dims split)
   const uint32_t heads = p.batch * p.H;
-  const int DC = heads >= 64 ? 1 : (heads >= 32 ? 2 : 4);
+  int DC = heads >= 64 ? 1 : (heads >= 32 ? 2 : 4);
+  if (p.merge_dc == 1 || p.merge_dc == 2 || p.merge_dc == 4) DC = static_cast<int>(p.merge_dc);  // probe override
   cudaLaunchConfig_t mcfg = cfg;
   mcfg.gridDim = dim3(heads * DC);
   mcfg.blockDim = dim3(p.G * 32 * ws);

@@ -37,6 +37,7 @@ struct DecodeParams {
   uint32_t hg_max;        // 0 = default head-group size
   uint32_t smem_budget;   // ring bytes per CTA; 0 = default
   uint32_t merge_threads; // merge CTA size cap; 0 = default (256)
+  uint32_t merge_dc;      // probe override of the merge's dims split (0 = auto)
   int debug;     // bit0: skip math, bit1: skip partial merge (probes only)
   int pdl;       // launch with programmatic stream serialization
   unsigned long long* trace;  // probes: per-warp globaltimer stamps (nullable)
