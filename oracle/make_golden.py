@@ -157,8 +157,33 @@ def main():
     np.savez_compressed(os.path.join(OUT, "churn.npz"), **arrays)
     with open(os.path.join(OUT, "churn.json"), "w") as f:
         json.dump(meta, f, indent=1)
+    c5()
     print("golden vectors written to", OUT)
 
 
+def c5():
+    """BASELINE configs[4]: the reference's own placement (place_models,
+    placement.cpp:135-205) of 16 mixed-precision models onto 8 B200 groups and
+    its Poisson trace (generate_workload, workload.cpp:130-190), from
+    oracle/_ref/ref_c5 (oracle/ref_c5.cpp)."""
+    out = subprocess.run([os.path.join(HERE, "_ref", "ref_c5")], capture_output=True, text=True,
+                         check=True).stdout.splitlines()
+    models, assign, reqs = [], {}, []
+    for l in out:
+        t = l.split()
+        if t[0] == "K":
+            models.append({"name": t[1], "kv_bits": int(t[2]), "key": int(t[3])})
+        elif t[0] == "A":
+            assign[t[1]] = t[2]
+        elif t[0] == "R":
+            reqs.append([int(t[1]), t[2], float(t[3]), int(t[4]), int(t[5])])
+    with open(os.path.join(OUT, "c5.json"), "w") as f:
+        json.dump({"cite": "oracle/ref_c5.cpp -> placement.cpp:135-205, workload.cpp:130-190",
+                   "models": models, "assign": assign, "requests": reqs}, f, indent=0)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "c5":
+        c5()
+    else:
+        main()
