@@ -115,7 +115,13 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, 
   const uint32_t G = p.G;
   const uint32_t q = warp / WS, w = warp % WS;
   const int ctx_s = p.ctx_lens[s];
-  if (ctx_s <= 0) return;  // empty sequence: written by decode CTA 0
+  // CTA 0 always waits for the decode grid, so this grid never completes
+  // before it (a PDL successor that waits on the merge then also sees the
+  // decode kernel's direct outputs, even when every unit was whole)
+  if (ctx_s <= 0) {  // empty sequence: written by decode CTA 0
+    if (blockIdx.x == 0) pdl_wait();
+    return;
+  }
   // blocks before sequence s and in total (ctx_lens is not written by the
   // PDL predecessor: same contract as the decode kernel's prologue)
   uint32_t before = 0, all = 0;
@@ -145,7 +151,10 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, 
   const uint32_t U0 = before * NG + grp * nblk;
   const CtaSplit sp = make_split(total, effective_ctas(total, grid));
   const uint32_t ca = cta_of(U0, sp), cb = cta_of(U0 + nblk - 1, sp);
-  if (ca == cb) return;  // whole unit: the decode kernel wrote it
+  if (ca == cb) {  // whole unit: the decode kernel wrote it
+    if (blockIdx.x == 0) pdl_wait();
+    return;
+  }
   // the unit is the last segment of CTA ca (its first if it starts there)
   // and the first segment of every later CTA
   const uint32_t slot_a = cta_start(ca, sp) < U0 ? 1u : 0u;
