@@ -58,7 +58,7 @@ struct PrefillParams {
   uint32_t batch, max_q_len;
   float sm_scale_log2;
   const float* kv_scales;  // FP8 [2][H]
-  uint32_t nt;  // query rows per warp / 8 (1 or 2; 0 = default 2)
+  uint32_t nt;  // query rows per warp / 8 (1 or 2; 0 = default: 1, or 2 when G > 8)
   // filled by the launcher
   uint32_t tiles, stages, stage_bytes, qbuf_offset, bar_offset;
 };

@@ -171,13 +171,41 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 240) prefill_kernel(const PrefillPar
   const uint32_t nb_w = wtok_end > wtok0 ? static_cast<uint32_t>(wlast) / kTPB + 1 : 0u;
   const float sml2 = p.sm_scale_log2;
   const uint32_t ring = smem_u32(smem);
-  uint32_t st = 0, ph = 0;
-  for (uint32_t b = 0; b < nb; ++b) {
+  uint32_t st = 0, ph = 0, since_flush = 0;
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (++st == S) {
+      st = 0;
+      ph ^= 1;
+    }
+  };
+  for (uint32_t b = 0; b < nb;) {
+    const int bstart = static_cast<int>(b) * kTPB;
+    if constexpr (NT == 1) {
+      // two whole blocks per step (independent score tiles: more ILP)
+      if (b + 1 < nb_w && bstart + 2 * kTPB - 1 <= wfirst) {
+        const uint32_t st1 = st + 1 == S ? 0 : st + 1, ph1 = st + 1 == S ? ph ^ 1 : ph;
+        mbar_wait(&full[st], ph);
+        mbar_wait(&full[st1], ph1);
+        const uint32_t sbs[2] = {ring + st * p.stage_bytes, ring + st1 * p.stage_bytes};
+        const int valid[2] = {kTPB, kTPB};
+        attend<FMT, NT, 2, false, false>(us, sbs, valid, 0u, 2 * chunk, chunk, prm, fo, qf, qsb, qst, kscale,
+                                         sml2, g, t);
+        release();
+        release();
+        b += 2;
+        if ((since_flush += 2) >= kBiasFlush) {
+          flush_bias<FMT, NT>(us);
+          since_flush = 0;
+        }
+        continue;
+      }
+    }
     mbar_wait(&full[st], ph);
     if (b < nb_w) {
       const uint32_t sbs[1] = {ring + st * p.stage_bytes};
       const int valid[1] = {kTPB};
-      const int bstart = static_cast<int>(b) * kTPB;
       if (bstart + kTPB - 1 <= wfirst) {  // every row of the warp sees the whole block
         attend<FMT, NT, 1, false, false>(us, sbs, valid, 0u, 2 * chunk, chunk, prm, fo, qf, qsb, qst, kscale,
                                          sml2, g, t);
@@ -191,14 +219,13 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 240) prefill_kernel(const PrefillPar
         attend<FMT, NT, 1, true, true>(us, sbs, valid, 0u, 2 * chunk, chunk, prm, fo, qf, qsb, qst, kscale,
                                        sml2, g, t, lim);
       }
-      if (b % kBiasFlush == kBiasFlush - 1) flush_bias<FMT, NT>(us);
+      if (++since_flush >= kBiasFlush) {
+        flush_bias<FMT, NT>(us);
+        since_flush = 0;
+      }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-    if (++st == S) {
-      st = 0;
-      ph ^= 1;
-    }
+    release();
+    ++b;
   }
   if (nb_w == 0) return;
   // ---- epilogue: normalise and store the warp's valid rows ----
@@ -260,7 +287,8 @@ static cudaError_t launch_prefill_fmt(const PrefillParams& p0, cudaStream_t stre
 
 cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStream_t stream) {
   using namespace dev;
-  const bool two = p.nt != 1;  // 16 query rows per warp (default); 8 when p.nt == 1
+  // 8 query rows per warp (default: more warps, two-block steps) or 16 (GQA 16)
+  const bool two = p.nt == 2 || p.G > 8;
   switch (kv_dtype) {
     case kFP16: return two ? launch_prefill_fmt<kFP16, 2>(p, stream) : launch_prefill_fmt<kFP16, 1>(p, stream);
     case kFP8: return two ? launch_prefill_fmt<kFP8, 2>(p, stream) : launch_prefill_fmt<kFP8, 1>(p, stream);
