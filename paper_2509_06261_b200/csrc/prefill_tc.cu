@@ -1,0 +1,318 @@
+// prefill_tc.cu -- K4 on the 5th-generation tensor cores (tcgen05 / TMEM),
+// FP16 KV.  Same contract and oracle as prefill.cu (orc_paged_prefill, 1e-3).
+//
+// One CTA (4 warps) per (sequence, kv head, tile of 128 query rows = 128/G
+// tokens x the G query heads).  The rows are the M=128 operand of UMMA:
+//   S[128 x 64]  = Q[128 x 128] . K_t^T           (8 x tcgen05.mma K=16, TMEM)
+//   O[128 x 128] += P[128 x 64] . V_t[64 x 128]   (4 x tcgen05.mma K=16, TMEM)
+// per KV tile t of 64 tokens (4 slab blocks).  Thread r owns query row r: it
+// reads its S row from TMEM (tcgen05.ld 32x32b), runs the online softmax with
+// no shuffles (lazy rescale: O is rescaled in TMEM only when the row max grows
+// by more than 2^8), and writes its P row into shared memory.  Operands live
+// in shared memory in the UMMA canonical 128-byte-swizzled layouts (Q, K, P
+// K-major; V token-major = MN-major B), so the slab chunk's own swizzled rows
+// are re-laid out by the cp.async copies themselves:
+// each 16-byte granule goes from its slab position straight to its operand
+// position, double-buffered one tile ahead.  Blocks past the sequence are
+// zero-filled.  Thread 0 issues the MMAs; tcgen05.commit signals mbarriers.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "attend.cuh"
+#include "kvslab_device.cuh"
+#include "launch.hpp"
+
+namespace kvslab {
+namespace dev {
+namespace tc {
+
+constexpr uint32_t kRows = 128;   // UMMA M: query rows per CTA
+constexpr uint32_t kTile = 64;    // KV tokens per tile (UMMA N of S, K of PV)
+constexpr uint32_t kThreads = 128;
+// shared memory map (1024-aligned): Q | K[2] | V[2] | P
+constexpr uint32_t kQ = 0, kQBytes = kRows * kD * 2;                // 32 KB
+constexpr uint32_t kK = kQ + kQBytes, kKVBytes = kTile * kD * 2;     // 16 KB each
+constexpr uint32_t kV = kK + 2 * kKVBytes;
+constexpr uint32_t kP = kV + 2 * kKVBytes, kPBytes = kRows * kTile * 2;  // 16 KB
+constexpr uint32_t kSmem = kP + kPBytes;
+constexpr uint32_t kTmemCols = 256;  // S: [0, 64), O: [64, 192)
+constexpr uint32_t kTmemO = kTile;
+
+// byte offset of element (row, k) of a K-major 128B-swizzled operand whose
+// 64-element column j is a [rows][128 B] region
+__device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t gran /*16B of the 128B row*/) {
+  return row * 128 + ((gran ^ (row & 7)) << 4);
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(lbo >> 4) << 16) |
+         (static_cast<uint64_t>(sbo >> 4) << 32) | (1ull << 46) | (2ull << 61);  // sm100, SWIZZLE_128B
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// 32 consecutive TMEM columns of this thread's lane -> registers
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 2) prefill_tc_fp16_kernel(const PrefillParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar_s, bar_pv;
+  __shared__ uint32_t tmem_base;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t s = blockIdx.x / p.H, h = blockIdx.x % p.H;
+  const uint32_t G = p.G, TPT = kRows / G;  // tokens per tile
+  const uint32_t tile = p.tiles - 1 - blockIdx.y;
+  const int q0 = p.cu_q[s], nq = p.cu_q[s + 1] - q0;
+  const int tok0 = static_cast<int>(tile * TPT);
+  if (tok0 >= nq) return;
+  const int ctx = p.ctx_lens[s];
+  const int pos0 = ctx - nq;
+  const int tok_end = min(nq, tok0 + static_cast<int>(TPT));
+  const int pos_last = pos0 + tok_end - 1;
+  const uint32_t ntiles = static_cast<uint32_t>(pos_last) / kTile + 1;
+  const uint32_t nblk = (static_cast<uint32_t>(ctx) + kTPB - 1) / kTPB;
+  const uint32_t Hq = p.H * G;
+  const uint32_t sbase = smem_u32(smem);
+
+  if (tid == 0) {
+    mbar_init(&bar_s, 1);
+    mbar_init(&bar_pv, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+
+  // ---- Q tile: row r = token r/G x head r%G, 16 granules of 16 B ----
+  for (uint32_t i = tid; i < kRows * 16; i += kThreads) {
+    const uint32_t r = i >> 4, c = i & 15;
+    const int tok = tok0 + static_cast<int>(r / G);
+    const bool ok = tok < tok_end;
+    const __half* src = p.q + (static_cast<uint64_t>(ok ? q0 + tok : q0) * Hq + h * G + r % G) * kD + c * 8;
+    cp_async16(sbase + kQ + (c >> 3) * (kRows * 128) + sw128(r, c & 7), src, ok ? 16u : 0u);
+  }
+  // ---- K/V tile t (4 slab blocks of head h) -> K-major K, token-major V ----
+  const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
+  auto load_tile = [&](uint32_t t, uint32_t buf) {
+    for (uint32_t i = tid; i < 2 * 4 * 256; i += kThreads) {
+      const uint32_t kv = i >> 10, bi = (i >> 8) & 3, gi = i & 255;  // gi: physical granule of the chunk
+      const uint32_t b = t * 4 + bi;
+      const bool ok = b < nblk;
+      const uint32_t gid = ok ? static_cast<uint32_t>(__ldg(bt + b)) : 0u;
+      const uint8_t* chunk = p.pool + block_offset(p.geom, gid) + p.layer_off +
+                             static_cast<uint64_t>(kv * p.H + h) * (kTPB * kD * 2);
+      const uint32_t line = gi >> 3, cl = (gi & 7) ^ (line & 7);  // logical granule within the line
+      const uint32_t tt = line >> 1, half = line & 1;
+      const uint32_t row = bi * kTPB + tt;
+      const uint32_t dst = sbase + (kv ? kV : kK) + buf * kKVBytes + half * (kTile * 128) + sw128(row, cl);
+      cp_async16(dst, chunk + gi * 16, ok ? 16u : 0u);
+    }
+    cp_async_commit();
+  };
+  load_tile(0, 0);
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  // instruction descriptors: fp32 accumulate, fp16 A/B, M=128; S: N=64, K-major B;
+  // PV: N=128, MN-major B (V token-major)
+  const uint32_t idesc_s = (1u << 4) | ((kTile >> 3) << 17) | ((kRows >> 4) << 24);
+  const uint32_t idesc_pv = (1u << 4) | (1u << 16) | ((kD >> 3) << 17) | ((kRows >> 4) << 24);
+
+  // this thread's query row
+  const uint32_t r = tid;
+  const int rtok = tok0 + static_cast<int>(r / G);
+  const bool rvalid = rtok < tok_end;
+  const int rpos = rvalid ? pos0 + rtok : pos_last;
+  const uint32_t trow = tmem + ((warp * 32) << 16);  // TMEM lane quarter of this warp
+  const float sml2 = p.sm_scale_log2;
+  float m = -INFINITY, l = 0.f;
+  uint32_t ph_s = 0, ph_pv = 0;
+
+  for (uint32_t t = 0; t < ntiles; ++t) {
+    const uint32_t buf = t & 1;
+    cp_async_wait_all();  // tile t (and at t = 0, Q) landed
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (uint32_t k = 0; k < kD / 16; ++k) {
+        const uint64_t ad = umma_desc(sbase + kQ + (k >> 2) * (kRows * 128) + (k & 3) * 32, 16, 1024);
+        const uint64_t bd = umma_desc(sbase + kK + buf * kKVBytes + (k >> 2) * (kTile * 128) + (k & 3) * 32, 16, 1024);
+        umma_f16(tmem, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+      }
+      umma_commit(&bar_s);
+    }
+    if (t > 0) {  // PV(t-1) done: P and the other K/V buffer are free
+      mbar_wait(&bar_pv, ph_pv);
+      ph_pv ^= 1;
+    }
+    if (t + 1 < ntiles) load_tile(t + 1, buf ^ 1);
+    mbar_wait(&bar_s, ph_s);
+    ph_s ^= 1;
+    tc_fence_after();
+    // ---- online softmax of row r over this tile's 64 keys ----
+    float sc[kTile];
+    {
+      float a[32], b2[32];
+      tmem_ld32(trow + 0, a);
+      tmem_ld32(trow + 32, b2);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        sc[j] = a[j] * sml2;
+        sc[32 + j] = b2[j] * sml2;
+      }
+    }
+    const int kbase = static_cast<int>(t * kTile);
+    if (kbase + static_cast<int>(kTile) - 1 > rpos) {  // diagonal tile: causal mask
+#pragma unroll
+      for (int j = 0; j < static_cast<int>(kTile); ++j)
+        if (kbase + j > rpos) sc[j] = -INFINITY;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < static_cast<int>(kTile); ++j) mx = fmaxf(mx, sc[j]);
+    // lazy rescale (P <= 2^8 stays exact in fp16); the TMEM accesses are
+    // warp-collective, so a warp rescales when any of its rows needs it
+    const bool grow = mx > m + kRescaleSlack;
+    const float alpha = grow ? ex2(m - mx) : 1.f;
+    if (t > 0 && __any_sync(0xffffffffu, grow)) {
+#pragma unroll
+      for (uint32_t c = 0; c < kD; c += 32) {
+        float o[32];
+        tmem_ld32(trow + kTmemO + c, o);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] *= alpha;
+        tmem_st32(trow + kTmemO + c, o);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    if (grow) {
+      l *= alpha;
+      m = mx;
+    }
+    uint8_t* prow = smem + kP;
+#pragma unroll
+    for (uint32_t c = 0; c < kTile / 8; ++c) {  // 8 keys -> one 16-byte granule of the P row
+      float pv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        pv[j] = ex2(sc[c * 8 + j] - m);
+        l += pv[j];
+      }
+      uint4 w;
+      w.x = pack_h2(pv[0], pv[1]);
+      w.y = pack_h2(pv[2], pv[3]);
+      w.z = pack_h2(pv[4], pv[5]);
+      w.w = pack_h2(pv[6], pv[7]);
+      *reinterpret_cast<uint4*>(prow + sw128(r, c)) = w;
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (uint32_t k = 0; k < kTile / 16; ++k) {
+        const uint64_t ad = umma_desc(sbase + kP + k * 32, 16, 1024);
+        const uint64_t bd = umma_desc(sbase + kV + buf * kKVBytes + k * 2048, kTile * 128, 1024);
+        umma_f16(tmem + kTmemO, ad, bd, idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
+      }
+      umma_commit(&bar_pv);
+    }
+  }
+  mbar_wait(&bar_pv, ph_pv);
+  tc_fence_after();
+  // ---- epilogue: O row / l -> fp16 (TMEM loads are warp-collective) ----
+  const float inv = 1.f / l;
+  __half* orow = p.out + (static_cast<uint64_t>(q0 + (rvalid ? rtok : 0)) * Hq + h * G + r % G) * kD;
+#pragma unroll
+  for (uint32_t c = 0; c < kD; c += 32) {
+    float o[32];
+    tmem_ld32(trow + kTmemO + c, o);
+    if (rvalid) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 w;
+        w.x = pack_h2(o[j] * inv, o[j + 1] * inv);
+        w.y = pack_h2(o[j + 2] * inv, o[j + 3] * inv);
+        w.z = pack_h2(o[j + 4] * inv, o[j + 5] * inv);
+        w.w = pack_h2(o[j + 6] * inv, o[j + 7] * inv);
+        *reinterpret_cast<uint4*>(orow + c + j) = w;
+      }
+    }
+  }
+  if (rvalid && p.lse)
+    p.lse[static_cast<uint64_t>(q0 + rtok) * Hq + h * G + r % G] = (m + __log2f(l)) * 0.69314718055994531f;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+}  // namespace tc
+}  // namespace dev
+
+cudaError_t launch_paged_prefill_tc(const PrefillParams& p0, cudaStream_t stream) {
+  using namespace dev::tc;
+  PrefillParams p = p0;
+  const uint32_t tpt = kRows / p.G;
+  p.tiles = (p.max_q_len + tpt - 1) / tpt;
+  if (p.tiles == 0) return cudaSuccess;
+  const size_t smem = kSmem + 1024;  // + alignment slack
+  cudaError_t e = cudaFuncSetAttribute(dev::tc::prefill_tc_fp16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  dev::tc::prefill_tc_fp16_kernel<<<dim3(p.batch * p.H, p.tiles), kThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace kvslab
