@@ -831,8 +831,9 @@ ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t laye
     p.sm_scale_log2 = scale * 1.4426950408889634f;
     p.kv_scales = fmt->kv_dtype == KS_KV_FP8_E4M3 ? d_kv_scales : nullptr;
     if (const char* nt = std::getenv("KVSLAB_PREFILL_NT")) p.nt = static_cast<uint32_t>(std::atoi(nt));
-    p.use_tc = 1;
+    p.use_tc = 2;
     if (const char* tc = std::getenv("KVSLAB_PREFILL_TC")) p.use_tc = std::atoi(tc);
+    if (const char* dbg = std::getenv("KVSLAB_PREFILL_DEBUG")) p.debug = std::atoi(dbg);
     cudaError_t e = kvslab::launch_paged_prefill(p, static_cast<int>(fmt->kv_dtype),
                                                  static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "paged_prefill launch");

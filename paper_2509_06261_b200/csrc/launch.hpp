@@ -59,7 +59,8 @@ struct PrefillParams {
   float sm_scale_log2;
   const float* kv_scales;  // FP8 [2][H]
   uint32_t nt;  // query rows per warp / 8 (1 or 2; 0 = default: 1, or 2 when G > 8)
-  int use_tc;   // FP16 KV: tcgen05 kernel (prefill_tc.cu) unless 0
+  int use_tc;   // FP16 KV on tcgen05 (prefill_tc.cu): 2 = warp-specialised (default), 1 = v1, 0 = mma.sync
+  int debug;    // probes: bit0 no KV loads after the first two tiles, bit1 no softmax math
   // filled by the launcher
   uint32_t tiles, stages, stage_bytes, qbuf_offset, bar_offset;
 };

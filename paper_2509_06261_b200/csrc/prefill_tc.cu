@@ -196,13 +196,16 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_tc_fp16_kernel(const Pref
       mbar_wait(&bar_pv, ph_pv);
       ph_pv ^= 1;
     }
-    if (t + 1 < ntiles) load_tile(t + 1, buf ^ 1);
+    if (t + 1 < ntiles && (!(p.debug & 1) || t < 1)) load_tile(t + 1, buf ^ 1);
     mbar_wait(&bar_s, ph_s);
     ph_s ^= 1;
     tc_fence_after();
     // ---- online softmax of row r over this tile's 64 keys ----
     float sc[kTile];
-    {
+    if (p.debug & 2) {
+#pragma unroll
+      for (int j = 0; j < static_cast<int>(kTile); ++j) sc[j] = 0.f;
+    } else {
       float a[32], b2[32];
       tmem_ld32(trow + 0, a);
       tmem_ld32(trow + 32, b2);
@@ -298,12 +301,273 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_tc_fp16_kernel(const Pref
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
+
+// ---------------------------------------------------------------------------
+// v2: warp-specialised, two query tiles per CTA (FA4-style ping-pong).
+//   warps 0-3 / 4-7: softmax of query tile A / B (thread = row)
+//   warp 8 lane 0  : MMA issuer (S_A, S_B, PV_A, PV_B in a software pipeline)
+//   warps 9-11     : cp.async loaders (Q tiles, then a 3-stage K/V ring)
+// While one tile's softmax runs the tensor core works on the other tile, and
+// the K/V ring keeps two tiles in flight.  TMEM: S_A | S_B | O_A | O_B.
+constexpr uint32_t kStages = 3;
+constexpr uint32_t kLoadWarp0 = 9, kLoaders = 96, kThreads2 = 384;
+constexpr uint32_t k2Q = 0;                                 // 2 x 32 KB
+constexpr uint32_t k2KV = 2 * kQBytes;                      // stages x (K 16 KB | V 16 KB)
+constexpr uint32_t k2P = k2KV + kStages * 2 * kKVBytes;     // 2 x 16 KB
+constexpr uint32_t k2Smem = k2P + 2 * kPBytes;
+constexpr uint32_t k2TmemCols = 512;
+
+__device__ __forceinline__ void tmem_ld32_to(uint32_t taddr, float* v) {
+  float t[32];
+  tmem_ld32(taddr, t);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = t[i];
+}
+
+__global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const PrefillParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t q_full, kv_full[kStages], kv_empty[kStages], s_full[2], p_full[2], o_final;
+  __shared__ uint32_t tmem_base;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t s = blockIdx.x / p.H, h = blockIdx.x % p.H;
+  const uint32_t G = p.G, TPC = 2 * kRows / G;  // tokens per CTA
+  const uint32_t tile = p.tiles - 1 - blockIdx.y;
+  const int q0 = p.cu_q[s], nq = p.cu_q[s + 1] - q0;
+  const int tok0 = static_cast<int>(tile * TPC);
+  if (tok0 >= nq) return;
+  const int ctx = p.ctx_lens[s];
+  const int pos0 = ctx - nq;
+  const int tok_end = min(nq, tok0 + static_cast<int>(TPC));
+  const int pos_last = pos0 + tok_end - 1;
+  const uint32_t ntiles = static_cast<uint32_t>(pos_last) / kTile + 1;
+  const uint32_t nblk = (static_cast<uint32_t>(ctx) + kTPB - 1) / kTPB;
+  const uint32_t Hq = p.H * G;
+  const uint32_t sbase = smem_u32(smem);
+
+  if (tid == 0) {
+    mbar_init(&q_full, kLoaders);
+    for (uint32_t i = 0; i < kStages; ++i) {
+      mbar_init(&kv_full[i], kLoaders);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], kRows);
+    }
+    mbar_init(&o_final, 1);
+    fence_mbar_init();
+  }
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(k2TmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp >= kLoadWarp0) {
+    // ============================ loaders ============================
+    const uint32_t lt = tid - kLoadWarp0 * 32;
+    for (uint32_t i = lt; i < 2 * kRows * 16; i += kLoaders) {
+      const uint32_t x = i >> 11, rem = i & 2047, r = rem >> 4, c = rem & 15;
+      const uint32_t rr = x * kRows + r;
+      const int tok = tok0 + static_cast<int>(rr / G);
+      const bool ok = tok < tok_end;
+      const __half* src = p.q + (static_cast<uint64_t>(ok ? q0 + tok : q0) * Hq + h * G + rr % G) * kD + c * 8;
+      cp_async16(sbase + k2Q + x * kQBytes + (c >> 3) * (kRows * 128) + sw128(r, c & 7), src, ok ? 16u : 0u);
+    }
+    cp_async_commit();
+    const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t st = t % kStages;
+      if (t >= kStages) mbar_wait(&kv_empty[st], ((t / kStages) - 1) & 1);
+      const uint32_t kb = sbase + k2KV + st * 2 * kKVBytes;
+      for (uint32_t i = lt; i < 2 * 4 * 256; i += kLoaders) {
+        const uint32_t kv = i >> 10, bi = (i >> 8) & 3, gi = i & 255;
+        const uint32_t b = t * 4 + bi;
+        const bool ok = b < nblk;
+        const uint32_t gid = ok ? static_cast<uint32_t>(__ldg(bt + b)) : 0u;
+        const uint8_t* chunk = p.pool + block_offset(p.geom, gid) + p.layer_off +
+                               static_cast<uint64_t>(kv * p.H + h) * (kTPB * kD * 2);
+        const uint32_t line = gi >> 3, cl = (gi & 7) ^ (line & 7);
+        const uint32_t row = bi * kTPB + (line >> 1);
+        cp_async16(kb + kv * kKVBytes + (line & 1) * (kTile * 128) + sw128(row, cl), chunk + gi * 16,
+                   ok ? 16u : 0u);
+      }
+      cp_async_commit();
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // the previous group (Q, or tile t-1) landed
+      fence_proxy_async();
+      mbar_arrive(t == 0 ? &q_full : &kv_full[(t - 1) % kStages]);
+    }
+    cp_async_wait_all();
+    fence_proxy_async();
+    mbar_arrive(&kv_full[(ntiles - 1) % kStages]);
+  } else if (warp == 8) {
+    // ============================ MMA issuer ============================
+    if (lane == 0) {
+      const uint32_t idesc_s = (1u << 4) | ((kTile >> 3) << 17) | ((kRows >> 4) << 24);
+      const uint32_t idesc_pv = (1u << 4) | (1u << 16) | ((kD >> 3) << 17) | ((kRows >> 4) << 24);
+      auto mma_s = [&](uint32_t x, uint32_t st) {
+#pragma unroll
+        for (uint32_t k = 0; k < kD / 16; ++k) {
+          const uint64_t ad = umma_desc(sbase + k2Q + x * kQBytes + (k >> 2) * (kRows * 128) + (k & 3) * 32, 16, 1024);
+          const uint64_t bd =
+              umma_desc(sbase + k2KV + st * 2 * kKVBytes + (k >> 2) * (kTile * 128) + (k & 3) * 32, 16, 1024);
+          umma_f16(tmem + x * kTile, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[x]);
+      };
+      auto mma_pv = [&](uint32_t x, uint32_t st, bool first) {
+#pragma unroll
+        for (uint32_t k = 0; k < kTile / 16; ++k) {
+          const uint64_t ad = umma_desc(sbase + k2P + x * kPBytes + k * 32, 16, 1024);
+          const uint64_t bd = umma_desc(sbase + k2KV + st * 2 * kKVBytes + kKVBytes + k * 2048, kTile * 128, 1024);
+          umma_f16(tmem + 2 * kTile + x * kD, ad, bd, idesc_pv, (!first || k > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(&q_full, 0);
+      tc_fence_after();
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t st = t % kStages, pst = (t + kStages - 1) % kStages;
+        mbar_wait(&kv_full[st], (t / kStages) & 1);
+        tc_fence_after();
+        if (t > 0) {
+          mbar_wait(&p_full[0], (t - 1) & 1);
+          tc_fence_after();
+          mma_pv(0, pst, t == 1);
+        }
+        mma_s(0, st);
+        if (t > 0) {
+          mbar_wait(&p_full[1], (t - 1) & 1);
+          tc_fence_after();
+          mma_pv(1, pst, t == 1);
+          umma_commit(&kv_empty[pst]);
+        }
+        mma_s(1, st);
+      }
+      const uint32_t lst = (ntiles - 1) % kStages;
+      mbar_wait(&p_full[0], (ntiles - 1) & 1);
+      tc_fence_after();
+      mma_pv(0, lst, ntiles == 1);
+      mbar_wait(&p_full[1], (ntiles - 1) & 1);
+      tc_fence_after();
+      mma_pv(1, lst, ntiles == 1);
+      umma_commit(&o_final);
+    }
+    __syncwarp();
+  } else {
+    // ============================ softmax (row per thread) ============================
+    const uint32_t x = warp >> 2, r = tid & (kRows - 1);
+    const uint32_t rr = x * kRows + r;
+    const int rtok = tok0 + static_cast<int>(rr / G);
+    const bool rvalid = rtok < tok_end;
+    const int rpos = rvalid ? pos0 + rtok : pos_last;
+    const uint32_t lanes = ((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lanes + x * kTile, tO = tmem + lanes + 2 * kTile + x * kD;
+    const float sml2 = p.sm_scale_log2;
+    uint8_t* prow = smem + k2P + x * kPBytes;
+    float m = -INFINITY, l = 0.f;
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      mbar_wait(&s_full[x], t & 1);
+      tc_fence_after();
+      float sc[kTile];
+      tmem_ld32_to(tS, sc);
+      tmem_ld32_to(tS + 32, sc + 32);
+      const int kbase = static_cast<int>(t * kTile);
+#pragma unroll
+      for (int j = 0; j < static_cast<int>(kTile); ++j) {
+        sc[j] *= sml2;
+        if (kbase + j > rpos) sc[j] = -INFINITY;
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < static_cast<int>(kTile); ++j) mx = fmaxf(mx, sc[j]);
+      const bool grow = mx > m + kRescaleSlack;
+      const float alpha = grow ? ex2(m - mx) : 1.f;
+      // PV of tile t-1 completed before s_full[x] of tile t (issue order), so
+      // O and this tile's P buffer are free
+      if (t > 0 && __any_sync(0xffffffffu, grow)) {
+#pragma unroll
+        for (uint32_t c = 0; c < kD; c += 32) {
+          float o[32];
+          tmem_ld32(tO + c, o);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] *= alpha;
+          tmem_st32(tO + c, o);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      if (grow) {
+        l *= alpha;
+        m = mx;
+      }
+#pragma unroll
+      for (uint32_t c = 0; c < kTile / 8; ++c) {
+        float pv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          pv[j] = ex2(sc[c * 8 + j] - m);
+          l += pv[j];
+        }
+        uint4 w;
+        w.x = pack_h2(pv[0], pv[1]);
+        w.y = pack_h2(pv[2], pv[3]);
+        w.z = pack_h2(pv[4], pv[5]);
+        w.w = pack_h2(pv[6], pv[7]);
+        *reinterpret_cast<uint4*>(prow + sw128(r, c)) = w;
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&p_full[x]);
+    }
+    mbar_wait(&o_final, 0);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __half* orow = p.out + (static_cast<uint64_t>(q0 + (rvalid ? rtok : 0)) * Hq + h * G + rr % G) * kD;
+#pragma unroll
+    for (uint32_t c = 0; c < kD; c += 32) {
+      float o[32];
+      tmem_ld32(tO + c, o);
+      if (rvalid) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 w;
+          w.x = pack_h2(o[j] * inv, o[j + 1] * inv);
+          w.y = pack_h2(o[j + 2] * inv, o[j + 3] * inv);
+          w.z = pack_h2(o[j + 4] * inv, o[j + 5] * inv);
+          w.w = pack_h2(o[j + 6] * inv, o[j + 7] * inv);
+          *reinterpret_cast<uint4*>(orow + c + j) = w;
+        }
+      }
+    }
+    if (rvalid && p.lse)
+      p.lse[static_cast<uint64_t>(q0 + rtok) * Hq + h * G + rr % G] = (m + __log2f(l)) * 0.69314718055994531f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(k2TmemCols));
+}
+
 }  // namespace tc
 }  // namespace dev
 
 cudaError_t launch_paged_prefill_tc(const PrefillParams& p0, cudaStream_t stream) {
   using namespace dev::tc;
   PrefillParams p = p0;
+  if (p.use_tc != 1) {  // v2 (default): warp-specialised, two query tiles per CTA
+    const uint32_t tpc = 2 * kRows / p.G;
+    p.tiles = (p.max_q_len + tpc - 1) / tpc;
+    if (p.tiles == 0) return cudaSuccess;
+    const size_t smem2 = k2Smem + 1024;
+    cudaError_t e2 = cudaFuncSetAttribute(dev::tc::prefill_tc2_fp16_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
+    if (e2 != cudaSuccess) return e2;
+    dev::tc::prefill_tc2_fp16_kernel<<<dim3(p.batch * p.H, p.tiles), kThreads2, smem2, stream>>>(p);
+    return cudaGetLastError();
+  }
   const uint32_t tpt = kRows / p.G;
   p.tiles = (p.max_q_len + tpt - 1) / tpt;
   if (p.tiles == 0) return cudaSuccess;
