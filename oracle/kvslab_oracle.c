@@ -383,6 +383,17 @@ static uint64_t params_off(const orc_fmt* f, uint32_t layer) {
   return (uint64_t)layer * orc_fmt_layer_bytes(f) + 2ULL * f->num_kv_heads * orc_fmt_chunk_bytes(f);
 }
 
+/* FP16 element i of token slot: 64-element halves are stored half-major
+ * ([dims 0-63 of all T tokens][dims 64-127 of all T tokens], 128-byte rows),
+ * so each half of a chunk is a 128B-swizzled UMMA operand as it lies
+ * (DESIGN.md section 3); head dims that are not a multiple of 64 keep plain
+ * token rows. */
+static uint64_t fp16_off(const orc_fmt* f, uint32_t slot, uint32_t i) {
+  const uint32_t d = f->head_dim, T = f->tokens_per_block;
+  if (d % 64 != 0) return orc_swz((uint64_t)slot * d * 2 + 2ULL * i);
+  return orc_swz((uint64_t)(i / 64) * T * 128 + (uint64_t)slot * 128 + 2ULL * (i % 64));
+}
+
 /* ======================= quantised append (K1 restated) ================== */
 static void quant_row(const orc_fmt* f, const uint16_t* x16, float fp8_scale, uint8_t* chunk,
                       uint32_t slot, uint8_t* params, uint32_t kv, uint32_t head) {
@@ -393,7 +404,7 @@ static void quant_row(const orc_fmt* f, const uint16_t* x16, float fp8_scale, ui
   for (uint32_t i = 0; i < d; ++i) x[i] = orc_f16_to_f32(x16[i]);
   if (f->kv_dtype == ORC_FP16) {
     for (uint32_t i = 0; i < d; ++i) {
-      uint64_t o = orc_swz(base + 2 * i);
+      uint64_t o = fp16_off(f, slot, i);
       chunk[o] = (uint8_t)(x16[i] & 0xff);
       chunk[o + 1] = (uint8_t)(x16[i] >> 8);
     }
@@ -477,7 +488,7 @@ void orc_dequant(const uint8_t* pool, uint64_t slab_size, uint64_t bps, const or
   uint64_t rowb = (uint64_t)d * fmt_bits(f) / 8, base = (uint64_t)slot * rowb;
   if (f->kv_dtype == ORC_FP16) {
     for (uint32_t i = 0; i < d; ++i) {
-      uint64_t o = orc_swz(base + 2 * i);
+      uint64_t o = fp16_off(f, slot, i);
       out[i] = orc_f16_to_f32((uint16_t)(chunk[o] | (chunk[o + 1] << 8)));
     }
   } else if (f->kv_dtype == ORC_FP8) {

@@ -56,11 +56,12 @@ __device__ __forceinline__ FragOff make_offsets(int g, int t) {
   if constexpr (FMT == kFP16) {
     const int gt = (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}[t]
 #pragma unroll
-    for (int c = 0; c < 4; ++c) o.k[c] = swz(g * 256 + 16 * (8 * (c >> 1) + gt + 2 * (c & 1)));
-    o.v[0] = swz(ta * 256 + 16 * g);
-    o.v[1] = swz(ta * 256 + 16 * (g + 8));
-    o.v[2] = swz(tb * 256 + 16 * g);
-    o.v[3] = swz(tb * 256 + 16 * (g + 8));
+    // half-major chunk: dims 64h.. of token t at h*2048 + t*128 (16 tokens)
+    for (int c = 0; c < 4; ++c) o.k[c] = swz((c >> 1) * 2048 + g * 128 + 16 * (gt + 2 * (c & 1)));
+    o.v[0] = swz(ta * 128 + 16 * g);
+    o.v[1] = swz(2048 + ta * 128 + 16 * g);
+    o.v[2] = swz(tb * 128 + 16 * g);
+    o.v[3] = swz(2048 + tb * 128 + 16 * g);
   } else if constexpr (FMT == kFP8 || FMT == kINT8) {
     o.k[0] = swz(g * 128 + 16 * (2 * t));
     o.k[1] = swz(g * 128 + 16 * (2 * t + 1));
@@ -89,7 +90,7 @@ __device__ __forceinline__ void load_k_frags(uint32_t sK, const FragOff& o, uint
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const uint4 lo = lds128(sK + o.k[c]);
-      const uint4 hi = lds128(sK + o.k[c] + 2048);
+      const uint4 hi = lds128(sK + o.k[c] + 1024);  // token g+8: 8 rows on
       a[2 * c][0] = lo.x; a[2 * c][1] = hi.x; a[2 * c][2] = lo.y; a[2 * c][3] = hi.y;
       a[2 * c + 1][0] = lo.z; a[2 * c + 1][1] = hi.z; a[2 * c + 1][2] = lo.w; a[2 * c + 1][3] = hi.w;
     }
@@ -190,8 +191,8 @@ __device__ __forceinline__ void load_v_frags(uint32_t sV, const FragOff& o, uint
     for (int h = 0; h < 2; ++h) {
       const uint4 va = lds128(sV + o.v[h]);
       const uint4 vb = lds128(sV + o.v[2 + h]);
-      const uint4 vc = lds128(sV + o.v[h] + 2048);
-      const uint4 vd = lds128(sV + o.v[2 + h] + 2048);
+      const uint4 vc = lds128(sV + o.v[h] + 1024);  // tokens +8: 8 rows on
+      const uint4 vd = lds128(sV + o.v[2 + h] + 1024);
       const uint32_t A[4] = {va.x, va.y, va.z, va.w}, B[4] = {vb.x, vb.y, vb.z, vb.w};
       const uint32_t C[4] = {vc.x, vc.y, vc.z, vc.w}, Dd[4] = {vd.x, vd.y, vd.z, vd.w};
 #pragma unroll

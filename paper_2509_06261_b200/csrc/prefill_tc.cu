@@ -97,211 +97,6 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 2) prefill_tc_fp16_kernel(const PrefillParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_s, bar_pv;
-  __shared__ uint32_t tmem_base;
-  const uint32_t tid = threadIdx.x, warp = tid >> 5;
-  const uint32_t s = blockIdx.x / p.H, h = blockIdx.x % p.H;
-  const uint32_t G = p.G, TPT = kRows / G;  // tokens per tile
-  const uint32_t tile = p.tiles - 1 - blockIdx.y;
-  const int q0 = p.cu_q[s], nq = p.cu_q[s + 1] - q0;
-  const int tok0 = static_cast<int>(tile * TPT);
-  if (tok0 >= nq) return;
-  const int ctx = p.ctx_lens[s];
-  const int pos0 = ctx - nq;
-  const int tok_end = min(nq, tok0 + static_cast<int>(TPT));
-  const int pos_last = pos0 + tok_end - 1;
-  const uint32_t ntiles = static_cast<uint32_t>(pos_last) / kTile + 1;
-  const uint32_t nblk = (static_cast<uint32_t>(ctx) + kTPB - 1) / kTPB;
-  const uint32_t Hq = p.H * G;
-  const uint32_t sbase = smem_u32(smem);
-
-  if (tid == 0) {
-    mbar_init(&bar_s, 1);
-    mbar_init(&bar_pv, 1);
-    fence_mbar_init();
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-
-  // ---- Q tile: row r = token r/G x head r%G, 16 granules of 16 B ----
-  for (uint32_t i = tid; i < kRows * 16; i += kThreads) {
-    const uint32_t r = i >> 4, c = i & 15;
-    const int tok = tok0 + static_cast<int>(r / G);
-    const bool ok = tok < tok_end;
-    const __half* src = p.q + (static_cast<uint64_t>(ok ? q0 + tok : q0) * Hq + h * G + r % G) * kD + c * 8;
-    cp_async16(sbase + kQ + (c >> 3) * (kRows * 128) + sw128(r, c & 7), src, ok ? 16u : 0u);
-  }
-  // ---- K/V tile t (4 slab blocks of head h) -> K-major K, token-major V ----
-  const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
-  auto load_tile = [&](uint32_t t, uint32_t buf) {
-    for (uint32_t i = tid; i < 2 * 4 * 256; i += kThreads) {
-      const uint32_t kv = i >> 10, bi = (i >> 8) & 3, gi = i & 255;  // gi: physical granule of the chunk
-      const uint32_t b = t * 4 + bi;
-      const bool ok = b < nblk;
-      const uint32_t gid = ok ? static_cast<uint32_t>(__ldg(bt + b)) : 0u;
-      const uint8_t* chunk = p.pool + block_offset(p.geom, gid) + p.layer_off +
-                             static_cast<uint64_t>(kv * p.H + h) * (kTPB * kD * 2);
-      const uint32_t line = gi >> 3, cl = (gi & 7) ^ (line & 7);  // logical granule within the line
-      const uint32_t tt = line >> 1, half = line & 1;
-      const uint32_t row = bi * kTPB + tt;
-      const uint32_t dst = sbase + (kv ? kV : kK) + buf * kKVBytes + half * (kTile * 128) + sw128(row, cl);
-      cp_async16(dst, chunk + gi * 16, ok ? 16u : 0u);
-    }
-    cp_async_commit();
-  };
-  load_tile(0, 0);
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_base;
-  // instruction descriptors: fp32 accumulate, fp16 A/B, M=128; S: N=64, K-major B;
-  // PV: N=128, MN-major B (V token-major)
-  const uint32_t idesc_s = (1u << 4) | ((kTile >> 3) << 17) | ((kRows >> 4) << 24);
-  const uint32_t idesc_pv = (1u << 4) | (1u << 16) | ((kD >> 3) << 17) | ((kRows >> 4) << 24);
-
-  // this thread's query row
-  const uint32_t r = tid;
-  const int rtok = tok0 + static_cast<int>(r / G);
-  const bool rvalid = rtok < tok_end;
-  const int rpos = rvalid ? pos0 + rtok : pos_last;
-  const uint32_t trow = tmem + ((warp * 32) << 16);  // TMEM lane quarter of this warp
-  const float sml2 = p.sm_scale_log2;
-  float m = -INFINITY, l = 0.f;
-  uint32_t ph_s = 0, ph_pv = 0;
-
-  for (uint32_t t = 0; t < ntiles; ++t) {
-    const uint32_t buf = t & 1;
-    cp_async_wait_all();  // tile t (and at t = 0, Q) landed
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-#pragma unroll
-      for (uint32_t k = 0; k < kD / 16; ++k) {
-        const uint64_t ad = umma_desc(sbase + kQ + (k >> 2) * (kRows * 128) + (k & 3) * 32, 16, 1024);
-        const uint64_t bd = umma_desc(sbase + kK + buf * kKVBytes + (k >> 2) * (kTile * 128) + (k & 3) * 32, 16, 1024);
-        umma_f16(tmem, ad, bd, idesc_s, k > 0 ? 1u : 0u);
-      }
-      umma_commit(&bar_s);
-    }
-    if (t > 0) {  // PV(t-1) done: P and the other K/V buffer are free
-      mbar_wait(&bar_pv, ph_pv);
-      ph_pv ^= 1;
-    }
-    if (t + 1 < ntiles && (!(p.debug & 1) || t < 1)) load_tile(t + 1, buf ^ 1);
-    mbar_wait(&bar_s, ph_s);
-    ph_s ^= 1;
-    tc_fence_after();
-    // ---- online softmax of row r over this tile's 64 keys ----
-    float sc[kTile];
-    if (p.debug & 2) {
-#pragma unroll
-      for (int j = 0; j < static_cast<int>(kTile); ++j) sc[j] = 0.f;
-    } else {
-      float a[32], b2[32];
-      tmem_ld32(trow + 0, a);
-      tmem_ld32(trow + 32, b2);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        sc[j] = a[j] * sml2;
-        sc[32 + j] = b2[j] * sml2;
-      }
-    }
-    const int kbase = static_cast<int>(t * kTile);
-    if (kbase + static_cast<int>(kTile) - 1 > rpos) {  // diagonal tile: causal mask
-#pragma unroll
-      for (int j = 0; j < static_cast<int>(kTile); ++j)
-        if (kbase + j > rpos) sc[j] = -INFINITY;
-    }
-    float mx = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < static_cast<int>(kTile); ++j) mx = fmaxf(mx, sc[j]);
-    // lazy rescale (P <= 2^8 stays exact in fp16); the TMEM accesses are
-    // warp-collective, so a warp rescales when any of its rows needs it
-    const bool grow = mx > m + kRescaleSlack;
-    const float alpha = grow ? ex2(m - mx) : 1.f;
-    if (t > 0 && __any_sync(0xffffffffu, grow)) {
-#pragma unroll
-      for (uint32_t c = 0; c < kD; c += 32) {
-        float o[32];
-        tmem_ld32(trow + kTmemO + c, o);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) o[j] *= alpha;
-        tmem_st32(trow + kTmemO + c, o);
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-    if (grow) {
-      l *= alpha;
-      m = mx;
-    }
-    uint8_t* prow = smem + kP;
-#pragma unroll
-    for (uint32_t c = 0; c < kTile / 8; ++c) {  // 8 keys -> one 16-byte granule of the P row
-      float pv[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        pv[j] = ex2(sc[c * 8 + j] - m);
-        l += pv[j];
-      }
-      uint4 w;
-      w.x = pack_h2(pv[0], pv[1]);
-      w.y = pack_h2(pv[2], pv[3]);
-      w.z = pack_h2(pv[4], pv[5]);
-      w.w = pack_h2(pv[6], pv[7]);
-      *reinterpret_cast<uint4*>(prow + sw128(r, c)) = w;
-    }
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-#pragma unroll
-      for (uint32_t k = 0; k < kTile / 16; ++k) {
-        const uint64_t ad = umma_desc(sbase + kP + k * 32, 16, 1024);
-        const uint64_t bd = umma_desc(sbase + kV + buf * kKVBytes + k * 2048, kTile * 128, 1024);
-        umma_f16(tmem + kTmemO, ad, bd, idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
-      }
-      umma_commit(&bar_pv);
-    }
-  }
-  mbar_wait(&bar_pv, ph_pv);
-  tc_fence_after();
-  // ---- epilogue: O row / l -> fp16 (TMEM loads are warp-collective) ----
-  const float inv = 1.f / l;
-  __half* orow = p.out + (static_cast<uint64_t>(q0 + (rvalid ? rtok : 0)) * Hq + h * G + r % G) * kD;
-#pragma unroll
-  for (uint32_t c = 0; c < kD; c += 32) {
-    float o[32];
-    tmem_ld32(trow + kTmemO + c, o);
-    if (rvalid) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        uint4 w;
-        w.x = pack_h2(o[j] * inv, o[j + 1] * inv);
-        w.y = pack_h2(o[j + 2] * inv, o[j + 3] * inv);
-        w.z = pack_h2(o[j + 4] * inv, o[j + 5] * inv);
-        w.w = pack_h2(o[j + 6] * inv, o[j + 7] * inv);
-        *reinterpret_cast<uint4*>(orow + c + j) = w;
-      }
-    }
-  }
-  if (rvalid && p.lse)
-    p.lse[static_cast<uint64_t>(q0 + rtok) * Hq + h * G + r % G] = (m + __log2f(l)) * 0.69314718055994531f;
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
-}
-
-
 // ---------------------------------------------------------------------------
 // v2: warp-specialised, two query tiles per CTA (FA4-style ping-pong).
 //   warps 0-3 / 4-7: softmax of query tile A / B (thread = row)
@@ -316,6 +111,8 @@ constexpr uint32_t k2KV = 2 * kQBytes;                      // stages x (K 16 KB
 constexpr uint32_t k2P = k2KV + kStages * 2 * kKVBytes;     // 2 x 16 KB
 constexpr uint32_t k2Smem = k2P + 2 * kPBytes;
 constexpr uint32_t k2TmemCols = 512;
+// bulk-copy source for blocks past the sequence (a chunk half of zeros)
+__device__ __align__(128) uint8_t g_zero_half[kTPB * 128];
 
 __device__ __forceinline__ void tmem_ld32_to(uint32_t taddr, float* v) {
   float t[32];
@@ -348,7 +145,7 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
   if (tid == 0) {
     mbar_init(&q_full, kLoaders);
     for (uint32_t i = 0; i < kStages; ++i) {
-      mbar_init(&kv_full[i], kLoaders);
+      mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -380,31 +177,37 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
       cp_async16(sbase + k2Q + x * kQBytes + (c >> 3) * (kRows * 128) + sw128(r, c & 7), src, ok ? 16u : 0u);
     }
     cp_async_commit();
-    const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
-    for (uint32_t t = 0; t < ntiles; ++t) {
-      const uint32_t st = t % kStages;
-      if (t >= kStages) mbar_wait(&kv_empty[st], ((t / kStages) - 1) & 1);
-      const uint32_t kb = sbase + k2KV + st * 2 * kKVBytes;
-      for (uint32_t i = lt; i < 2 * 4 * 256; i += kLoaders) {
-        const uint32_t kv = i >> 10, bi = (i >> 8) & 3, gi = i & 255;
-        const uint32_t b = t * 4 + bi;
-        const bool ok = b < nblk;
-        const uint32_t gid = ok ? static_cast<uint32_t>(__ldg(bt + b)) : 0u;
-        const uint8_t* chunk = p.pool + block_offset(p.geom, gid) + p.layer_off +
-                               static_cast<uint64_t>(kv * p.H + h) * (kTPB * kD * 2);
-        const uint32_t line = gi >> 3, cl = (gi & 7) ^ (line & 7);
-        const uint32_t row = bi * kTPB + (line >> 1);
-        cp_async16(kb + kv * kKVBytes + (line & 1) * (kTile * 128) + sw128(row, cl), chunk + gi * 16,
-                   ok ? 16u : 0u);
-      }
-      cp_async_commit();
-      asm volatile("cp.async.wait_group 1;" ::: "memory");  // the previous group (Q, or tile t-1) landed
-      fence_proxy_async();
-      mbar_arrive(t == 0 ? &q_full : &kv_full[(t - 1) % kStages]);
-    }
-    cp_async_wait_all();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     fence_proxy_async();
-    mbar_arrive(&kv_full[(ntiles - 1) % kStages]);
+    mbar_arrive(&q_full);
+    if (tid == kLoadWarp0 * 32) {
+      // K/V: each FP16 chunk half (16 tokens x 64 dims, 2 KB) is already a
+      // 128B-swizzled operand slice, so one bulk copy (TMA engine) per half
+      // places it at rows 16*bi.. of the tile; 16 copies per 64-token tile
+      const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
+      const uint64_t pol = policy_evict_last();  // every query tile of the head re-reads them
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t st = t % kStages;
+        if (t >= kStages) mbar_wait(&kv_empty[st], ((t / kStages) - 1) & 1);
+        const uint32_t kb = sbase + k2KV + st * 2 * kKVBytes;
+        mbar_expect_tx(&kv_full[st], 2 * kKVBytes);
+#pragma unroll
+        for (uint32_t bi = 0; bi < 4; ++bi) {
+          const uint32_t b = t * 4 + bi;
+          const uint8_t* blk = b < nblk ? p.pool + block_offset(p.geom, static_cast<uint32_t>(__ldg(bt + b))) + p.layer_off
+                                        : nullptr;
+#pragma unroll
+          for (uint32_t kv = 0; kv < 2; ++kv)
+#pragma unroll
+            for (uint32_t half = 0; half < 2; ++half) {
+              const uint8_t* src = blk ? blk + static_cast<uint64_t>(kv * p.H + h) * (kTPB * kD * 2) + half * (kTPB * 128)
+                                       : g_zero_half;
+              bulk_g2s_u32(kb + kv * kKVBytes + half * (kTile * 128) + bi * (kTPB * 128), src, kTPB * 128,
+                           &kv_full[st], pol);
+            }
+        }
+      }
+    }
   } else if (warp == 8) {
     // ============================ MMA issuer ============================
     if (lane == 0) {
@@ -476,6 +279,10 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
       float sc[kTile];
       tmem_ld32_to(tS, sc);
       tmem_ld32_to(tS + 32, sc + 32);
+      if (p.debug & 2) {
+#pragma unroll
+        for (int j = 0; j < static_cast<int>(kTile); ++j) sc[j] = 0.f;
+      }
       const int kbase = static_cast<int>(t * kTile);
 #pragma unroll
       for (int j = 0; j < static_cast<int>(kTile); ++j) {
@@ -557,25 +364,14 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
 cudaError_t launch_paged_prefill_tc(const PrefillParams& p0, cudaStream_t stream) {
   using namespace dev::tc;
   PrefillParams p = p0;
-  if (p.use_tc != 1) {  // v2 (default): warp-specialised, two query tiles per CTA
-    const uint32_t tpc = 2 * kRows / p.G;
-    p.tiles = (p.max_q_len + tpc - 1) / tpc;
-    if (p.tiles == 0) return cudaSuccess;
-    const size_t smem2 = k2Smem + 1024;
-    cudaError_t e2 = cudaFuncSetAttribute(dev::tc::prefill_tc2_fp16_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem2));
-    if (e2 != cudaSuccess) return e2;
-    dev::tc::prefill_tc2_fp16_kernel<<<dim3(p.batch * p.H, p.tiles), kThreads2, smem2, stream>>>(p);
-    return cudaGetLastError();
-  }
-  const uint32_t tpt = kRows / p.G;
-  p.tiles = (p.max_q_len + tpt - 1) / tpt;
+  const uint32_t tpc = 2 * kRows / p.G;  // tokens per CTA (two 128-row query tiles)
+  p.tiles = (p.max_q_len + tpc - 1) / tpc;
   if (p.tiles == 0) return cudaSuccess;
-  const size_t smem = kSmem + 1024;  // + alignment slack
-  cudaError_t e = cudaFuncSetAttribute(dev::tc::prefill_tc_fp16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = k2Smem + 1024;  // + alignment slack
+  cudaError_t e = cudaFuncSetAttribute(dev::tc::prefill_tc2_fp16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dev::tc::prefill_tc_fp16_kernel<<<dim3(p.batch * p.H, p.tiles), kThreads, smem, stream>>>(p);
+  dev::tc::prefill_tc2_fp16_kernel<<<dim3(p.batch * p.H, p.tiles), kThreads2, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
