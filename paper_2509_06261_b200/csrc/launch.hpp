@@ -59,7 +59,7 @@ struct PrefillParams {
   float sm_scale_log2;
   const float* kv_scales;  // FP8 [2][H]
   uint32_t nt;  // query rows per warp / 8 (1 or 2; 0 = default: 1, or 2 when G > 8)
-  int use_tc;   // FP16 KV on tcgen05 (prefill_tc.cu): 2 = warp-specialised (default), 1 = v1, 0 = mma.sync
+  int use_tc;   // tcgen05 kernel (prefill_tc.cu) unless 0 (then mma.sync, prefill.cu)
   int debug;    // probes: bit0 no KV loads after the first two tiles, bit1 no softmax math
   // filled by the launcher
   uint32_t tiles, stages, stage_bytes, qbuf_offset, bar_offset;
@@ -94,7 +94,7 @@ cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms
                                 cudaStream_t stream);
 size_t decode_partials_bytes(int num_sms, int G);
 cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStream_t stream);
-cudaError_t launch_paged_prefill_tc(const PrefillParams& p, cudaStream_t stream);  // FP16 KV, tcgen05
+cudaError_t launch_paged_prefill_tc(const PrefillParams& p, int kv_dtype, cudaStream_t stream);  // tcgen05
 cudaError_t launch_kv_append(const AppendParams& p, int kv_dtype, cudaStream_t stream);
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_table_scatter(int32_t* table, uint32_t row_stride, const int32_t* triples,

@@ -288,7 +288,7 @@ static cudaError_t launch_prefill_fmt(const PrefillParams& p0, cudaStream_t stre
 cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStream_t stream) {
   using namespace dev;
   // 8 query rows per warp (default: more warps, two-block steps) or 16 (GQA 16)
-  if (kv_dtype == kFP16 && p.use_tc) return launch_paged_prefill_tc(p, stream);
+  if (p.use_tc) return launch_paged_prefill_tc(p, kv_dtype, stream);
   const bool two = p.nt == 2 || p.G > 8;
   switch (kv_dtype) {
     case kFP16: return two ? launch_prefill_fmt<kFP16, 2>(p, stream) : launch_prefill_fmt<kFP16, 1>(p, stream);

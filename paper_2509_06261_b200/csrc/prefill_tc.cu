@@ -104,13 +104,26 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
 //   warps 9-11     : cp.async loaders (Q tiles, then a 3-stage K/V ring)
 // While one tile's softmax runs the tensor core works on the other tile, and
 // the K/V ring keeps two tiles in flight.  TMEM: S_A | S_B | O_A | O_B.
-constexpr uint32_t kStages = 3;
 constexpr uint32_t kLoadWarp0 = 9, kLoaders = 96, kThreads2 = 384;
-constexpr uint32_t k2Q = 0;                                 // 2 x 32 KB
-constexpr uint32_t k2KV = 2 * kQBytes;                      // stages x (K 16 KB | V 16 KB)
-constexpr uint32_t k2P = k2KV + kStages * 2 * kKVBytes;     // 2 x 16 KB
-constexpr uint32_t k2Smem = k2P + 2 * kPBytes;
 constexpr uint32_t k2TmemCols = 512;
+// Shared memory per format: Q (2 x 32 KB) | fp16 K/V operand ring | P (2 x
+// 16 KB) | raw ring.  FP16 chunks are operands as stored (3 operand stages,
+// no raw ring); FP8/INT8/INT4 chunks and their per-token params land raw
+// (bulk copies, 2 stages) and the loader warps dequantise them into the
+// operand ring.
+template <int FMT>
+struct TcCfg {
+  static constexpr uint32_t kStages = FMT == kFP16 ? 3 : 2;
+  static constexpr uint32_t kChunk = Geo<FMT>::kChunk, kParam = Geo<FMT>::kParam;
+  static constexpr uint32_t kRawBlock = 2 * kChunk + 2 * kParam;  // K, V, K params, V params
+  static constexpr uint32_t kRawBytes = FMT == kFP16 ? 0 : (4 * kRawBlock + 127) / 128 * 128;
+  static constexpr uint32_t kQo = 0, kKV = 2 * kQBytes, kP = kKV + kStages * 2 * kKVBytes;
+  static constexpr uint32_t kRaw = kP + 2 * kPBytes;
+  // INT8/INT4: K enters the MMA as exact integers; its per-token scale (and
+  // zero) are applied to S in fp32 from these arrays ([stage][64] x 2 floats)
+  static constexpr uint32_t kSZ = kRaw + 2 * kRawBytes;
+  static constexpr uint32_t kSmem = kSZ + kStages * kTile * 8;
+};
 // bulk-copy source for blocks past the sequence (a chunk half of zeros)
 __device__ __align__(128) uint8_t g_zero_half[kTPB * 128];
 
@@ -121,10 +134,68 @@ __device__ __forceinline__ void tmem_ld32_to(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = t[i];
 }
 
-__global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const PrefillParams p) {
+// 16 raw bytes of K or V (token `tok` of block `bi`, dims d0.. of the
+// format's row) -> fp16 operand granules at their swizzled tile positions.
+// FP8 is converted exactly (its static per-head scale is applied in fp32 to S
+// and O); INT8 / INT4 apply the token's scale (and zero) in one fp16 rounding.
+template <int FMT>
+__device__ __forceinline__ void dequant_granule(uint8_t* tile, uint32_t row, uint32_t d0, uint4 w, uint32_t sz,
+                                                bool exact) {
+  auto put = [&](uint32_t d, uint32_t a, uint32_t b, uint32_t c, uint32_t e) {  // 8 dims at d
+    const uint32_t half = d >> 6, gran = (d & 63) >> 3;
+    *reinterpret_cast<uint4*>(tile + half * (kTile * 128) + sw128(row, gran)) = make_uint4(a, b, c, e);
+  };
+  const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
+  if constexpr (FMT == kFP8) {
+    uint32_t o[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      o[2 * i] = e4m3x2_to_f16x2(static_cast<uint16_t>(wd[i] & 0xffff));
+      o[2 * i + 1] = e4m3x2_to_f16x2(static_cast<uint16_t>(wd[i] >> 16));
+    }
+    put(d0, o[0], o[1], o[2], o[3]);
+    put(d0 + 8, o[4], o[5], o[6], o[7]);
+  } else if constexpr (FMT == kINT8) {
+    // K (exact): the integer itself; V: times the token's fp16 scale
+    const uint32_t s2 = exact ? 0x3C003C00u : ((sz & 0xffffu) | (sz << 16));
+    uint32_t o[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t x = wd[i] ^ 0x80808080u;  // exact 1152 + b, minus 1152, times s
+      o[2 * i] = hmul2_u32(hsub2_u32(__byte_perm(x, 0x64646464u, 0x4140), 0x64806480u), s2);
+      o[2 * i + 1] = hmul2_u32(hsub2_u32(__byte_perm(x, 0x64646464u, 0x4342), 0x64806480u), s2);
+    }
+    put(d0, o[0], o[1], o[2], o[3]);
+    put(d0 + 8, o[4], o[5], o[6], o[7]);
+  } else {  // INT4: 32 dims, byte k = (dim 2k low nibble, dim 2k+1 high nibble)
+    // K (exact): n itself, i.e. scale 1 and zero 0; V: s*n + z (one rounding)
+    const uint32_t sc = exact ? 0x3C00u : (sz & 0xffffu), z = exact ? 0u : (sz >> 16);
+    const uint32_t s2 = sc | (hmul2_u32(sc, 0x2C00u) << 16);  // (s, s/16): the high nibble enters as 16 n
+    const uint32_t z2 = z | (z << 16);
+    uint32_t o[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t y = __byte_perm(wd[i], 0, k | (k << 8) | (k << 16) | (k << 24));
+        const uint32_t n = hsub2_u32(lop3_and_or(y, 0x00F0000Fu, 0x64006400u), 0x64006400u);
+        o[4 * i + k] = hfma2_u32(n, s2, z2);
+      }
+    put(d0, o[0], o[1], o[2], o[3]);
+    put(d0 + 8, o[4], o[5], o[6], o[7]);
+    put(d0 + 16, o[8], o[9], o[10], o[11]);
+    put(d0 + 24, o[12], o[13], o[14], o[15]);
+  }
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const PrefillParams p) {
+  using Cfg = TcCfg<FMT>;
+  constexpr uint32_t kStages = Cfg::kStages, k2Q = Cfg::kQo, k2KV = Cfg::kKV, k2P = Cfg::kP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t q_full, kv_full[kStages], kv_empty[kStages], s_full[2], p_full[2], o_final;
+  __shared__ uint64_t raw_full[2], raw_empty[2];
   __shared__ uint32_t tmem_base;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t s = blockIdx.x / p.H, h = blockIdx.x % p.H;
@@ -145,8 +216,12 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
   if (tid == 0) {
     mbar_init(&q_full, kLoaders);
     for (uint32_t i = 0; i < kStages; ++i) {
-      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_full[i], FMT == kFP16 ? 1u : kLoaders);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], kLoaders);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
@@ -180,7 +255,79 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     fence_proxy_async();
     mbar_arrive(&q_full);
-    if (tid == kLoadWarp0 * 32) {
+    if constexpr (FMT != kFP16) {
+      // ---- raw blocks (bulk copies, one thread) -> dequantised operand tiles (96 threads) ----
+      constexpr uint32_t kC = Cfg::kChunk, kPm = Cfg::kParam, kRB = Cfg::kRawBlock;
+      const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
+      const uint32_t raw0 = sbase + Cfg::kRaw;
+      auto issue_raw = [&](uint32_t t) {
+        const uint32_t rs = t & 1;
+        if (t >= 2) mbar_wait(&raw_empty[rs], ((t >> 1) - 1) & 1);
+        mbar_expect_tx(&raw_full[rs], 4 * kRB);
+        const uint64_t pol = policy_evict_last();
+        for (uint32_t bi = 0; bi < 4; ++bi) {
+          const uint32_t b = t * 4 + bi;
+          const uint32_t dst = raw0 + rs * Cfg::kRawBytes + bi * kRB;
+          if (b < nblk) {
+            const uint8_t* blk = p.pool + block_offset(p.geom, static_cast<uint32_t>(__ldg(bt + b))) + p.layer_off;
+            bulk_g2s_u32(dst, blk + static_cast<uint64_t>(h) * kC, kC, &raw_full[rs], pol);
+            bulk_g2s_u32(dst + kC, blk + static_cast<uint64_t>(p.H + h) * kC, kC, &raw_full[rs], pol);
+            if constexpr (kPm > 0) {
+              const uint8_t* prm = blk + 2ull * p.H * kC + static_cast<uint64_t>(h) * kPm;
+              bulk_g2s_u32(dst + 2 * kC, prm, kPm, &raw_full[rs], pol);
+              bulk_g2s_u32(dst + 2 * kC + kPm, prm + static_cast<uint64_t>(p.H) * kPm, kPm, &raw_full[rs], pol);
+            }
+          } else {  // past the sequence: zeros (scale 0 -> exact 0)
+            for (uint32_t o = 0; o < kRB; o += kTPB * 128) {
+              const uint32_t n = min(kTPB * 128, kRB - o);
+              bulk_g2s_u32(dst + o, g_zero_half, n, &raw_full[rs], pol);
+            }
+          }
+        }
+      };
+      if (lt == 0) issue_raw(0);
+      constexpr uint32_t kRowB = kD * Fmt<FMT>::kBits / 8;     // raw bytes per token row
+      constexpr uint32_t kGran = 2 * 4 * kC / 16;               // raw 16-byte granules per tile
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        if (lt == 0 && t + 1 < ntiles) issue_raw(t + 1);
+        const uint32_t rs = t & 1, st = t % kStages;
+        mbar_wait(&raw_full[rs], (t >> 1) & 1);
+        if (t >= kStages) mbar_wait(&kv_empty[st], ((t / kStages) - 1) & 1);
+        const uint8_t* raw = smem + Cfg::kRaw + rs * Cfg::kRawBytes;
+        uint8_t* kt = smem + k2KV + st * 2 * kKVBytes;
+        for (uint32_t i = lt; i < kGran; i += kLoaders) {
+          const uint32_t kv = i / (4 * kC / 16), rem = i % (4 * kC / 16);
+          const uint32_t bi = rem / (kC / 16), gi = rem % (kC / 16);  // physical granule of the chunk
+          const uint32_t off = gi * 16, line = off >> 7;
+          const uint32_t lo = (off & 127) ^ ((line & 7) << 4);          // unswizzle: logical byte in the line
+          const uint32_t lb = (line << 7) | lo;                          // logical byte in the chunk
+          const uint32_t tok = lb / kRowB, d0 = (lb % kRowB) * 8 / Fmt<FMT>::kBits;
+          const uint8_t* rb = raw + bi * kRB;
+          const uint4 w = *reinterpret_cast<const uint4*>(rb + kv * kC + off);
+          uint32_t sz = 0;
+          if constexpr (FMT == kINT8) sz = *reinterpret_cast<const uint16_t*>(rb + 2 * kC + kv * kPm + tok * 2);
+          if constexpr (FMT == kINT4) sz = *reinterpret_cast<const uint32_t*>(rb + 2 * kC + kv * kPm + tok * 4);
+          dequant_granule<FMT>(kt + kv * kKVBytes, bi * kTPB + tok, d0, w, sz, kv == 0 && FMT != kFP8);
+        }
+        if constexpr (FMT == kINT8 || FMT == kINT4) {  // K scale / zero of the tile's 64 tokens, fp32
+          if (lt < kTile) {
+            const uint8_t* rp = raw + (lt / kTPB) * kRB + 2 * kC + (lt % kTPB) * (FMT == kINT8 ? 2 : 4);
+            float* sz = reinterpret_cast<float*>(smem + Cfg::kSZ + st * kTile * 8);
+            if constexpr (FMT == kINT8) {
+              sz[lt] = __half2float(*reinterpret_cast<const __half*>(rp));
+              sz[kTile + lt] = 0.f;
+            } else {
+              const __half2 v = *reinterpret_cast<const __half2*>(rp);
+              sz[lt] = __low2float(v);
+              sz[kTile + lt] = __high2float(v);
+            }
+          }
+        }
+        fence_proxy_async();
+        mbar_arrive(&kv_full[st]);
+        mbar_arrive(&raw_empty[rs]);
+      }
+    } else if (tid == kLoadWarp0 * 32) {
       // K/V: each FP16 chunk half (16 tokens x 64 dims, 2 KB) is already a
       // 128B-swizzled operand slice, so one bulk copy (TMA engine) per half
       // places it at rows 16*bi.. of the tile; 16 copies per 64-token tile
@@ -270,9 +417,15 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
     const int rpos = rvalid ? pos0 + rtok : pos_last;
     const uint32_t lanes = ((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + lanes + x * kTile, tO = tmem + lanes + 2 * kTile + x * kD;
-    const float sml2 = p.sm_scale_log2;
+    float sml2 = p.sm_scale_log2, oscale = 1.f;
+    if constexpr (FMT == kFP8) {  // static per-head scales: K into S, V into O
+      if (p.kv_scales) {
+        sml2 *= p.kv_scales[h];
+        oscale = p.kv_scales[p.H + h];
+      }
+    }
     uint8_t* prow = smem + k2P + x * kPBytes;
-    float m = -INFINITY, l = 0.f;
+    float m = -INFINITY, l = 0.f, qsum = 0.f;
     for (uint32_t t = 0; t < ntiles; ++t) {
       mbar_wait(&s_full[x], t & 1);
       tc_fence_after();
@@ -284,10 +437,34 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
         for (int j = 0; j < static_cast<int>(kTile); ++j) sc[j] = 0.f;
       }
       const int kbase = static_cast<int>(t * kTile);
+      if constexpr (FMT == kINT8 || FMT == kINT4) {
+        if (t == 0 && FMT == kINT4) {  // sum of this row's (exact fp16) query, for the zero term
+          const uint8_t* qr = smem + k2Q + x * kQBytes;
+          float acc = 0.f;
 #pragma unroll
-      for (int j = 0; j < static_cast<int>(kTile); ++j) {
-        sc[j] *= sml2;
-        if (kbase + j > rpos) sc[j] = -INFINITY;
+          for (uint32_t c = 0; c < 16; ++c) {
+            const uint4 v = *reinterpret_cast<const uint4*>(qr + (c >> 3) * (kRows * 128) + sw128(r, c & 7));
+            const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&wv[i]));
+              acc += f.x + f.y;
+            }
+          }
+          qsum = acc;
+        }
+        const float* sz = reinterpret_cast<const float*>(smem + Cfg::kSZ + (t % kStages) * kTile * 8);
+#pragma unroll
+        for (int j = 0; j < static_cast<int>(kTile); ++j) {
+          sc[j] = (sc[j] * sz[j] + sz[kTile + j] * qsum) * sml2;
+          if (kbase + j > rpos) sc[j] = -INFINITY;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < static_cast<int>(kTile); ++j) {
+          sc[j] *= sml2;
+          if (kbase + j > rpos) sc[j] = -INFINITY;
+        }
       }
       float mx = -INFINITY;
 #pragma unroll
@@ -332,7 +509,7 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
     }
     mbar_wait(&o_final, 0);
     tc_fence_after();
-    const float inv = 1.f / l;
+    const float inv = oscale / l;
     __half* orow = p.out + (static_cast<uint64_t>(q0 + (rvalid ? rtok : 0)) * Hq + h * G + rr % G) * kD;
 #pragma unroll
     for (uint32_t c = 0; c < kD; c += 32) {
@@ -361,18 +538,30 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_fp16_kernel(const Pr
 }  // namespace tc
 }  // namespace dev
 
-cudaError_t launch_paged_prefill_tc(const PrefillParams& p0, cudaStream_t stream) {
+template <int FMT>
+static cudaError_t launch_tc(const PrefillParams& p0, cudaStream_t stream) {
   using namespace dev::tc;
   PrefillParams p = p0;
   const uint32_t tpc = 2 * kRows / p.G;  // tokens per CTA (two 128-row query tiles)
   p.tiles = (p.max_q_len + tpc - 1) / tpc;
   if (p.tiles == 0) return cudaSuccess;
-  const size_t smem = k2Smem + 1024;  // + alignment slack
-  cudaError_t e = cudaFuncSetAttribute(dev::tc::prefill_tc2_fp16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  const size_t smem = TcCfg<FMT>::kSmem + 1024;  // + alignment slack
+  auto kern = prefill_tc2_kernel<FMT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  dev::tc::prefill_tc2_fp16_kernel<<<dim3(p.batch * p.H, p.tiles), kThreads2, smem, stream>>>(p);
+  kern<<<dim3(p.batch * p.H, p.tiles), kThreads2, smem, stream>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_paged_prefill_tc(const PrefillParams& p, int kv_dtype, cudaStream_t stream) {
+  using namespace dev;
+  switch (kv_dtype) {
+    case kFP16: return launch_tc<kFP16>(p, stream);
+    case kFP8: return launch_tc<kFP8>(p, stream);
+    case kINT8: return launch_tc<kINT8>(p, stream);
+    case kINT4: return launch_tc<kINT4>(p, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace kvslab

@@ -83,12 +83,20 @@ def test_prefill_last_token_equals_decode(dt):
 
 
 @pytest.mark.parametrize("nt", ["1", "2"])
-def test_prefill_row_tiling_variants(nt, monkeypatch):
-    """Both warp tilings (8 or 16 query rows per warp) agree with the oracle
-    (GQA 16 always takes the 16-row tiling)."""
+def test_prefill_mma_sync_row_tilings(nt, monkeypatch):
+    """The mma.sync kernel (KVSLAB_PREFILL_TC=0), both warp tilings (8 or 16
+    query rows per warp; GQA 16 always takes 16)."""
+    monkeypatch.setenv("KVSLAB_PREFILL_TC", "0")
     monkeypatch.setenv("KVSLAB_PREFILL_NT", nt)
     _, _, _, _, o, _, r, _ = run_prefill(KvDtype.INT8, 2, 8, [(300, 45), (700, 161), (5, 5)], seed=21)
     assert rel_err(o, r) <= 1e-2
+
+
+@pytest.mark.parametrize("dt", FORMATS, ids=[d.name for d in FORMATS])
+def test_prefill_mma_sync_path_all_formats(dt, monkeypatch):
+    monkeypatch.setenv("KVSLAB_PREFILL_TC", "0")
+    _, _, _, _, o, _, r, _ = run_prefill(dt, 2, 8, CASES, seed=31 + int(dt))
+    assert rel_err(o, r) <= TOL[dt]
 
 
 def test_prefill_long_chunk_fp8():
