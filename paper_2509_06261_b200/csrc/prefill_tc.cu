@@ -114,6 +114,7 @@ constexpr uint32_t k2TmemCols = 512;
 template <int FMT>
 struct TcCfg {
   static constexpr uint32_t kStages = FMT == kFP16 ? 3 : 2;
+  static constexpr uint32_t kRawStages = 3;  // raw blocks land two tiles ahead of the dequant
   static constexpr uint32_t kChunk = Geo<FMT>::kChunk, kParam = Geo<FMT>::kParam;
   static constexpr uint32_t kRawBlock = 2 * kChunk + 2 * kParam;  // K, V, K params, V params
   static constexpr uint32_t kRawBytes = FMT == kFP16 ? 0 : (4 * kRawBlock + 127) / 128 * 128;
@@ -121,7 +122,7 @@ struct TcCfg {
   static constexpr uint32_t kRaw = kP + 2 * kPBytes;
   // INT8/INT4: K enters the MMA as exact integers; its per-token scale (and
   // zero) are applied to S in fp32 from these arrays ([stage][64] x 2 floats)
-  static constexpr uint32_t kSZ = kRaw + 2 * kRawBytes;
+  static constexpr uint32_t kSZ = kRaw + kRawStages * kRawBytes;
   static constexpr uint32_t kSmem = kSZ + kStages * kTile * 8;
 };
 // bulk-copy source for blocks past the sequence (a chunk half of zeros)
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t q_full, kv_full[kStages], kv_empty[kStages], s_full[2], p_full[2], o_final;
-  __shared__ uint64_t raw_full[2], raw_empty[2];
+  __shared__ uint64_t raw_full[Cfg::kRawStages], raw_empty[Cfg::kRawStages];
   __shared__ uint32_t tmem_base;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t s = blockIdx.x / p.H, h = blockIdx.x % p.H;
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
       mbar_init(&kv_full[i], FMT == kFP16 ? 1u : kLoaders);
       mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (uint32_t i = 0; i < Cfg::kRawStages; ++i) {
       mbar_init(&raw_full[i], 1);
       mbar_init(&raw_empty[i], kLoaders);
     }
@@ -260,9 +261,10 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
       constexpr uint32_t kC = Cfg::kChunk, kPm = Cfg::kParam, kRB = Cfg::kRawBlock;
       const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
       const uint32_t raw0 = sbase + Cfg::kRaw;
+      constexpr uint32_t RS = Cfg::kRawStages;
       auto issue_raw = [&](uint32_t t) {
-        const uint32_t rs = t & 1;
-        if (t >= 2) mbar_wait(&raw_empty[rs], ((t >> 1) - 1) & 1);
+        const uint32_t rs = t % RS;
+        if (t >= RS) mbar_wait(&raw_empty[rs], ((t / RS) - 1) & 1);
         mbar_expect_tx(&raw_full[rs], 4 * kRB);
         const uint64_t pol = policy_evict_last();
         for (uint32_t bi = 0; bi < 4; ++bi) {
@@ -285,17 +287,19 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
           }
         }
       };
-      if (lt == 0) issue_raw(0);
+      if (lt == 0)
+        for (uint32_t t = 0; t + 1 < RS && t < ntiles; ++t) issue_raw(t);
       constexpr uint32_t kRowB = kD * Fmt<FMT>::kBits / 8;     // raw bytes per token row
       constexpr uint32_t kGran = 2 * 4 * kC / 16;               // raw 16-byte granules per tile
       for (uint32_t t = 0; t < ntiles; ++t) {
-        if (lt == 0 && t + 1 < ntiles) issue_raw(t + 1);
-        const uint32_t rs = t & 1, st = t % kStages;
-        mbar_wait(&raw_full[rs], (t >> 1) & 1);
+        if (lt == 0 && t + RS - 1 < ntiles) issue_raw(t + RS - 1);
+        const uint32_t rs = t % RS, st = t % kStages;
+        mbar_wait(&raw_full[rs], (t / RS) & 1);
         if (t >= kStages) mbar_wait(&kv_empty[st], ((t / kStages) - 1) & 1);
         const uint8_t* raw = smem + Cfg::kRaw + rs * Cfg::kRawBytes;
         uint8_t* kt = smem + k2KV + st * 2 * kKVBytes;
-        for (uint32_t i = lt; i < kGran; i += kLoaders) {
+#pragma unroll 4
+        for (uint32_t i = lt; i < ((p.debug & 4) ? 0u : kGran); i += kLoaders) {
           const uint32_t kv = i / (4 * kC / 16), rem = i % (4 * kC / 16);
           const uint32_t bi = rem / (kC / 16), gi = rem % (kC / 16);  // physical granule of the chunk
           const uint32_t off = gi * 16, line = off >> 7;
