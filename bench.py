@@ -336,7 +336,7 @@ def format_sweep(peak):
             del g, pool
         res["decode"][f"B{B}_ctx{ctx0}"] = row
     nq = 4096
-    for dt in (KvDtype.FP16, KvDtype.INT4):
+    for dt in (KvDtype.FP16, KvDtype.FP8_E4M3, KvDtype.INT8, KvDtype.INT4):
         fmt, pool, m = world(dt, 1, nq)
         ctx = torch.full((1,), nq, dtype=torch.int32, device="cuda")
         cu = torch.tensor([0, nq], dtype=torch.int32, device="cuda")
@@ -690,7 +690,7 @@ def run_ours():
         **({"formats": sweep["decode"], "prefill": sweep["prefill"]} if sweep else {}),
         "clocks": clk.summary(),
     }
-    if not ARGS.no_cpu_baseline:
+    if not ARGS.no_cpu_baseline and WORLD == 1:  # rank 0 at N=1 only
         v, cores, sample = cpu_sample()
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "GB/s", "cores": cores,
                                 "kind": "port", "sample": sample}
