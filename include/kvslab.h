@@ -267,8 +267,9 @@ ks_status ks_paged_decode_append(ks_pool* pool, const ks_kv_format* fmt, uint32_
  * (int32 [batch+1], device), at positions d_ctx_lens[s]-n_s..d_ctx_lens[s]-1
  * (so d_ctx_lens[s] >= n_s); each query attends causally to keys 0..its
  * position.  max_q_len >= every n_s (sizes the grid).  d_lse: fp32
- * [T_total][Hq] natural-log LSE (nullable).  GQA group must divide 8.
- * No workspace; no host synchronisation. */
+ * [T_total][Hq] natural-log LSE (nullable).  GQA group must divide 16.
+ * Runs on the tcgen05 tensor cores (TMEM accumulators) for every KV format;
+ * no workspace; no host synchronisation. */
 ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
                            void* d_out, float* d_lse, const int32_t* d_block_table,
                            uint32_t bt_stride, const int32_t* d_cu_q, const int32_t* d_ctx_lens,
