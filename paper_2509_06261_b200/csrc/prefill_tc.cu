@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
   constexpr uint32_t kStages = Cfg::kStages, k2Q = Cfg::kQo, k2KV = Cfg::kKV, k2P = Cfg::kP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t q_full, kv_full[kStages], kv_empty[kStages], s_full[2], p_full[2], o_final;
+  __shared__ uint64_t q_full, kv_full[kStages], kv_empty[kStages], s_full[2], p_full[2], pv_done[2], o_final;
   __shared__ uint64_t raw_full[Cfg::kRawStages], raw_empty[Cfg::kRawStages];
   __shared__ uint32_t tmem_base;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], kRows);
+      mbar_init(&pv_done[i], 1);
     }
     mbar_init(&o_final, 1);
     fence_mbar_init();
@@ -364,13 +365,13 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
     if (lane == 0) {
       const uint32_t idesc_s = (1u << 4) | ((kTile >> 3) << 17) | ((kRows >> 4) << 24);
       const uint32_t idesc_pv = (1u << 4) | (1u << 16) | ((kD >> 3) << 17) | ((kRows >> 4) << 24);
-      auto mma_s = [&](uint32_t x, uint32_t st) {
+      auto mma_s = [&](uint32_t x, uint32_t st, uint32_t sb) {  // sb: S buffer (tile parity)
 #pragma unroll
         for (uint32_t k = 0; k < kD / 16; ++k) {
           const uint64_t ad = umma_desc(sbase + k2Q + x * kQBytes + (k >> 2) * (kRows * 128) + (k & 3) * 32, 16, 1024);
           const uint64_t bd =
               umma_desc(sbase + k2KV + st * 2 * kKVBytes + (k >> 2) * (kTile * 128) + (k & 3) * 32, 16, 1024);
-          umma_f16(tmem + x * kTile, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          umma_f16(tmem + x * 2 * kTile + sb * kTile, ad, bd, idesc_s, k > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[x]);
       };
@@ -379,36 +380,35 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
         for (uint32_t k = 0; k < kTile / 16; ++k) {
           const uint64_t ad = umma_desc(sbase + k2P + x * kPBytes + k * 32, 16, 1024);
           const uint64_t bd = umma_desc(sbase + k2KV + st * 2 * kKVBytes + kKVBytes + k * 2048, kTile * 128, 1024);
-          umma_f16(tmem + 2 * kTile + x * kD, ad, bd, idesc_pv, (!first || k > 0) ? 1u : 0u);
+          umma_f16(tmem + 4 * kTile + x * kD, ad, bd, idesc_pv, (!first || k > 0) ? 1u : 0u);
         }
+        umma_commit(&pv_done[x]);
       };
+      // S is double-buffered in TMEM, so S(t+1) of a tile runs while its
+      // softmax of t is still reading S(t):  S_A(t+1), PV_A(t), S_B(t+1), PV_B(t)
       mbar_wait(&q_full, 0);
       tc_fence_after();
+      mbar_wait(&kv_full[0], 0);
+      tc_fence_after();
+      mma_s(0, 0, 0);
+      mma_s(1, 0, 0);
       for (uint32_t t = 0; t < ntiles; ++t) {
-        const uint32_t st = t % kStages, pst = (t + kStages - 1) % kStages;
-        mbar_wait(&kv_full[st], (t / kStages) & 1);
+        const uint32_t st = t % kStages, nst = (t + 1) % kStages;
+        const bool more = t + 1 < ntiles;
+        if (more) {
+          mbar_wait(&kv_full[nst], ((t + 1) / kStages) & 1);
+          tc_fence_after();
+          mma_s(0, nst, (t + 1) & 1);  // S_A buffer (t+1)&1 was read by softmax A(t-1): p_full waited below
+        }
+        mbar_wait(&p_full[0], t & 1);
         tc_fence_after();
-        if (t > 0) {
-          mbar_wait(&p_full[0], (t - 1) & 1);
-          tc_fence_after();
-          mma_pv(0, pst, t == 1);
-        }
-        mma_s(0, st);
-        if (t > 0) {
-          mbar_wait(&p_full[1], (t - 1) & 1);
-          tc_fence_after();
-          mma_pv(1, pst, t == 1);
-          umma_commit(&kv_empty[pst]);
-        }
-        mma_s(1, st);
+        mma_pv(0, st, t == 0);
+        if (more) mma_s(1, nst, (t + 1) & 1);
+        mbar_wait(&p_full[1], t & 1);
+        tc_fence_after();
+        mma_pv(1, st, t == 0);
+        umma_commit(&kv_empty[st]);
       }
-      const uint32_t lst = (ntiles - 1) % kStages;
-      mbar_wait(&p_full[0], (ntiles - 1) & 1);
-      tc_fence_after();
-      mma_pv(0, lst, ntiles == 1);
-      mbar_wait(&p_full[1], (ntiles - 1) & 1);
-      tc_fence_after();
-      mma_pv(1, lst, ntiles == 1);
       umma_commit(&o_final);
     }
     __syncwarp();
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
     const bool rvalid = rtok < tok_end;
     const int rpos = rvalid ? pos0 + rtok : pos_last;
     const uint32_t lanes = ((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + lanes + x * kTile, tO = tmem + lanes + 2 * kTile + x * kD;
+    const uint32_t tS = tmem + lanes + x * 2 * kTile, tO = tmem + lanes + 4 * kTile + x * kD;
     float sml2 = p.sm_scale_log2, oscale = 1.f;
     if constexpr (FMT == kFP8) {  // static per-head scales: K into S, V into O
       if (p.kv_scales) {
@@ -434,8 +434,8 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
       mbar_wait(&s_full[x], t & 1);
       tc_fence_after();
       float sc[kTile];
-      tmem_ld32_to(tS, sc);
-      tmem_ld32_to(tS + 32, sc + 32);
+      tmem_ld32_to(tS + (t & 1) * kTile, sc);
+      tmem_ld32_to(tS + (t & 1) * kTile + 32, sc + 32);
       if (p.debug & 2) {
 #pragma unroll
         for (int j = 0; j < static_cast<int>(kTile); ++j) sc[j] = 0.f;
@@ -463,20 +463,24 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
           sc[j] = (sc[j] * sz[j] + sz[kTile + j] * qsum) * sml2;
           if (kbase + j > rpos) sc[j] = -INFINITY;
         }
-      } else {
+      } else if (kbase + static_cast<int>(kTile) - 1 > rpos) {  // diagonal tile only: causal mask
 #pragma unroll
-        for (int j = 0; j < static_cast<int>(kTile); ++j) {
-          sc[j] *= sml2;
+        for (int j = 0; j < static_cast<int>(kTile); ++j)
           if (kbase + j > rpos) sc[j] = -INFINITY;
-        }
       }
+      // FP16/FP8 keep raw scores: the scale rides in the exp2's FFMA below
+      constexpr bool kRaw = !(FMT == kINT8 || FMT == kINT4);
       float mx = -INFINITY;
 #pragma unroll
       for (int j = 0; j < static_cast<int>(kTile); ++j) mx = fmaxf(mx, sc[j]);
+      if constexpr (kRaw) mx *= sml2;
       const bool grow = mx > m + kRescaleSlack;
       const float alpha = grow ? ex2(m - mx) : 1.f;
-      // PV of tile t-1 completed before s_full[x] of tile t (issue order), so
-      // O and this tile's P buffer are free
+      // O and the P buffer are free once PV of tile t-1 completed
+      if (t > 0) {
+        mbar_wait(&pv_done[x], (t - 1) & 1);
+        tc_fence_after();
+      }
       if (t > 0 && __any_sync(0xffffffffu, grow)) {
 #pragma unroll
         for (uint32_t c = 0; c < kD; c += 32) {
@@ -497,7 +501,7 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
         float pv[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          pv[j] = ex2(sc[c * 8 + j] - m);
+          pv[j] = kRaw ? ex2(fmaf(sc[c * 8 + j], sml2, -m)) : ex2(sc[c * 8 + j] - m);
           l += pv[j];
         }
         uint4 w;
