@@ -318,13 +318,14 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
           if (lt < kTile) {
             const uint8_t* rp = raw + (lt / kTPB) * kRB + 2 * kC + (lt % kTPB) * (FMT == kINT8 ? 2 : 4);
             float* sz = reinterpret_cast<float*>(smem + Cfg::kSZ + st * kTile * 8);
+            // pre-multiplied by the softmax scale (log2 domain): S = s'*dot + z'*sum(q)
             if constexpr (FMT == kINT8) {
-              sz[lt] = __half2float(*reinterpret_cast<const __half*>(rp));
+              sz[lt] = __half2float(*reinterpret_cast<const __half*>(rp)) * p.sm_scale_log2;
               sz[kTile + lt] = 0.f;
             } else {
               const __half2 v = *reinterpret_cast<const __half2*>(rp);
-              sz[lt] = __low2float(v);
-              sz[kTile + lt] = __high2float(v);
+              sz[lt] = __low2float(v) * p.sm_scale_log2;
+              sz[kTile + lt] = __high2float(v) * p.sm_scale_log2;
             }
           }
         }
@@ -460,10 +461,11 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
         const float* sz = reinterpret_cast<const float*>(smem + Cfg::kSZ + (t % kStages) * kTile * 8);
 #pragma unroll
         for (int j = 0; j < static_cast<int>(kTile); ++j) {
-          sc[j] = (sc[j] * sz[j] + sz[kTile + j] * qsum) * sml2;
-          if (kbase + j > rpos) sc[j] = -INFINITY;
+          if constexpr (FMT == kINT8) sc[j] *= sz[j];
+          else sc[j] = fmaf(sc[j], sz[j], sz[kTile + j] * qsum);
         }
-      } else if (kbase + static_cast<int>(kTile) - 1 > rpos) {  // diagonal tile only: causal mask
+      }
+      if (kbase + static_cast<int>(kTile) - 1 > rpos) {  // diagonal tile only: causal mask
 #pragma unroll
         for (int j = 0; j < static_cast<int>(kTile); ++j)
           if (kbase + j > rpos) sc[j] = -INFINITY;
