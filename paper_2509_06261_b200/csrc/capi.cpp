@@ -745,7 +745,6 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
     p.fp8_inblock = fmt->kv_dtype == KS_KV_FP8_E4M3 && fmt->quant_param_bytes_per_block > 0;
     if ((d_k_new == nullptr) != (d_v_new == nullptr))
       return fail(KS_INVALID_ARGUMENT, "k_new and v_new must both be set or both be null");
-    const size_t part = kvslab::decode_partials_bytes(pool->num_sms, static_cast<int>(p.G));
     p.partials = static_cast<float*>(d_workspace);
     p.max_ctas = 0;
     if (const char* dbg = std::getenv("KVSLAB_DECODE_DEBUG")) p.debug = std::atoi(dbg);
