@@ -396,15 +396,15 @@ __global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const Prefill
       for (uint32_t t = 0; t < ntiles; ++t) {
         const uint32_t st = t % kStages, nst = (t + 1) % kStages;
         const bool more = t + 1 < ntiles;
-        if (more) {
+        if (more) {  // both tiles' next S first: neither waits on the other's softmax
           mbar_wait(&kv_full[nst], ((t + 1) / kStages) & 1);
           tc_fence_after();
-          mma_s(0, nst, (t + 1) & 1);  // S_A buffer (t+1)&1 was read by softmax A(t-1): p_full waited below
+          mma_s(0, nst, (t + 1) & 1);  // buffer (t+1)&1 was read by softmax(t-1): p_full(t-1) waited
+          mma_s(1, nst, (t + 1) & 1);
         }
         mbar_wait(&p_full[0], t & 1);
         tc_fence_after();
         mma_pv(0, st, t == 0);
-        if (more) mma_s(1, nst, (t + 1) & 1);
         mbar_wait(&p_full[1], t & 1);
         tc_fence_after();
         mma_pv(1, st, t == 0);
