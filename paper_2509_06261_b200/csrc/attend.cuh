@@ -36,16 +36,17 @@ struct FragOff {
 };
 
 // token held in PV k-slot: slot 2t -> ta(t), 2t+1 -> tb(t), +8 for 2t+8/2t+9
+// (FP16 pairs tokens (2t, 2t+1) like the 8-bit formats: with the half-major
+// chunk a row is one 128-byte line, and even/odd rows keep the two lanes of a
+// quarter-warp on different banks)
 template <int FMT>
 __device__ __forceinline__ int tok_a(int t) {
-  if constexpr (FMT == kFP16) return t;
-  else if constexpr (FMT == kINT4) return (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}
+  if constexpr (FMT == kINT4) return (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}
   else return 2 * t;
 }
 template <int FMT>
 __device__ __forceinline__ int tok_b(int t) {
-  if constexpr (FMT == kFP16) return t + 4;
-  else if constexpr (FMT == kINT4) return 2 + (t & 1) + ((t >> 1) << 2);  // {2,3,6,7}
+  if constexpr (FMT == kINT4) return 2 + (t & 1) + ((t >> 1) << 2);  // {2,3,6,7}
   else return 2 * t + 1;
 }
 
@@ -54,10 +55,11 @@ __device__ __forceinline__ FragOff make_offsets(int g, int t) {
   FragOff o;
   const int ta = tok_a<FMT>(t), tb = tok_b<FMT>(t);
   if constexpr (FMT == kFP16) {
-    const int gt = (t & 1) + ((t >> 1) << 2);  // {0,1,4,5}[t]
 #pragma unroll
-    // half-major chunk: dims 64h.. of token t at h*2048 + t*128 (16 tokens)
-    for (int c = 0; c < 4; ++c) o.k[c] = swz((c >> 1) * 2048 + g * 128 + 16 * (gt + 2 * (c & 1)));
+    // half-major chunk: dims 64h.. of token t at h*2048 + t*128 (16 tokens);
+    // granule 2t + (c&1) of the half: rows g and g^1 of a quarter-warp then
+    // hit disjoint banks under the row-keyed swizzle
+    for (int c = 0; c < 4; ++c) o.k[c] = swz((c >> 1) * 2048 + g * 128 + 16 * (2 * t + (c & 1)));
     o.v[0] = swz(ta * 128 + 16 * g);
     o.v[1] = swz(2048 + ta * 128 + 16 * g);
     o.v[2] = swz(tb * 128 + 16 * g);
@@ -153,10 +155,9 @@ __device__ __forceinline__ void load_q_frags(uint32_t sQ, int g, int t, uint32_t
     const bool ok = qrow < static_cast<int>(G);
     const uint32_t row = sQ + qrow * kD * 2;
     if constexpr (FMT == kFP16) {
-      const int gt = (t & 1) + ((t >> 1) << 2);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int gr = 8 * (c >> 1) + gt + 2 * (c & 1);
+        const int gr = 8 * (c >> 1) + 2 * t + (c & 1);  // the K fragments' dim order
         const uint4 v = ok ? lds128(row + 16 * gr) : make_uint4(0, 0, 0, 0);
         qf[nt][2 * c][0] = v.x; qf[nt][2 * c][1] = v.y;
         qf[nt][2 * c + 1][0] = v.z; qf[nt][2 * c + 1][1] = v.w;

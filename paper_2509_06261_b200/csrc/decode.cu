@@ -266,8 +266,14 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, 
 // Probe stamps (p.trace only): per CTA, the time the producer issues stage k
 // (k < 32) and the time consumer warp 0 sees it full.
 constexpr uint32_t kTrStage = 12288, kTrReady = kTrStage + 148 * 4 * 32;
+// Compiled in only with -DKVSLAB_STAGE_PROBES (scripts/probe_stages.py): the
+// per-block checks cost the consumer loop ~1 % even when p.trace is null.
 __device__ __forceinline__ void trace_ready(const DecodeParams& p, int warp, int lane, uint32_t k) {
+#ifdef KVSLAB_STAGE_PROBES
   if (p.trace && warp == 0 && lane == 0 && k < 32) p.trace[kTrReady + blockIdx.x * 32 + k] = gtimer();
+#else
+  (void)p, (void)warp, (void)lane, (void)k;
+#endif
 }
 
 // Formats whose consumer step runs two full blocks at a time (measured per format
@@ -438,7 +444,9 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       const uint32_t gw = __shfl_sync(0xffffffffu, w.g0, j);
       const uint32_t g0 = gw & 0x7fffffffu;
       mbar_wait(&empty[st], ph ^ 1);
+#ifdef KVSLAB_STAGE_PROBES
       if (p.trace && lane == 0 && k < 32) p.trace[kTrStage + blockIdx.x * 32 + k] = gtimer();
+#endif
       if (lane == 0) {
         const uint32_t sb = ring_u + st * p.stage_bytes;
         meta[st] = src - static_cast<uint64_t>(g0) * Gm::kChunk;  // layer sub-block (fused append)

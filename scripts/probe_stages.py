@@ -1,7 +1,9 @@
 """Per-stage timeline of K2 (design probe): for layer 1 of an L-layer graph,
 per CTA the producer issue time and consumer-ready time of its first 32 stages
 (us from the layer's first CTA start).  Prints percentiles over CTAs per stage
-index, plus the layer's Q-available time (merge of the previous layer done)."""
+index, plus the layer's Q-available time (merge of the previous layer done).
+Needs the stamps compiled in:
+  make -C paper_2509_06261_b200/csrc clean && make -C paper_2509_06261_b200/csrc NVFLAGS_EXTRA=-DKVSLAB_STAGE_PROBES"""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
