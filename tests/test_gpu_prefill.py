@@ -112,3 +112,22 @@ def test_prefill_rejects_bad_group():
     cu = dev(np.array([0, 16], np.int32))
     with pytest.raises(Exception, match="GQA"):
         kv.paged_prefill(w["pool"], fmt, 0, q, dev(w["table"]), cu, dev(w["ctx"]), 16)
+
+
+@pytest.mark.parametrize("dt", [KvDtype.FP16, KvDtype.FP8_E4M3], ids=["FP16", "FP8"])
+def test_prefill_tc_long_context_and_layer(dt):
+    """tcgen05 path: a chunk at the end of a 3k context (47 KV tiles, 3-stage
+    ring wraps many times), layer 1 of a 2-layer key, plus a 1-token chunk."""
+    _, _, _, _, o, lse, r, rl = run_prefill(dt, 2, 8, [(3000, 300), (129, 1), (64, 64)], seed=41,
+                                            layers=2, layer=1)
+    assert rel_err(o, r) <= TOL[dt]
+    assert np.abs(lse - rl).max() <= 1e-3
+
+
+def test_prefill_tc_int4_gqa1_ragged():
+    """tcgen05 path, MHA (256 tokens per CTA), ragged chunks incl. empty ones."""
+    _, _, _, _, o, lse, r, rl = run_prefill(KvDtype.INT4, 2, 2, [(513, 300), (40, 0), (1000, 257), (3, 3)],
+                                            seed=43)
+    assert rel_err(o, r) <= 1e-2
+    assert np.abs(lse - rl).max() <= 1e-3
+
