@@ -7,15 +7,17 @@
 // 1e-2 (INT8/INT4) relative.
 //
 // Design:
-//  * Work = every (sequence, kv-head, block) of the batch, flattened
-//    seq-major; each warp of a persistent grid owns an equal contiguous range
-//    (stream-K style), so ragged contexts balance perfectly.  A unit (seq,
-//    kv-head) cut by a range boundary produces fp32 partials that the last
-//    finishing warp merges (per-unit counter; no second launch).
-//  * Each warp runs its own STAGES-deep ring: lane 0 issues 1-D
-//    cp.async.bulk copies (TMA engine) of the K chunk, V chunk, their
-//    quant params and -- at a unit start -- the G query rows, completing on a
-//    per-stage mbarrier.  Block-table entries are prefetched one block ahead.
+//  * Work = every (sequence, kv-head group, block) of the batch, flattened
+//    seq-major and cut into one equal contiguous range per CTA of a
+//    persistent grid (stream-K), so ragged contexts balance exactly.  A unit
+//    (sequence, head group) cut by a range boundary leaves fp32 partials that
+//    merge_kernel, launched behind with programmatic dependent launch,
+//    combines; whole units are written directly.
+//  * CTA = HG consumer warps (one kv head each) + one producer warp.  The
+//    producer streams each block's K, V and params of the group with
+//    cp.async.bulk (TMA engine; one copy when the group spans all kv heads)
+//    into a STAGES-deep ring of full/empty mbarriers, and the group's Q rows
+//    (plus, for the fused append, the new token's K/V rows) at unit starts.
 //  * QK^T and PV run on tensor cores as m16n8k16 tiles with the query group
 //    as N (8 or 16): S^T = K.Q^T (M = 16 tokens), O^T += V^T.P^T (M = dims).
 //    Quantised K/V enter the MMA as exact small integers (or e4m3 -> f16);
@@ -291,7 +293,7 @@ constexpr bool kPairs = NT == 1 && FMT != kFP16;  // FP16: no gain, spills
 // (full/empty mbarriers), and the group's Q rows into a ping-pong Q buffer at
 // each unit start.  Every consumer warp runs the tensor-core online softmax
 // for its head; a (sequence, head) cut by a CTA-range boundary leaves an fp32
-// partial that the warp finishing the unit last merges (per-unit counter).
+// partial that merge_kernel (the PDL-launched successor) combines.
 // <= 152 registers for the 9-warp CTA: three warps on one SM sub-partition
 // then leave room for a merge warp (<= 56 registers) of a co-resident merge CTA
 template <int FMT, int NT>
