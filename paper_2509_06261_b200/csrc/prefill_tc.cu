@@ -104,7 +104,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
 //   warps 9-11     : cp.async loaders (Q tiles, then a 3-stage K/V ring)
 // While one tile's softmax runs the tensor core works on the other tile, and
 // the K/V ring keeps two tiles in flight.  TMEM: S_A | S_B | O_A | O_B.
-constexpr uint32_t kLoadWarp0 = 9, kLoaders = 96, kThreads2 = 384;
+constexpr uint32_t kLoadWarp0 = 9;
+// FP16 needs only Q gathers and bulk copies from its 3 loader warps (12 warps,
+// <= 168 registers), FP8 little more (one cvt per pair); INT8/INT4 get 7
+// (16 warps, <= 128 registers: their dequantisation is the limiter, measured
+// +4-7 %; FP8 loses 10 % to the spills)
+template <int FMT>
+constexpr uint32_t kLoadersOf = (FMT == kINT8 || FMT == kINT4) ? 224u : 96u;
+template <int FMT>
+constexpr uint32_t kThreadsOf = kLoadWarp0 * 32 + kLoadersOf<FMT>;
 constexpr uint32_t k2TmemCols = 512;
 // Shared memory per format: Q (2 x 32 KB) | fp16 K/V operand ring | P (2 x
 // 16 KB) | raw ring.  FP16 chunks are operands as stored (3 operand stages,
@@ -190,8 +198,9 @@ __device__ __forceinline__ void dequant_granule(uint8_t* tile, uint32_t row, uin
 }
 
 template <int FMT>
-__global__ void __launch_bounds__(kThreads2, 1) prefill_tc2_kernel(const PrefillParams p) {
+__global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const PrefillParams p) {
   using Cfg = TcCfg<FMT>;
+  constexpr uint32_t kLoaders = kLoadersOf<FMT>;
   constexpr uint32_t kStages = Cfg::kStages, k2Q = Cfg::kQo, k2KV = Cfg::kKV, k2P = Cfg::kP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -559,7 +568,7 @@ static cudaError_t launch_tc(const PrefillParams& p0, cudaStream_t stream) {
   auto kern = prefill_tc2_kernel<FMT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<dim3(p.batch * p.H, p.tiles), kThreads2, smem, stream>>>(p);
+  kern<<<dim3(p.batch * p.H, p.tiles), kThreadsOf<FMT>, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
