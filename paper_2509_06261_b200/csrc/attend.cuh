@@ -291,7 +291,7 @@ constexpr float kRescaleSlack = 8.0f;  // log2 units: P <= 2^8 before a rescale
 // bits of the signal (INT4: bias/signal ~ 1024/8).  Folding the column sums of
 // u.zb into the accumulator every kBiasFlush blocks bounds the bias to a few
 // blocks' worth (measured: INT4 prefill at ctx 700, 1.5e-2 -> see DESIGN.md).
-constexpr uint32_t kBiasFlush = 4;
+constexpr uint32_t kBiasFlush = 8;
 template <int FMT, int NT>
 __device__ __forceinline__ void flush_bias(UnitState<NT>& u) {
   if constexpr (Geo<FMT>::kBiased) {

@@ -613,7 +613,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         attend<FMT, NT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
         release();
         release();
-        if ((i & 3) == 2) flush_bias<FMT, NT>(us);  // every kBiasFlush blocks
+        if ((i % kBiasFlush) == kBiasFlush - 2) flush_bias<FMT, NT>(us);  // every kBiasFlush blocks
       }
     }
     for (; i < nfull; ++i) {
