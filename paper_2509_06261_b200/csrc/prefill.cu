@@ -288,7 +288,13 @@ static cudaError_t launch_prefill_fmt(const PrefillParams& p0, cudaStream_t stre
 cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStream_t stream) {
   using namespace dev;
   // 8 query rows per warp (default: more warps, two-block steps) or 16 (GQA 16)
-  if (p.use_tc) return launch_paged_prefill_tc(p, kv_dtype, stream);
+  // tcgen05 kernel (two 128-row query tiles per CTA), except for quantised KV
+  // when every chunk has <= 64 query rows: the dequantising loaders then
+  // stream the whole context for a quarter-full tile, and the mma.sync kernel
+  // measured faster (INT4, 16 x chunk 16 at ctx 4k: 142 vs 186 us; at chunk
+  // 32 the tcgen05 kernel wins, 187 vs 295)
+  const bool small = kv_dtype != kFP16 && p.max_q_len * p.G <= 64;
+  if (p.use_tc && !small) return launch_paged_prefill_tc(p, kv_dtype, stream);
   const bool two = p.nt == 2 || p.G > 8;
   switch (kv_dtype) {
     case kFP16: return two ? launch_prefill_fmt<kFP16, 2>(p, stream) : launch_prefill_fmt<kFP16, 1>(p, stream);
