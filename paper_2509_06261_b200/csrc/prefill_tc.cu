@@ -97,6 +97,30 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       : "memory");
 }
 
+// 16 columns at a time (the O rescale runs while the 64 scores are live)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // v2: warp-specialised, two query tiles per CTA (FA4-style ping-pong).
 //   warps 0-3 / 4-7: softmax of query tile A / B (thread = row)
@@ -105,12 +129,11 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
 // While one tile's softmax runs the tensor core works on the other tile, and
 // the K/V ring keeps two tiles in flight.  TMEM: S_A | S_B | O_A | O_B.
 constexpr uint32_t kLoadWarp0 = 9;
-// FP16 needs only Q gathers and bulk copies from its 3 loader warps (12 warps,
-// <= 168 registers), FP8 little more (one cvt per pair); INT8/INT4 get 7
-// (16 warps, <= 128 registers: their dequantisation is the limiter, measured
-// +4-7 %; FP8 loses 10 % to the spills)
+// FP16 needs only Q gathers and bulk copies from its 3 loader warps (12 warps);
+// the dequantising formats get 7 (16 warps, <= 128 registers; with the O
+// rescale in 16-column TMEM chunks the spills are small): measured +6-14 %
 template <int FMT>
-constexpr uint32_t kLoadersOf = (FMT == kINT8 || FMT == kINT4) ? 224u : 96u;
+constexpr uint32_t kLoadersOf = FMT == kFP16 ? 96u : 224u;
 template <int FMT>
 constexpr uint32_t kThreadsOf = kLoadWarp0 * 32 + kLoadersOf<FMT>;
 constexpr uint32_t k2TmemCols = 512;
@@ -494,12 +517,12 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
       }
       if (t > 0 && __any_sync(0xffffffffu, grow)) {
 #pragma unroll
-        for (uint32_t c = 0; c < kD; c += 32) {
-          float o[32];
-          tmem_ld32(tO + c, o);
+        for (uint32_t c = 0; c < kD; c += 16) {
+          float o[16];
+          tmem_ld16(tO + c, o);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] *= alpha;
-          tmem_st32(tO + c, o);
+          for (int j = 0; j < 16; ++j) o[j] *= alpha;
+          tmem_st16(tO + c, o);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
