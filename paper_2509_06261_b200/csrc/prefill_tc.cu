@@ -97,6 +97,25 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       : "memory");
 }
 
+// Packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100a): two scores per
+// instruction in the softmax.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, c, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mov.b64 c, {%6, %7};\n\tfma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
 // 16 columns at a time (the O rescale runs while the 64 scores are live)
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -530,13 +549,18 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
         l *= alpha;
         m = mx;
       }
+      float2 l2 = make_float2(0.f, 0.f);
+      const float2 sml22 = make_float2(sml2, sml2), nm2 = make_float2(-m, -m);
 #pragma unroll
       for (uint32_t c = 0; c < kTile / 8; ++c) {
         float pv[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          pv[j] = kRaw ? ex2(fmaf(sc[c * 8 + j], sml2, -m)) : ex2(sc[c * 8 + j] - m);
-          l += pv[j];
+        for (int j = 0; j < 8; j += 2) {  // two scores per FFMA2 / FADD2
+          const float2 sj = make_float2(sc[c * 8 + j], sc[c * 8 + j + 1]);
+          const float2 xj = kRaw ? ffma2(sj, sml22, nm2) : fadd2(sj, nm2);
+          pv[j] = ex2(xj.x);
+          pv[j + 1] = ex2(xj.y);
+          l2 = fadd2(l2, make_float2(pv[j], pv[j + 1]));
         }
         uint4 w;
         w.x = pack_h2(pv[0], pv[1]);
@@ -545,6 +569,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
         w.w = pack_h2(pv[6], pv[7]);
         *reinterpret_cast<uint4*>(prow + sw128(r, c)) = w;
       }
+      l += l2.x + l2.y;
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&p_full[x]);
