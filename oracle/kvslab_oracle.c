@@ -394,6 +394,19 @@ static uint64_t fp16_off(const orc_fmt* f, uint32_t slot, uint32_t i) {
   return orc_swz((uint64_t)(i / 64) * T * 128 + (uint64_t)slot * 128 + 2ULL * (i % 64));
 }
 
+/* INT4 byte j (dims 2j, 2j+1) of token slot.  K: 64-byte token rows.  V (with
+ * T = 16, d = 128, as the kernels require): the PV fragment's token pair
+ * (tok_a, tok_b) = ({0,1,4,5}, {2,3,6,7}) (+8) shares one 128-byte line,
+ * interleaved in 2-byte units; other geometries keep
+ * token rows. */
+static uint64_t int4_off(const orc_fmt* f, uint32_t kv, uint32_t slot, uint32_t j) {
+  const uint32_t d = f->head_dim, T = f->tokens_per_block;
+  if (kv == 0 || d != 128 || T != 16) return orc_swz((uint64_t)slot * (d / 2) + j);
+  const uint32_t t8 = slot & 7, tp = (t8 & 1) | ((t8 >> 2) << 1), side = (t8 >> 1) & 1;
+  const uint32_t line = 2 * tp + (slot >> 3);
+  return orc_swz((uint64_t)line * 128 + 4 * (j >> 1) + 2 * side + (j & 1));
+}
+
 /* ======================= quantised append (K1 restated) ================== */
 static void quant_row(const orc_fmt* f, const uint16_t* x16, float fp8_scale, uint8_t* chunk,
                       uint32_t slot, uint8_t* params, uint32_t kv, uint32_t head) {
@@ -448,7 +461,7 @@ static void quant_row(const orc_fmt* f, const uint16_t* x16, float fp8_scale, ui
           q[j] = t > 15.0f ? 15 : (t < 0.0f ? 0 : (int)t);
         }
       }
-      chunk[orc_swz(base + i / 2)] = (uint8_t)(q[0] | (q[1] << 4));
+      chunk[int4_off(f, kv, slot, i / 2)] = (uint8_t)(q[0] | (q[1] << 4));
     }
     uint8_t* ps = params + (((uint64_t)kv * H + head) * T + slot) * 4;
     ps[0] = (uint8_t)(sh & 0xff);
@@ -503,7 +516,7 @@ void orc_dequant(const uint8_t* pool, uint64_t slab_size, uint64_t bps, const or
     double sf = orc_f16_to_f32((uint16_t)(ps[0] | (ps[1] << 8)));
     double zf = orc_f16_to_f32((uint16_t)(ps[2] | (ps[3] << 8)));
     for (uint32_t i = 0; i < d; ++i) {
-      uint8_t b = chunk[orc_swz(base + i / 2)];
+      uint8_t b = chunk[int4_off(f, kv, slot, i / 2)];
       int q = (i & 1) ? (b >> 4) : (b & 15);
       out[i] = (double)q * sf + zf;
     }

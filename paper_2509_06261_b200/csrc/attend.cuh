@@ -75,10 +75,11 @@ __device__ __forceinline__ FragOff make_offsets(int g, int t) {
     o.k[0] = swz(g * 64 + 16 * t);
     o.k[1] = swz((g + 8) * 64 + 16 * t);
     o.k[2] = o.k[3] = 0;
-    o.v[0] = swz(ta * 64 + 8 * g);
-    o.v[1] = swz(tb * 64 + 8 * g);
-    o.v[2] = swz((ta + 8) * 64 + 8 * g);
-    o.v[3] = swz((tb + 8) * 64 + 8 * g);
+    // V token-pair lines: 2t holds (ta, tb), 2t+1 holds (ta+8, tb+8); with
+    // the line-keyed swizzle a quarter-warp's 16-byte loads are conflict-free
+    o.v[0] = swz(2 * t * 128 + 16 * g);
+    o.v[1] = swz((2 * t + 1) * 128 + 16 * g);
+    o.v[2] = o.v[3] = 0;
   }
   return o;
 }
@@ -146,12 +147,13 @@ __device__ __forceinline__ void load_k_frags(uint32_t sK, const FragOff& o, uint
 
 // Q rows of the unit -> MMA B fragments for query g of each n-tile, with the
 // K dims permuted exactly like load_k_frags (the reduction order is free).
-template <int FMT, int NT>
+// PK (packed decode, G <= 4): column g carries query g & 3 (see attend_pk).
+template <int FMT, int NT, bool PK = false>
 __device__ __forceinline__ void load_q_frags(uint32_t sQ, int g, int t, uint32_t G,
                                              uint32_t (&qf)[NT][8][2]) {
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    const int qrow = nt * 8 + g;
+    const int qrow = PK ? (g & 3) : nt * 8 + g;
     const bool ok = qrow < static_cast<int>(G);
     const uint32_t row = sQ + qrow * kD * 2;
     if constexpr (FMT == kFP16) {
@@ -234,27 +236,21 @@ __device__ __forceinline__ void load_v_frags(uint32_t sV, const FragOff& o, uint
         }
       }
     }
-  } else {  // INT4: 8 bytes (16 dims) per token per thread
-    const uint2 va = lds64(sV + o.v[0]);
-    const uint2 vb = lds64(sV + o.v[1]);
-    const uint2 vc = lds64(sV + o.v[2]);
-    const uint2 vd = lds64(sV + o.v[3]);
-    const uint32_t A[2] = {va.x, va.y}, B[2] = {vb.x, vb.y}, C[2] = {vc.x, vc.y},
-                   Dd[2] = {vd.x, vd.y};
+  } else {  // INT4: one 16-byte load per token pair, [A.j A.j+1 B.j B.j+1] per word
+    const uint4 va = lds128(sV + o.v[0]);  // tokens ta, tb: bytes 8g .. 8g+7
+    const uint4 vc = lds128(sV + o.v[1]);  // tokens ta+8, tb+8
+    const uint32_t A[4] = {va.x, va.y, va.z, va.w}, C[4] = {vc.x, vc.y, vc.z, vc.w};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int w = i >> 2, k = i & 3;
-      // bytes [A.k, A.k, B.k, B.k]: A.k in the low half, B.k in the high half
-      const uint32_t sel = k | (k << 4) | ((4 + k) << 8) | ((4 + k) << 12);
-      const uint32_t ab = __byte_perm(A[w], B[w], sel);
-      const uint32_t cd = __byte_perm(C[w], Dd[w], sel);
+    for (int i = 0; i < 8; ++i) {  // m-tile i: byte 8g + i (dims 16g + 2i, +1)
+      const uint32_t x = (i & 1) ? A[i >> 1] >> 8 : A[i >> 1];
+      const uint32_t y = (i & 1) ? C[i >> 1] >> 8 : C[i >> 1];
       uint32_t* r = a[i];
       // rows g+8 (high nibbles, in place) enter as 1024 + 16 n: the epilogue
       // divides those output dims by 16
-      r[0] = lop3_and_or(ab, 0x000F000Fu, 0x64006400u);
-      r[1] = lop3_and_or(ab, 0x00F000F0u, 0x64006400u);
-      r[2] = lop3_and_or(cd, 0x000F000Fu, 0x64006400u);
-      r[3] = lop3_and_or(cd, 0x00F000F0u, 0x64006400u);
+      r[0] = lop3_and_or(x, 0x000F000Fu, 0x64006400u);
+      r[1] = lop3_and_or(x, 0x00F000F0u, 0x64006400u);
+      r[2] = lop3_and_or(y, 0x000F000Fu, 0x64006400u);
+      r[3] = lop3_and_or(y, 0x00F000F0u, 0x64006400u);
     }
   }
 }
@@ -448,6 +444,179 @@ __device__ __forceinline__ void attend(UnitState<NT>& u, const uint32_t (&sbs)[B
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
         mma16816(u.acc[mt][nt], va[mt][0], va[mt][1], va[mt][2], va[mt][3], pb[bi][nt][0], pb[bi][nt][1]);
+  }
+}
+
+// ------------------------------------------------- packed step (G <= 4)
+// With a query group of at most 4 the m16n8k16 score tile (N = 8 query
+// columns) would be half empty.  The packed step gives each tile column n the
+// query n & 3 and lets columns 0-3 attend block sbs[0] and columns 4-7 block
+// sbs[1]: two independent online-softmax streams of the same queries, folded
+// at the end of the unit segment (fold_halves).  The MMA count is unchanged
+// (both blocks' S^T and O^T tiles are computed in full); the per-element
+// score epilogue, the softmax, the scale loads and the P shuffles -- most of
+// a step's non-MMA instructions -- now serve two blocks.  Thread (g, t) owns
+// columns 2t, 2t+1, i.e. block t >> 1.  NB = 1: one block in columns 0-3,
+// columns 4-7 are masked (their P' is exactly 0).
+// Split in two so K2 can software-pipeline it: pk_scores (QK^T of the next
+// pair) is issued before pk_update (softmax + PV of the current pair), and the
+// two independent dependency chains interleave.
+template <int FMT, int NB>
+__device__ __forceinline__ void pk_scores(const uint32_t (&sbs)[2], uint32_t wK, const FragOff& fo,
+                                          const uint32_t (&qf)[1][8][2], int t, float (&dsel)[4]) {
+  const bool hb = t >= 2;  // this thread's columns attend block 1
+  float dot[NB][4];
+#pragma unroll
+  for (int bi = 0; bi < NB; ++bi) {
+    uint32_t ka[8][4];
+    load_k_frags<FMT>(sbs[bi] + wK, fo, ka);
+    float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 2) {
+      mma16816(s1, ka[kk][0], ka[kk][1], ka[kk][2], ka[kk][3], qf[0][kk][0], qf[0][kk][1]);
+      mma16816(s2, ka[kk + 1][0], ka[kk + 1][1], ka[kk + 1][2], ka[kk + 1][3], qf[0][kk + 1][0],
+               qf[0][kk + 1][1]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dot[bi][e] = s1[e] + s2[e];
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) dsel[e] = (NB == 2 && hb) ? dot[NB - 1][e] : dot[0][e];
+}
+
+template <int FMT, int NB, bool MASK>
+__device__ __forceinline__ void pk_update(UnitState<1>& u, const float (&dsel)[4],
+                                          const uint32_t (&sbs)[2], const int (&valid)[2],
+                                          uint32_t wK, uint32_t wP, uint32_t kvq, uint32_t pq,
+                                          const FragOff& fo, const float (&qsb)[1][2],
+                                          const float (&qst)[1][2], float kscale, float sml2, int g,
+                                          int t) {
+  using Gm = Geo<FMT>;
+  const bool hb = t >= 2;
+  // ---- this thread's block: token scales and the score epilogue ----
+  const uint32_t sbh = (NB == 2 && hb) ? sbs[1] : sbs[0];
+  const int vh = NB == 2 ? (hb ? valid[1] : valid[0]) : (hb ? 0 : valid[0]);
+  float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f}, svv[2] = {1.f, 1.f}, zvv[2] = {0.f, 0.f};
+  const uint32_t sKp = sbh + wP, sVp = sKp + pq;
+  if constexpr (FMT == kINT8) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
+      svv[r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
+    }
+  } else if constexpr (FMT == kINT4) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
+      sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
+      zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
+      svv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
+      zvv[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
+    }
+  }
+  float sc[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int r = e >> 1;
+    float x;
+    if constexpr (Gm::kBiased)  // s * (dot' - bias*sum(q')) + z * sum(q)
+      x = sk[r] * (dsel[e] - Gm::kBias * qsb[0][e & 1]) + zk[r] * qst[0][e & 1];
+    else
+      x = dsel[e] * sk[r];
+    sc[e] = (MASK || NB == 1) && !(g + 8 * r < vh) ? -INFINITY : x * sml2;
+  }
+  // ---- online softmax (lazy rescale, as in attend) ----
+  bool grow = false;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) grow |= sc[e] > u.m[0][e & 1] + kRescaleSlack;
+  if (__any_sync(0xffffffffu, grow)) {
+    float mx[2] = {fmaxf(sc[0], sc[2]), fmaxf(sc[1], sc[3])};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 4));
+      mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 8));
+      mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], 16));
+      const float mn = fmaxf(u.m[0][c], mx[c]);
+      const float alpha = ex2(u.m[0][c] - mn);
+      u.m[0][c] = mn;
+      u.l[0][c] *= alpha;
+      u.zb[0][c] *= alpha;
+      u.zz[0][c] *= alpha;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        u.acc[mt][0][c] *= alpha;
+        u.acc[mt][0][2 + c] *= alpha;
+      }
+    }
+  }
+  float pr[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) pr[e] = ex2(sc[e] - u.m[0][e & 1]);
+  const uint32_t plo = pack_h2(pr[0] * svv[0], pr[1] * svv[0]);
+  const uint32_t phi = pack_h2(pr[2] * svv[1], pr[3] * svv[1]);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) u.l[0][c] += pr[c] + pr[c + 2];
+  if constexpr (Gm::kBiased) {
+    const float2 flo = __half22float2(*reinterpret_cast<const __half2*>(&plo));
+    const float2 fhi = __half22float2(*reinterpret_cast<const __half2*>(&phi));
+    u.zb[0][0] -= Gm::kBias * (flo.x + fhi.x);
+    u.zb[0][1] -= Gm::kBias * (flo.y + fhi.y);
+    if constexpr (FMT == kINT4) {
+      u.zz[0][0] += pr[0] * zvv[0] + pr[2] * zvv[1];
+      u.zz[0][1] += pr[1] * zvv[0] + pr[3] * zvv[1];
+    }
+  }
+  const int la = tok_a<FMT>(t) * 4 + (g >> 1), lb = tok_b<FMT>(t) * 4 + (g >> 1);
+  const uint32_t xa = __shfl_sync(0xffffffffu, plo, la), xb = __shfl_sync(0xffffffffu, plo, lb);
+  const uint32_t ya = __shfl_sync(0xffffffffu, phi, la), yb = __shfl_sync(0xffffffffu, phi, lb);
+  const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;
+  const uint32_t pb0 = __byte_perm(xa, xb, sel), pb1 = __byte_perm(ya, yb, sel);
+  // ---- O^T += V^T . P^T: block bi feeds only its own columns (B column = g) ----
+#pragma unroll
+  for (int bi = 0; bi < NB; ++bi) {
+    const bool mine = NB == 1 || ((g >> 2) == bi);
+    const uint32_t b0 = mine ? pb0 : 0u, b1 = mine ? pb1 : 0u;
+    uint32_t va[8][4];
+    load_v_frags<FMT>(sbs[bi] + kvq + wK, fo, va);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) mma16816(u.acc[mt][0], va[mt][0], va[mt][1], va[mt][2], va[mt][3], b0, b1);
+  }
+}
+
+template <int FMT, int NB, bool MASK>
+__device__ __forceinline__ void attend_pk(UnitState<1>& u, const uint32_t (&sbs)[2],
+                                          const int (&valid)[2], uint32_t wK, uint32_t wP,
+                                          uint32_t kvq, uint32_t pq, const FragOff& fo,
+                                          const uint32_t (&qf)[1][8][2], const float (&qsb)[1][2],
+                                          const float (&qst)[1][2], float kscale, float sml2, int g,
+                                          int t) {
+  float d[4];
+  pk_scores<FMT, NB>(sbs, wK, fo, qf, t, d);
+  pk_update<FMT, NB, MASK>(u, d, sbs, valid, wK, wP, kvq, pq, fo, qsb, qst, kscale, sml2, g, t);
+}
+
+// Folds the two packed streams (columns c and c + 4 = lanes t and t ^ 2) of
+// every query into one online-softmax state, as the merge kernel does.
+// Afterwards threads t < 2 hold the unit segment's state of queries 2t, 2t+1.
+__device__ __forceinline__ void fold_halves(UnitState<1>& u) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const float mo = __shfl_xor_sync(0xffffffffu, u.m[0][c], 2);
+    const float mn = fmaxf(u.m[0][c], mo);
+    const float a = ex2(u.m[0][c] - mn);
+    u.m[0][c] = mn;
+    auto f = [&](float x) {
+      x *= a;
+      return x + __shfl_xor_sync(0xffffffffu, x, 2);
+    };
+    u.l[0][c] = f(u.l[0][c]);
+    u.zb[0][c] = f(u.zb[0][c]);
+    u.zz[0][c] = f(u.zz[0][c]);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      u.acc[mt][0][c] = f(u.acc[mt][0][c]);
+      u.acc[mt][0][2 + c] = f(u.acc[mt][0][2 + c]);
+    }
   }
 }
 

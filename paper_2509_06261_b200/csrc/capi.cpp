@@ -757,6 +757,7 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
     if (const char* sb = std::getenv("KVSLAB_DECODE_SMEM")) p.smem_budget = static_cast<uint32_t>(std::atoi(sb));
     if (const char* mt = std::getenv("KVSLAB_MERGE_THREADS")) p.merge_threads = static_cast<uint32_t>(std::atoi(mt));
     if (const char* md = std::getenv("KVSLAB_MERGE_DC")) p.merge_dc = static_cast<uint32_t>(std::atoi(md));
+    if (const char* pk = std::getenv("KVSLAB_DECODE_PACK")) p.pack_mode = static_cast<uint32_t>(std::atoi(pk));
     p.pdl = 1;
     if (const char* tr = std::getenv("KVSLAB_DECODE_TRACE"))
       p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(tr, nullptr, 0));

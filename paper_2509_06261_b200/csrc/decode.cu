@@ -280,8 +280,8 @@ __device__ __forceinline__ void trace_ready(const DecodeParams& p, int warp, int
 
 // Formats whose consumer step runs two full blocks at a time (measured per format
 // with scripts/microbench_consumer.cu and in the kernel).
-template <int FMT, int NT>
-constexpr bool kPairs = NT == 1 && FMT != kFP16;  // FP16: no gain, spills
+template <int FMT, int NT, bool PK>
+constexpr bool kPairs = NT == 1 && (PK || FMT != kFP16);  // FP16 unpacked: no gain, spills
 
 // ------------------------------------------------------------------ kernel
 // CTA = HG consumer warps (one KV head each, a head group) + 1 producer warp.
@@ -296,7 +296,9 @@ constexpr bool kPairs = NT == 1 && FMT != kFP16;  // FP16: no gain, spills
 // partial that merge_kernel (the PDL-launched successor) combines.
 // <= 152 registers for the 9-warp CTA: three warps on one SM sub-partition
 // then leave room for a merge warp (<= 56 registers) of a co-resident merge CTA
-template <int FMT, int NT>
+// PK: packed step for G <= 4 (attend_pk): tile columns 0-3 and 4-7 attend
+// alternate blocks of the segment, folded at the segment end.
+template <int FMT, int NT, bool PK>
 __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const DecodeParams p) {
   using Gm = Geo<FMT>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -543,7 +545,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     {  // ---- unit segment start: Q fragments, state ----
       const uint32_t qs = ui & 1;
       if (!compute_only) mbar_wait(&qfull[qs], (ui >> 1) & 1);
-      load_q_frags<FMT, NT>(smem_u32(qbuf + qs * qslot) + warp * p.G * kD * 2, g, t, p.G, qf);
+      load_q_frags<FMT, NT, PK>(smem_u32(qbuf + qs * qslot) + warp * p.G * kD * 2, g, t, p.G, qf);
       if (p.k_new != nullptr && has_last) {  // staged with Q by the producer
         const uint32_t nk = smem_u32(qbuf + qs * qslot + qbytes) + warp * kD * 2 + lane * 8;
         new_k = lds64(nk);
@@ -574,7 +576,8 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
           qst[nt][0] = __shfl_sync(0xffffffffu, stq, (2 * t) * 4);
           qst[nt][1] = __shfl_sync(0xffffffffu, stq, (2 * t + 1) * 4);
         }
-        us.m[nt][0] = us.m[nt][1] = -INFINITY;
+        // packed: finite so a column stream that sees no block stays NaN-free
+        us.m[nt][0] = us.m[nt][1] = PK ? -1e30f : -INFINITY;
         us.l[nt][0] = us.l[nt][1] = 0.f;
         us.zb[nt][0] = us.zb[nt][1] = 0.f;
         us.zz[nt][0] = us.zz[nt][1] = 0.f;
@@ -596,7 +599,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     // ---- full blocks: all 16 tokens valid ----
     const uint32_t nfull = seg_len - (has_last ? 1u : 0u);
     uint32_t i = 0;
-    if constexpr (kPairs<FMT, NT>) {
+    if constexpr (kPairs<FMT, NT, PK>) {
       // two full blocks per step: two independent score tiles, one softmax
       // update (INT4: the dequant-heavy step gains from the extra ILP)
       for (; i + 1 < nfull; i += 2) {
@@ -610,7 +613,10 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         trace_ready(p, warp, lane, k + i + 1);
         const uint32_t sbs[2] = {sb, sb1};
         const int valid[2] = {kTPB, kTPB};
-        attend<FMT, NT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+        if constexpr (PK)
+          attend_pk<FMT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+        else
+          attend<FMT, NT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
         release();
         release();
         if ((i % kBiasFlush) == kBiasFlush - 2) flush_bias<FMT, NT>(us);  // every kBiasFlush blocks
@@ -619,10 +625,16 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     for (; i < nfull; ++i) {
       if (!compute_only) mbar_wait(&full[st], ph);
       trace_ready(p, warp, lane, k + i);
-      const uint32_t sbs[1] = {sb};
-      const int valid[1] = {kTPB};
-      if (!(p.debug & 8))  // probe: stream only
-        attend<FMT, NT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+      if constexpr (PK) {
+        const uint32_t sbs[2] = {sb, sb};
+        const int valid[2] = {kTPB, 0};
+        attend_pk<FMT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+      } else {
+        const uint32_t sbs[1] = {sb};
+        const int valid[1] = {kTPB};
+        if (!(p.debug & 8))  // probe: stream only
+          attend<FMT, NT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+      }
       release();
       if (i % kBiasFlush == kBiasFlush - 1) flush_bias<FMT, NT>(us);
     }
@@ -650,11 +662,19 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         put_row<FMT>(sst + kvq + warp * Gm::kChunk, sprm, slot, 1, warp, HG, kTPB, rv, scv, false, lane);
         __syncwarp();
       }
-      const uint32_t sbs[1] = {sb};
-      const int valid[1] = {ctx_cur - static_cast<int>(cc.nblk - 1) * kTPB};
-      attend<FMT, NT, 1, true>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+      const int vlast = ctx_cur - static_cast<int>(cc.nblk - 1) * kTPB;
+      if constexpr (PK) {
+        const uint32_t sbs[2] = {sb, sb};
+        const int valid[2] = {vlast, 0};
+        attend_pk<FMT, 1, true>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+      } else {
+        const uint32_t sbs[1] = {sb};
+        const int valid[1] = {vlast};
+        attend<FMT, NT, 1, true>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+      }
       release();
     }
+    if constexpr (PK) fold_halves(us);
     const bool first_seg = k == 0;  // the segment opens this CTA's range
     k += seg_len;
     cc.b = seg_b0 + seg_len - 1;  // last block consumed
@@ -735,7 +755,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
 
 // Ring depth per format: ~150-200 KB in flight per SM with one CTA (HG
 // consumer warps + a producer) per SM.
-template <int FMT, int NT>
+template <int FMT, int NT, bool PK>
 static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t stream) {
   using Gm = Geo<FMT>;
   DecodeParams p = p0;
@@ -756,7 +776,7 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   p.bar_offset = (p.qbuf_offset + 2 * qbytes + 15) / 16 * 16;
   p.prefix_offset = p.bar_offset + (2 * stages + 4) * 8 + stages * 8;  // + stage block addresses
   const size_t smem = p.prefix_offset + (p.batch + 1) * 4;
-  auto kern = paged_decode_kernel<FMT, NT>;
+  auto kern = paged_decode_kernel<FMT, NT, PK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -812,13 +832,22 @@ cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms
                                 cudaStream_t stream) {
   using namespace dev;
   const bool two = p.G > 8;
+  // packed G <= 4 step: INT4 by default (measured: INT4 B64 ctx4k 69.5 -> 66.5 us;
+  // FP8/INT8 neutral at large batch and ~0.5 us slower at B16, FP16 neutral)
+  const bool pk = p.G <= 4 && p.pack_mode != 1 && (kv_dtype == kINT4 || p.pack_mode == 2);
+#define KVSLAB_DECODE_CASE(F)                                          \
+  case F:                                                              \
+    if (two) return launch_fmt<F, 2, false>(p, num_sms, stream);       \
+    if (pk) return launch_fmt<F, 1, true>(p, num_sms, stream);         \
+    return launch_fmt<F, 1, false>(p, num_sms, stream);
   switch (kv_dtype) {
-    case kFP16: return two ? launch_fmt<kFP16, 2>(p, num_sms, stream) : launch_fmt<kFP16, 1>(p, num_sms, stream);
-    case kFP8: return two ? launch_fmt<kFP8, 2>(p, num_sms, stream) : launch_fmt<kFP8, 1>(p, num_sms, stream);
-    case kINT8: return two ? launch_fmt<kINT8, 2>(p, num_sms, stream) : launch_fmt<kINT8, 1>(p, num_sms, stream);
-    case kINT4: return two ? launch_fmt<kINT4, 2>(p, num_sms, stream) : launch_fmt<kINT4, 1>(p, num_sms, stream);
+    KVSLAB_DECODE_CASE(kFP16)
+    KVSLAB_DECODE_CASE(kFP8)
+    KVSLAB_DECODE_CASE(kINT8)
+    KVSLAB_DECODE_CASE(kINT4)
     default: return cudaErrorInvalidValue;
   }
+#undef KVSLAB_DECODE_CASE
 }
 
 size_t decode_partials_bytes(int num_sms, int G) {

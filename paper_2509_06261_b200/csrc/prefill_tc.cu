@@ -220,6 +220,37 @@ __device__ __forceinline__ void dequant_granule(uint8_t* tile, uint32_t row, uin
   }
 }
 
+// INT4 V granule of the token-pair layout: 16 dims
+// (bytes j .. j+7) of two tokens interleaved in 2-byte units,
+// w = [A.j A.j+1 B.j B.j+1][A.j+2 ...]; scaled as in dequant_granule.
+__device__ __forceinline__ void dequant_int4_vpair(uint8_t* tile, uint32_t row_a, uint32_t row_b, uint32_t d0,
+                                                   uint4 w, uint32_t sza, uint32_t szb) {
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const uint32_t sel = side ? 0x7632u : 0x5410u, sz = side ? szb : sza;
+    const uint32_t wd[2] = {__byte_perm(w.x, w.y, sel), __byte_perm(w.z, w.w, sel)};
+    const uint32_t sc = sz & 0xffffu, z = sz >> 16;
+    const uint32_t s2 = sc | (hmul2_u32(sc, 0x2C00u) << 16);
+    const uint32_t z2 = z | (z << 16);
+    uint32_t o[8];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t y = __byte_perm(wd[i], 0, k | (k << 8) | (k << 16) | (k << 24));
+        const uint32_t n = hsub2_u32(lop3_and_or(y, 0x00F0000Fu, 0x64006400u), 0x64006400u);
+        o[4 * i + k] = hfma2_u32(n, s2, z2);
+      }
+    const uint32_t row = side ? row_b : row_a;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t d = d0 + 8 * h, half = d >> 6, gran = (d & 63) >> 3;
+      *reinterpret_cast<uint4*>(tile + half * (kTile * 128) + sw128(row, gran)) =
+          make_uint4(o[4 * h], o[4 * h + 1], o[4 * h + 2], o[4 * h + 3]);
+    }
+  }
+}
+
 template <int FMT>
 __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const PrefillParams p) {
   using Cfg = TcCfg<FMT>;
@@ -341,6 +372,17 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
           const uint32_t tok = lb / kRowB, d0 = (lb % kRowB) * 8 / Fmt<FMT>::kBits;
           const uint8_t* rb = raw + bi * kRB;
           const uint4 w = *reinterpret_cast<const uint4*>(rb + kv * kC + off);
+          if constexpr (FMT == kINT4) {
+            if (kv == 1) {  // token-pair line: tokens (tok_a, tok_b) [+8], 16 dims each
+              const uint32_t tp = line >> 1;
+              const uint32_t ta = (tp & 1) + ((tp >> 1) << 2) + 8 * (line & 1), tb = ta + 2;
+              const uint8_t* pv = rb + 2 * kC + kPm;
+              dequant_int4_vpair(kt + kKVBytes, bi * kTPB + ta, bi * kTPB + tb, 2 * ((lo >> 4) * 8), w,
+                                 *reinterpret_cast<const uint32_t*>(pv + ta * 4),
+                                 *reinterpret_cast<const uint32_t*>(pv + tb * 4));
+              continue;
+            }
+          }
           uint32_t sz = 0;
           if constexpr (FMT == kINT8) sz = *reinterpret_cast<const uint16_t*>(rb + 2 * kC + kv * kPm + tok * 2);
           if constexpr (FMT == kINT4) sz = *reinterpret_cast<const uint32_t*>(rb + 2 * kC + kv * kPm + tok * 4);

@@ -192,6 +192,47 @@ def test_decode_matches_oracle(dt, Hkv, Hq, ctx):
     assert np.isneginf(l[~live]).all()
 
 
+PACK_CASES = [
+    # (dtype, Hkv, Hq, ctx lens): G = 4, 2, 1 with odd/even block counts per unit
+    (KvDtype.FP16, 8, 32, [4096, 17, 33, 1, 0, 48]),
+    (KvDtype.FP8_E4M3, 4, 8, [2000, 31, 16]),
+    (KvDtype.INT8, 8, 32, [3000, 49, 2]),
+    (KvDtype.INT8, 4, 4, [700, 65]),
+    (KvDtype.INT4, 8, 32, [4100, 15, 16, 32, 0]),
+    (KvDtype.INT4, 2, 4, [999, 1024]),
+]
+
+
+@pytest.mark.parametrize("mode", ["1", "2"], ids=["unpacked", "packed"])
+@pytest.mark.parametrize("dt,Hkv,Hq,ctx", PACK_CASES,
+                         ids=[f"{c[0].name}-{c[1]}x{c[2]}" for c in PACK_CASES])
+def test_decode_packed_and_unpacked_steps(dt, Hkv, Hq, ctx, mode, monkeypatch):
+    """Both K2 inner steps for G <= 4 -- the packed one (tile columns 0-3 and
+    4-7 attend alternate blocks, folded per segment) and the plain one --
+    match the oracle for every format (the default picks one per format)."""
+    monkeypatch.setenv("KVSLAB_DECODE_PACK", mode)
+    fmt = KvFormat(dt, Hkv, Hq, num_layers=1)
+    sc = list(np.linspace(0.5, 1.5, 2 * Hkv)) if dt == KvDtype.FP8_E4M3 else None
+    w = make_world(fmt, ctx, seed=11 + Hq, fp8_scale=sc)
+    append_gpu(w, fmt, 0)
+    img = kv.kv_tensor(w["pool"]).cpu().numpy()
+    q = w["rng"].standard_normal((len(ctx), Hq, 128)).astype(np.float16)
+    lse = torch.empty((len(ctx), Hq), dtype=torch.float32, device="cuda")
+    out = kv.paged_decode(w["pool"], fmt, 0, dev(q), dev(w["table"]), dev(w["ctx"]), lse=lse,
+                          kv_scales=None if w["scales"] is None else dev(w["scales"]))
+    torch.cuda.synchronize()
+    f = oracle.fmt(int(dt), Hkv, Hq, 128, 1, 16, fmt.qparams)
+    ref, ref_lse = oracle.paged_decode(img, w["pool"].slab_size(),
+                                       w["pool"].blocks_per_slab(fmt.key), f, 0, q.view(np.uint16),
+                                       w["table"], w["ctx"], 1 / math.sqrt(128), w["scales"],
+                                       nthreads=oracle.NPROC)
+    o = out.cpu().numpy()
+    live = w["ctx"] > 0
+    assert rel_err(o[live], ref[live]) <= TOL[dt]
+    assert (o[~live] == 0).all()
+    assert np.abs(lse.cpu().numpy()[live] - ref_lse[live]).max() < 1e-3
+
+
 @pytest.mark.parametrize("dt", FORMATS, ids=[d.name for d in FORMATS])
 def test_decode_repeatable_and_workspace_clean(dt):
     """Two launches give identical bits (merge counters reset themselves)."""
