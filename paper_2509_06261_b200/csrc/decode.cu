@@ -522,9 +522,10 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
   const uint32_t slot_f = slot_hdr + p.G * kD;
   const float sml2 = p.sm_scale_log2;
   const uint32_t wK = warp * Gm::kChunk, wP = 2 * kvq + warp * Gm::kParam;
+  const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
   auto release = [&]() {
     __syncwarp();
-    if (lane == 0 && !compute_only) mbar_arrive(&empty[st]);
+    if (lane == 0 && !compute_only) mbar_arrive_s(empty_s + 8 * st);
     sb += p.stage_bytes;
     if (++st == S) {
       st = 0;
@@ -606,8 +607,8 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         const uint32_t sb1 = sb + p.stage_bytes == ring_end ? ring_u32 : sb + p.stage_bytes;
         const uint32_t st1 = st + 1 == S ? 0 : st + 1, ph1 = st + 1 == S ? ph ^ 1 : ph;
         if (!compute_only) {
-          mbar_wait(&full[st], ph);
-          mbar_wait(&full[st1], ph1);
+          mbar_wait_s(full_s + 8 * st, ph);
+          mbar_wait_s(full_s + 8 * st1, ph1);
         }
         trace_ready(p, warp, lane, k + i);
         trace_ready(p, warp, lane, k + i + 1);
@@ -623,7 +624,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       }
     }
     for (; i < nfull; ++i) {
-      if (!compute_only) mbar_wait(&full[st], ph);
+      if (!compute_only) mbar_wait_s(full_s + 8 * st, ph);
       trace_ready(p, warp, lane, k + i);
       if constexpr (PK) {
         const uint32_t sbs[2] = {sb, sb};
@@ -640,7 +641,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     }
     // ---- the unit's last block (partial; holds the appended token) ----
     if (has_last) {
-      if (!compute_only) mbar_wait(&full[st], ph);
+      if (!compute_only) mbar_wait_s(full_s + 8 * st, ph);
       trace_ready(p, warp, lane, k + nfull);
       if (app) {
         // Fused K1: the block holding the new token (position ctx-1) was
