@@ -516,14 +516,19 @@ __device__ __forceinline__ void pk_update(UnitState<1>& u, const float (&dsel)[4
   }
   float sc[4];
 #pragma unroll
+  for (int r = 0; r < 2; ++r) {  // the softmax scale rides in the row scales
+    sk[r] *= sml2;
+    zk[r] *= sml2;
+  }
+#pragma unroll
   for (int e = 0; e < 4; ++e) {
     const int r = e >> 1;
     float x;
-    if constexpr (Gm::kBiased)  // s * (dot' - bias*sum(q')) + z * sum(q)
+    if constexpr (Gm::kBiased)  // s' * (dot' - bias*sum(q')) + z' * sum(q)
       x = sk[r] * (dsel[e] - Gm::kBias * qsb[0][e & 1]) + zk[r] * qst[0][e & 1];
     else
       x = dsel[e] * sk[r];
-    sc[e] = (MASK || NB == 1) && !(g + 8 * r < vh) ? -INFINITY : x * sml2;
+    sc[e] = (MASK || NB == 1) && !(g + 8 * r < vh) ? -INFINITY : x;
   }
   // ---- online softmax (lazy rescale, as in attend) ----
   bool grow = false;

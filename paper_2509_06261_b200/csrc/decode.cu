@@ -599,6 +599,9 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
 
     // ---- full blocks: all 16 tokens valid ----
     const uint32_t nfull = seg_len - (has_last ? 1u : 0u);
+    // packed: each column stream sees every other block, so twice the blocks
+    // between flushes keep the same per-stream bias bound
+    constexpr uint32_t kFlush = PK ? 2 * kBiasFlush : kBiasFlush;
     uint32_t i = 0;
     if constexpr (kPairs<FMT, NT, PK>) {
       // two full blocks per step: two independent score tiles, one softmax
@@ -620,7 +623,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
           attend<FMT, NT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
         release();
         release();
-        if ((i % kBiasFlush) == kBiasFlush - 2) flush_bias<FMT, NT>(us);  // every kBiasFlush blocks
+        if ((i % kFlush) == kFlush - 2) flush_bias<FMT, NT>(us);  // every kFlush blocks
       }
     }
     for (; i < nfull; ++i) {
@@ -637,7 +640,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
           attend<FMT, NT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
       }
       release();
-      if (i % kBiasFlush == kBiasFlush - 1) flush_bias<FMT, NT>(us);
+      if (i % kFlush == kFlush - 1) flush_bias<FMT, NT>(us);
     }
     // ---- the unit's last block (partial; holds the appended token) ----
     if (has_last) {
