@@ -325,22 +325,22 @@ __device__ __forceinline__ void attend(UnitState<NT>& u, const uint32_t (&sbs)[B
   for (int bi = 0; bi < BPI; ++bi) {
     uint32_t ka[8][4];
     load_k_frags<FMT>(sbs[bi] + wK, fo, ka);
-    float sk[2] = {kscale, kscale}, zk[2] = {0.f, 0.f};
+    float sk[2] = {kscale * sml2, kscale * sml2}, zk[2] = {0.f, 0.f};  // softmax scale folded in
     svv[bi][0] = svv[bi][1] = 1.f;
     zvv[bi][0] = zvv[bi][1] = 0.f;
     const uint32_t sKp = sbs[bi] + wP, sVp = sKp + pq;
     if constexpr (FMT == kINT8) {
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
+        sk[r] = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r)))) * sml2;
         svv[bi][r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
       }
     } else if constexpr (FMT == kINT4) {
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
-        sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff)));
-        zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16)));
+        sk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp & 0xffff))) * sml2;
+        zk[r] = __half2float(__ushort_as_half(static_cast<uint16_t>(kp >> 16))) * sml2;
         svv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp & 0xffff)));
         zvv[bi][r] = __half2float(__ushort_as_half(static_cast<uint16_t>(vp >> 16)));
       }
@@ -359,13 +359,13 @@ __device__ __forceinline__ void attend(UnitState<NT>& u, const uint32_t (&sbs)[B
         const int r = e >> 1;
         const float dot = s1[e] + s2[e];
         float x;
-        if constexpr (Gm::kBiased)  // s * (dot' - bias*sum(q')) + z * sum(q)
+        if constexpr (Gm::kBiased)  // s' * (dot' - bias*sum(q')) + z' * sum(q)
           x = sk[r] * (dot - Gm::kBias * qsb[nt][e & 1]) + zk[r] * qst[nt][e & 1];
         else
           x = dot * sk[r];
         bool ok = g + 8 * r < valid[bi];
         if constexpr (CAUSAL) ok = ok && g + 8 * r < qlim[nt][e & 1];
-        sc[bi][nt][e] = ok ? x * sml2 : -INFINITY;
+        sc[bi][nt][e] = ok ? x : -INFINITY;
       }
     }
   }
