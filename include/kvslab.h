@@ -276,6 +276,22 @@ ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t laye
                            uint32_t batch, uint32_t max_q_len, float sm_scale,
                            const float* d_kv_scales, void* stream);
 
+/* K4 with a workspace (quantised formats).  When the chunk is long enough
+ * that every KV tile would be dequantised by several query-tile CTAs
+ * (max_q_len x GQA group >= 1024), the context blocks are first expanded
+ * once into fp16 scratch blocks (block b of sequence s at s*bt_stride + b,
+ * laid out like FP16 slab blocks) and attended by the FP16 tcgen05 kernel.
+ * d_workspace >= ks_paged_prefill_workspace_size bytes (0 for FP16); a null
+ * workspace, FP16, or a short chunk runs exactly ks_paged_prefill. */
+ks_status ks_paged_prefill_workspace_size(const ks_kv_format* fmt, uint32_t batch, uint32_t bt_stride,
+                                          size_t* bytes);
+ks_status ks_paged_prefill_ws(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
+                              void* d_out, float* d_lse, const int32_t* d_block_table,
+                              uint32_t bt_stride, const int32_t* d_cu_q, const int32_t* d_ctx_lens,
+                              uint32_t batch, uint32_t max_q_len, float sm_scale,
+                              const float* d_kv_scales, void* d_workspace, size_t workspace_bytes,
+                              void* stream);
+
 /* Spatial sharing between co-located models (MPS-style SM partitioning,
  * PAPER.md section 2.4): cap the persistent K2 grid of the model with slab
  * key `key` at max_ctas CTAs (one CTA per SM), so co-located models' decode

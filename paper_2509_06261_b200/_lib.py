@@ -121,6 +121,9 @@ _SIGS = {
                                     u32, C.c_float, P, P, C.c_size_t, P]),
     "ks_paged_prefill": (st, [P, C.POINTER(ks_kv_format), u32, P, P, P, P, u32, P, P, u32, u32,
                               C.c_float, P, P]),
+    "ks_paged_prefill_workspace_size": (st, [C.POINTER(ks_kv_format), u32, u32, C.POINTER(C.c_size_t)]),
+    "ks_paged_prefill_ws": (st, [P, C.POINTER(ks_kv_format), u32, P, P, P, P, u32, P, P, u32, u32,
+                                 C.c_float, P, P, C.c_size_t, P]),
     "ks_set_decode_sm_share": (st, [P, u64, u32]),
     "ks_compact_plan": (st, [P, u64, u32, C.POINTER(ks_block_move), pu32, pu32]),
     "ks_compact_apply": (st, [P, u64, C.POINTER(ks_block_move), u32, P]),

@@ -792,11 +792,26 @@ ks_status ks_paged_decode_append(ks_pool* pool, const ks_kv_format* fmt, uint32_
                      workspace_bytes, stream);
 }
 
-ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
-                           void* d_out, float* d_lse, const int32_t* d_block_table,
-                           uint32_t bt_stride, const int32_t* d_cu_q, const int32_t* d_ctx_lens,
-                           uint32_t batch, uint32_t max_q_len, float sm_scale,
-                           const float* d_kv_scales, void* stream) {
+ks_status ks_paged_prefill_workspace_size(const ks_kv_format* fmt, uint32_t batch, uint32_t bt_stride,
+                                          size_t* bytes) {
+  if (!fmt || !bytes) return fail(KS_INVALID_ARGUMENT, "null argument");
+  *bytes = fmt->kv_dtype == KS_KV_FP16 ? 0 : kvslab::prefill_expand_bytes(fmt->num_kv_heads, batch, bt_stride);
+  return KS_OK;
+}
+
+// Expand-once pays off when each KV tile would otherwise be dequantised by
+// several query-tile CTAs of a head (two 128-row tiles per CTA).
+static bool prefill_expands(uint32_t max_q_len, uint32_t G) {
+  if (const char* e = std::getenv("KVSLAB_PREFILL_EXPAND")) return std::atoi(e) != 0;
+  return static_cast<uint64_t>(max_q_len) * G >= 1024;
+}
+
+static ks_status prefill_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
+                              void* d_out, float* d_lse, const int32_t* d_block_table,
+                              uint32_t bt_stride, const int32_t* d_cu_q, const int32_t* d_ctx_lens,
+                              uint32_t batch, uint32_t max_q_len, float sm_scale,
+                              const float* d_kv_scales, void* d_workspace, size_t workspace_bytes,
+                              void* stream) {
   return guarded([&] {
     FmtInfo fi;
     ks_status st = check_kernel_format(pool, fmt, &fi);
@@ -834,12 +849,43 @@ ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t laye
     p.use_tc = 2;
     if (const char* tc = std::getenv("KVSLAB_PREFILL_TC")) p.use_tc = std::atoi(tc);
     if (const char* dbg = std::getenv("KVSLAB_PREFILL_DEBUG")) p.debug = std::atoi(dbg);
+    const bool expand = d_workspace != nullptr && fmt->kv_dtype != KS_KV_FP16 && p.use_tc &&
+                        prefill_expands(max_q_len, G);
+    if (expand) {
+      if (workspace_bytes < kvslab::prefill_expand_bytes(p.H, batch, bt_stride))
+        return fail(KS_INVALID_ARGUMENT, "prefill workspace too small");
+      cudaError_t e = kvslab::launch_paged_prefill_expand(p, static_cast<int>(fmt->kv_dtype),
+                                                          static_cast<uint8_t*>(d_workspace),
+                                                          static_cast<cudaStream_t>(stream));
+      if (e != cudaSuccess) return cuda_fail(e, "paged_prefill (expand) launch");
+      g_launches += 2;
+      return KS_OK;
+    }
     cudaError_t e = kvslab::launch_paged_prefill(p, static_cast<int>(fmt->kv_dtype),
                                                  static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "paged_prefill launch");
     ++g_launches;
     return KS_OK;
   });
+}
+
+ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
+                           void* d_out, float* d_lse, const int32_t* d_block_table,
+                           uint32_t bt_stride, const int32_t* d_cu_q, const int32_t* d_ctx_lens,
+                           uint32_t batch, uint32_t max_q_len, float sm_scale,
+                           const float* d_kv_scales, void* stream) {
+  return prefill_impl(pool, fmt, layer, d_q, d_out, d_lse, d_block_table, bt_stride, d_cu_q, d_ctx_lens,
+                      batch, max_q_len, sm_scale, d_kv_scales, nullptr, 0, stream);
+}
+
+ks_status ks_paged_prefill_ws(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
+                              void* d_out, float* d_lse, const int32_t* d_block_table,
+                              uint32_t bt_stride, const int32_t* d_cu_q, const int32_t* d_ctx_lens,
+                              uint32_t batch, uint32_t max_q_len, float sm_scale,
+                              const float* d_kv_scales, void* d_workspace, size_t workspace_bytes,
+                              void* stream) {
+  return prefill_impl(pool, fmt, layer, d_q, d_out, d_lse, d_block_table, bt_stride, d_cu_q, d_ctx_lens,
+                      batch, max_q_len, sm_scale, d_kv_scales, d_workspace, workspace_bytes, stream);
 }
 
 ks_status ks_set_decode_sm_share(ks_pool* pool, uint64_t key, uint32_t max_ctas) {

@@ -59,6 +59,7 @@ struct PrefillParams {
   uint32_t batch, max_q_len;
   float sm_scale_log2;
   const float* kv_scales;  // FP8 [2][H]
+  const float* exp_sz;     // expand scratch: K scale/zero per (seq, block, head) (EXP kernels)
   uint32_t nt;  // query rows per warp / 8 (1 or 2; 0 = default: 1, or 2 when G > 8)
   int use_tc;   // tcgen05 kernel (prefill_tc.cu) unless 0 (then mma.sync, prefill.cu)
   int debug;    // probes: bit0 no KV loads after the first two tiles, bit1 no softmax math
@@ -96,6 +97,10 @@ cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms
 size_t decode_partials_bytes(int num_sms, int G);
 cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStream_t stream);
 cudaError_t launch_paged_prefill_tc(const PrefillParams& p, int kv_dtype, cudaStream_t stream);  // tcgen05
+// quantised formats: expand the context once into fp16 scratch, then the FP16 kernel
+size_t prefill_expand_bytes(uint32_t H, uint32_t batch, uint32_t bt_stride);
+cudaError_t launch_paged_prefill_expand(const PrefillParams& p, int kv_dtype, uint8_t* scratch,
+                                        cudaStream_t stream);
 cudaError_t launch_kv_append(const AppendParams& p, int kv_dtype, cudaStream_t stream);
 cudaError_t launch_compact(const CompactParams& p, int num_sms, cudaStream_t stream);
 cudaError_t launch_table_scatter(int32_t* table, uint32_t row_stride, const int32_t* triples,

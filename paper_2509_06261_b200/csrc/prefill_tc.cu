@@ -132,23 +132,27 @@ constexpr uint32_t kLoadWarp0 = 9;
 // FP16 needs only Q gathers and bulk copies from its 3 loader warps (12 warps);
 // the dequantising formats get 7 (16 warps, <= 128 registers; with the O
 // rescale in 16-column TMEM chunks the spills are small): measured +6-14 %
-template <int FMT>
-constexpr uint32_t kLoadersOf = FMT == kFP16 ? 96u : 224u;
-template <int FMT>
-constexpr uint32_t kThreadsOf = kLoadWarp0 * 32 + kLoadersOf<FMT>;
+// EXP: INT8/INT4 over the expand scratch -- K as exact integers and V
+// dequantised, both fp16 operands as stored, so the loaders only issue bulk
+// copies like FP16 (plus the tile's K scale/zero arrays)
+template <int FMT, bool EXP = false>
+constexpr uint32_t kLoadersOf = (FMT == kFP16 || EXP) ? 96u : 224u;
+template <int FMT, bool EXP = false>
+constexpr uint32_t kThreadsOf = kLoadWarp0 * 32 + kLoadersOf<FMT, EXP>;
 constexpr uint32_t k2TmemCols = 512;
 // Shared memory per format: Q (2 x 32 KB) | fp16 K/V operand ring | P (2 x
 // 16 KB) | raw ring.  FP16 chunks are operands as stored (3 operand stages,
 // no raw ring); FP8/INT8/INT4 chunks and their per-token params land raw
 // (bulk copies, 2 stages) and the loader warps dequantise them into the
 // operand ring.
-template <int FMT>
+template <int FMT, bool EXP = false>
 struct TcCfg {
-  static constexpr uint32_t kStages = FMT == kFP16 ? 3 : 2;
+  static constexpr bool kOperands = FMT == kFP16 || EXP;  // chunks are fp16 operands as stored
+  static constexpr uint32_t kStages = kOperands ? 3 : 2;
   static constexpr uint32_t kRawStages = 3;  // raw blocks land two tiles ahead of the dequant
   static constexpr uint32_t kChunk = Geo<FMT>::kChunk, kParam = Geo<FMT>::kParam;
   static constexpr uint32_t kRawBlock = 2 * kChunk + 2 * kParam;  // K, V, K params, V params
-  static constexpr uint32_t kRawBytes = FMT == kFP16 ? 0 : (4 * kRawBlock + 127) / 128 * 128;
+  static constexpr uint32_t kRawBytes = kOperands ? 0 : (4 * kRawBlock + 127) / 128 * 128;
   static constexpr uint32_t kQo = 0, kKV = 2 * kQBytes, kP = kKV + kStages * 2 * kKVBytes;
   static constexpr uint32_t kRaw = kP + 2 * kPBytes;
   // INT8/INT4: K enters the MMA as exact integers; its per-token scale (and
@@ -251,10 +255,10 @@ __device__ __forceinline__ void dequant_int4_vpair(uint8_t* tile, uint32_t row_a
   }
 }
 
-template <int FMT>
-__global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const PrefillParams p) {
-  using Cfg = TcCfg<FMT>;
-  constexpr uint32_t kLoaders = kLoadersOf<FMT>;
+template <int FMT, bool EXP = false>
+__global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(const PrefillParams p) {
+  using Cfg = TcCfg<FMT, EXP>;
+  constexpr uint32_t kLoaders = kLoadersOf<FMT, EXP>;
   constexpr uint32_t kStages = Cfg::kStages, k2Q = Cfg::kQo, k2KV = Cfg::kKV, k2P = Cfg::kP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
   if (tid == 0) {
     mbar_init(&q_full, kLoaders);
     for (uint32_t i = 0; i < kStages; ++i) {
-      mbar_init(&kv_full[i], FMT == kFP16 ? 1u : kLoaders);
+      mbar_init(&kv_full[i], Cfg::kOperands ? 1u : kLoaders);
       mbar_init(&kv_empty[i], 1);
     }
     for (uint32_t i = 0; i < Cfg::kRawStages; ++i) {
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     fence_proxy_async();
     mbar_arrive(&q_full);
-    if constexpr (FMT != kFP16) {
+    if constexpr (!Cfg::kOperands) {
       // ---- raw blocks (bulk copies, one thread) -> dequantised operand tiles (96 threads) ----
       constexpr uint32_t kC = Cfg::kChunk, kPm = Cfg::kParam, kRB = Cfg::kRawBlock;
       const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
@@ -417,12 +421,13 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
         const uint32_t st = t % kStages;
         if (t >= kStages) mbar_wait(&kv_empty[st], ((t / kStages) - 1) & 1);
         const uint32_t kb = sbase + k2KV + st * 2 * kKVBytes;
-        mbar_expect_tx(&kv_full[st], 2 * kKVBytes);
+        mbar_expect_tx(&kv_full[st], 2 * kKVBytes + (EXP ? kTile * 8 : 0u));
 #pragma unroll
         for (uint32_t bi = 0; bi < 4; ++bi) {
           const uint32_t b = t * 4 + bi;
-          const uint8_t* blk = b < nblk ? p.pool + block_offset(p.geom, static_cast<uint32_t>(__ldg(bt + b))) + p.layer_off
-                                        : nullptr;
+          // null table: the expand scratch, block b of sequence s at s * bt_stride + b
+          const uint32_t gid = p.block_table ? static_cast<uint32_t>(__ldg(bt + b)) : s * p.bt_stride + b;
+          const uint8_t* blk = b < nblk ? p.pool + block_offset(p.geom, gid) + p.layer_off : nullptr;
 #pragma unroll
           for (uint32_t kv = 0; kv < 2; ++kv)
 #pragma unroll
@@ -432,6 +437,14 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
               bulk_g2s_u32(kb + kv * kKVBytes + half * (kTile * 128) + bi * (kTPB * 128), src, kTPB * 128,
                            &kv_full[st], pol);
             }
+          if constexpr (EXP) {  // the block's 16 K scales', then 16 zeros' (fp32, x sm_scale_log2)
+            const uint8_t* zs = b < nblk ? reinterpret_cast<const uint8_t*>(
+                                               p.exp_sz + ((static_cast<uint64_t>(s) * p.bt_stride + b) * p.H + h) * 32)
+                                         : g_zero_half;
+            const uint32_t szs = sbase + Cfg::kSZ + st * kTile * 8 + bi * kTPB * 4;
+            bulk_g2s_u32(szs, zs, kTPB * 4, &kv_full[st], pol);
+            bulk_g2s_u32(szs + kTile * 4, zs + kTPB * 4, kTPB * 4, &kv_full[st], pol);
+          }
         }
       }
     }
@@ -497,7 +510,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
     const uint32_t lanes = ((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + lanes + x * 2 * kTile, tO = tmem + lanes + 4 * kTile + x * kD;
     float sml2 = p.sm_scale_log2, oscale = 1.f;
-    if constexpr (FMT == kFP8) {  // static per-head scales: K into S, V into O
+    if constexpr (FMT == kFP8 || FMT == kFP16) {  // static per-head scales (FP8, also when expanded to fp16): K into S, V into O
       if (p.kv_scales) {
         sml2 *= p.kv_scales[h];
         oscale = p.kv_scales[p.H + h];
@@ -533,10 +546,23 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
           qsum = acc;
         }
         const float* sz = reinterpret_cast<const float*>(smem + Cfg::kSZ + (t % kStages) * kTile * 8);
+        const float2 qs2 = make_float2(qsum, qsum);
 #pragma unroll
-        for (int j = 0; j < static_cast<int>(kTile); ++j) {
-          if constexpr (FMT == kINT8) sc[j] *= sz[j];
-          else sc[j] = fmaf(sc[j], sz[j], sz[kTile + j] * qsum);
+        for (int j = 0; j < static_cast<int>(kTile); j += 4) {  // packed fp32x2, 16-byte scale loads
+          const float4 a = *reinterpret_cast<const float4*>(sz + j);
+          float2 lo = make_float2(sc[j], sc[j + 1]), hi = make_float2(sc[j + 2], sc[j + 3]);
+          if constexpr (FMT == kINT8) {
+            lo = fmul2(lo, make_float2(a.x, a.y));
+            hi = fmul2(hi, make_float2(a.z, a.w));
+          } else {
+            const float4 z = *reinterpret_cast<const float4*>(sz + kTile + j);
+            lo = ffma2(lo, make_float2(a.x, a.y), fmul2(make_float2(z.x, z.y), qs2));
+            hi = ffma2(hi, make_float2(a.z, a.w), fmul2(make_float2(z.z, z.w), qs2));
+          }
+          sc[j] = lo.x;
+          sc[j + 1] = lo.y;
+          sc[j + 2] = hi.x;
+          sc[j + 3] = hi.y;
         }
       }
       if (kbase + static_cast<int>(kTile) - 1 > rpos) {  // diagonal tile only: causal mask
@@ -625,22 +651,153 @@ __global__ void __launch_bounds__(kThreadsOf<FMT>, 1) prefill_tc2_kernel(const P
   if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(k2TmemCols));
 }
 
+// ------------------------------------------------------------ K4 expand
+// Quantised prefill, expand-once form: every context block of the batch is
+// dequantised ONCE per call into fp16 chunks laid out exactly like an FP16
+// slab block (half-major, 128B-swizzled, section 3) in the scratch block
+// s * bt_stride + b, and the FP16 tcgen05 kernel then attends over the
+// scratch (identity block table).  The direct quantised kernel instead
+// re-dequantises each KV tile in every query-tile CTA of the head (up to
+// max_q_len*G/256 times).  HBM-bound: one warp per (sequence, block, K|V,
+// head) chunk reads 1-2 KB and writes 4 KB.  FP8 converts exactly (its
+// per-head scales are applied in the FP16 kernel, as in the direct path);
+// INT8 / INT4 apply the token's scale (and zero) in one fp16 rounding.
+template <int FMT>
+__global__ void __launch_bounds__(256) expand_kernel(const PrefillParams p, uint8_t* __restrict__ scratch,
+                                                     float* __restrict__ sz_out) {
+  constexpr uint32_t kChunk = kTPB * kD * Fmt<FMT>::kBits / 8;
+  constexpr uint32_t kParam = FMT == kINT8 ? kTPB * 2 : (FMT == kINT4 ? kTPB * 4 : 0);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t twoH = 2 * p.H;
+  const uint64_t per_seq = static_cast<uint64_t>(p.bt_stride) * twoH;
+  const uint32_t s = static_cast<uint32_t>(gw / per_seq);
+  if (s >= p.batch) return;
+  const uint32_t rem = static_cast<uint32_t>(gw % per_seq), b = rem / twoH, c = rem % twoH;
+  const int ctx = p.ctx_lens[s];
+  if (ctx <= 0 || b * kTPB >= static_cast<uint32_t>(ctx)) return;
+  const uint32_t kv = c / p.H;
+  const uint8_t* blk = p.pool + block_offset(p.geom, static_cast<uint32_t>(
+                                    __ldg(p.block_table + static_cast<uint64_t>(s) * p.bt_stride + b))) + p.layer_off;
+  const uint8_t* chunk = blk + static_cast<uint64_t>(c) * kChunk;
+  const uint8_t* prm = blk + static_cast<uint64_t>(twoH) * kChunk + static_cast<uint64_t>(c) * kParam;
+  uint8_t* out = scratch + (static_cast<uint64_t>(s) * p.bt_stride + b) * (twoH * kTPB * kD * 2) +
+                 static_cast<uint64_t>(c) * (kTPB * kD * 2);
+  // INT8/INT4 K: exact integers (scale 1, zero 0); its per-token scale and
+  // zero go to sz_out as fp32 x sm_scale_log2, applied to S by the kernel
+  const bool exact = (FMT == kINT8 || FMT == kINT4) && kv == 0;
+  if ((FMT == kINT8 || FMT == kINT4) && kv == 0 && lane < 2 * kTPB) {
+    float v = 0.f;
+    if constexpr (FMT == kINT8) {
+      if (lane < kTPB) v = __half2float(*reinterpret_cast<const __half*>(prm + 2 * lane));
+    } else {
+      const __half2 sz = *reinterpret_cast<const __half2*>(prm + 4 * (lane & 15));
+      v = lane < kTPB ? __low2float(sz) : __high2float(sz);
+    }
+    sz_out[((static_cast<uint64_t>(s) * p.bt_stride + b) * p.H + c) * 32 + lane] = v * p.sm_scale_log2;
+  }
+#pragma unroll
+  for (uint32_t j = 0; j < 8; ++j) {
+    const uint32_t q = lane + 32 * j, t = q >> 4, gi = q & 15;  // token t, dims 8gi .. 8gi+7
+    uint32_t o[4];
+    if constexpr (FMT == kFP8 || FMT == kINT8) {
+      const uint2 w = *reinterpret_cast<const uint2*>(chunk + swz(t * 128 + 8 * gi));
+      if constexpr (FMT == kFP8) {
+        o[0] = e4m3x2_to_f16x2(static_cast<uint16_t>(w.x & 0xffff));
+        o[1] = e4m3x2_to_f16x2(static_cast<uint16_t>(w.x >> 16));
+        o[2] = e4m3x2_to_f16x2(static_cast<uint16_t>(w.y & 0xffff));
+        o[3] = e4m3x2_to_f16x2(static_cast<uint16_t>(w.y >> 16));
+      } else {
+        const uint32_t sc = exact ? 0x3C00u : *reinterpret_cast<const uint16_t*>(prm + 2 * t);
+        const uint32_t s2 = sc | (sc << 16);
+        const uint32_t x = w.x ^ 0x80808080u, y = w.y ^ 0x80808080u;  // exact 1152 + b, minus 1152, times s
+        o[0] = hmul2_u32(hsub2_u32(__byte_perm(x, 0x64646464u, 0x4140), 0x64806480u), s2);
+        o[1] = hmul2_u32(hsub2_u32(__byte_perm(x, 0x64646464u, 0x4342), 0x64806480u), s2);
+        o[2] = hmul2_u32(hsub2_u32(__byte_perm(y, 0x64646464u, 0x4140), 0x64806480u), s2);
+        o[3] = hmul2_u32(hsub2_u32(__byte_perm(y, 0x64646464u, 0x4342), 0x64806480u), s2);
+      }
+    } else {  // INT4: bytes 4gi .. 4gi+3 of token t (K rows / V token-pair lines)
+      uint32_t w;
+      if (kv == 0) {
+        w = *reinterpret_cast<const uint32_t*>(chunk + swz(t * 64 + 4 * gi));
+      } else {
+        const uint32_t t8 = t & 7, tp = (t8 & 1) | ((t8 >> 2) << 1), side = (t8 >> 1) & 1;
+        const uint32_t line = (2 * tp + (t >> 3)) * 128;
+        const uint32_t lo = *reinterpret_cast<const uint16_t*>(chunk + swz(line + 8 * gi + 2 * side));
+        const uint32_t hi = *reinterpret_cast<const uint16_t*>(chunk + swz(line + 8 * gi + 4 + 2 * side));
+        w = lo | (hi << 16);
+      }
+      const uint32_t sz = exact ? 0x3C00u : *reinterpret_cast<const uint32_t*>(prm + 4 * t);
+      const uint32_t sc = sz & 0xffffu, z = sz >> 16;
+      const uint32_t s2 = sc | (hmul2_u32(sc, 0x2C00u) << 16);  // (s, s/16): the high nibble enters as 16 n
+      const uint32_t z2 = z | (z << 16);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t y = __byte_perm(w, 0, k | (k << 8) | (k << 16) | (k << 24));
+        const uint32_t n = hsub2_u32(lop3_and_or(y, 0x00F0000Fu, 0x64006400u), 0x64006400u);
+        o[k] = hfma2_u32(n, s2, z2);
+      }
+    }
+    *reinterpret_cast<uint4*>(out + swz((gi >> 3) * (kTPB * 128) + t * 128 + (gi & 7) * 16)) =
+        make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 }  // namespace tc
 }  // namespace dev
 
-template <int FMT>
+template <int FMT, bool EXP = false>
 static cudaError_t launch_tc(const PrefillParams& p0, cudaStream_t stream) {
   using namespace dev::tc;
   PrefillParams p = p0;
   const uint32_t tpc = 2 * kRows / p.G;  // tokens per CTA (two 128-row query tiles)
   p.tiles = (p.max_q_len + tpc - 1) / tpc;
   if (p.tiles == 0) return cudaSuccess;
-  const size_t smem = TcCfg<FMT>::kSmem + 1024;  // + alignment slack
-  auto kern = prefill_tc2_kernel<FMT>;
+  const size_t smem = TcCfg<FMT, EXP>::kSmem + 1024;  // + alignment slack
+  auto kern = prefill_tc2_kernel<FMT, EXP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<dim3(p.batch * p.H, p.tiles), kThreadsOf<FMT>, smem, stream>>>(p);
+  kern<<<dim3(p.batch * p.H, p.tiles), kThreadsOf<FMT, EXP>, smem, stream>>>(p);
   return cudaGetLastError();
+}
+
+// scratch: fp16 blocks [batch * bt_stride][2H chunks], then the K scale/zero
+// arrays [batch * bt_stride][H][16 scales | 16 zeros] fp32
+size_t prefill_expand_bytes(uint32_t H, uint32_t batch, uint32_t bt_stride) {
+  return static_cast<size_t>(batch) * bt_stride * (2ull * H * dev::kTPB * dev::kD * 2 + H * 128ull);
+}
+
+cudaError_t launch_paged_prefill_expand(const PrefillParams& p, int kv_dtype, uint8_t* scratch,
+                                        cudaStream_t stream) {
+  using namespace dev;
+  const uint64_t warps = static_cast<uint64_t>(p.batch) * p.bt_stride * 2 * p.H;
+  const uint64_t blocks = (warps + 7) / 8;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffULL) return cudaErrorInvalidValue;
+  float* sz = reinterpret_cast<float*>(scratch + static_cast<size_t>(p.batch) * p.bt_stride *
+                                                       (2ull * p.H * kTPB * kD * 2));
+  const uint32_t nb = static_cast<uint32_t>(blocks);
+  switch (kv_dtype) {
+    case kFP8: tc::expand_kernel<kFP8><<<nb, 256, 0, stream>>>(p, scratch, sz); break;
+    case kINT8: tc::expand_kernel<kINT8><<<nb, 256, 0, stream>>>(p, scratch, sz); break;
+    case kINT4: tc::expand_kernel<kINT4><<<nb, 256, 0, stream>>>(p, scratch, sz); break;
+    default: return cudaErrorInvalidValue;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // the scratch as a one-layer FP16 pool: block g at g * key, identity table
+  PrefillParams q = p;
+  q.pool = scratch;
+  q.geom.key = 2ull * p.H * kTPB * kD * 2;
+  q.geom.slab_size = q.geom.key;
+  q.geom.bps = make_fastdiv(1);
+  q.layer_off = 0;
+  q.block_table = nullptr;
+  q.kv_scales = kv_dtype == kFP8 ? p.kv_scales : nullptr;
+  q.exp_sz = sz;
+  if (kv_dtype == kINT8) return launch_tc<kINT8, true>(q, stream);
+  if (kv_dtype == kINT4) return launch_tc<kINT4, true>(q, stream);
+  return launch_tc<kFP16>(q, stream);  // FP8: exact in fp16, per-head scales in the kernel
 }
 
 cudaError_t launch_paged_prefill_tc(const PrefillParams& p, int kv_dtype, cudaStream_t stream) {

@@ -251,18 +251,40 @@ def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
     return out
 
 
+_PF_WS: Dict[int, torch.Tensor] = {}
+
+
+def prefill_workspace(pool: SlabPool, fmt: KvFormat, batch: int,
+                      bt_stride: int) -> Optional[torch.Tensor]:
+    """Expand scratch for K4 on a quantised format (None for FP16): one
+    per-device buffer, grown on demand and reused by every call."""
+    f = fmt.to_c()
+    n = C.c_size_t()
+    check(L.lib.ks_paged_prefill_workspace_size(C.byref(f), batch, bt_stride, C.byref(n)))
+    if n.value == 0:
+        return None
+    buf = _PF_WS.get(pool.device)
+    if buf is None or buf.numel() < n.value:
+        buf = torch.empty(n.value, dtype=torch.uint8, device=f"cuda:{pool.device}")
+        _PF_WS[pool.device] = buf
+    return buf
+
+
 def paged_prefill(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
                   block_table: torch.Tensor, cu_q: torch.Tensor, ctx_lens: torch.Tensor,
                   max_q_len: int, out: Optional[torch.Tensor] = None,
                   lse: Optional[torch.Tensor] = None, sm_scale: Optional[float] = None,
-                  kv_scales: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                  kv_scales: Optional[torch.Tensor] = None, stream=None,
+                  workspace="auto") -> torch.Tensor:
     """K4: causal chunked-prefill attention over slab blocks.
 
     q: fp16 [T, Hq, d], the rows of sequence s being cu_q[s]..cu_q[s+1]-1
     (int32 [B+1], device) at positions ctx_lens[s]-n_s..ctx_lens[s]-1 (int32
     [B], device; the chunk's K/V already appended with kv_append).  Each query
     attends keys 0..its position.  max_q_len >= every n_s.  Returns out fp16
-    [T, Hq, d]."""
+    [T, Hq, d].  workspace: "auto" (the cached expand scratch of quantised
+    formats, see ks_paged_prefill_ws), a uint8 device tensor, or None (the
+    direct quantised kernel)."""
     assert q.dtype == torch.float16 and q.is_contiguous()
     assert block_table.dtype == torch.int32 and ctx_lens.dtype == torch.int32
     assert cu_q.dtype == torch.int32
@@ -270,10 +292,13 @@ def paged_prefill(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
         out = torch.empty_like(q)
     f = fmt.to_c()
     scale = 0.0 if sm_scale is None else float(sm_scale)
-    check(L.lib.ks_paged_prefill(pool.handle, C.byref(f), layer, _ptr(q), _ptr(out), _ptr(lse),
-                                 _ptr(block_table), block_table.stride(0), _ptr(cu_q),
-                                 _ptr(ctx_lens), ctx_lens.shape[0], int(max_q_len), scale,
-                                 _ptr(kv_scales), _stream(stream)))
+    if isinstance(workspace, str):
+        workspace = prefill_workspace(pool, fmt, ctx_lens.shape[0], block_table.stride(0))
+    ws_bytes = 0 if workspace is None else workspace.numel()
+    check(L.lib.ks_paged_prefill_ws(pool.handle, C.byref(f), layer, _ptr(q), _ptr(out), _ptr(lse),
+                                    _ptr(block_table), block_table.stride(0), _ptr(cu_q),
+                                    _ptr(ctx_lens), ctx_lens.shape[0], int(max_q_len), scale,
+                                    _ptr(kv_scales), _ptr(workspace), ws_bytes, _stream(stream)))
     return out
 
 

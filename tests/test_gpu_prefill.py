@@ -131,3 +131,41 @@ def test_prefill_tc_int4_gqa1_ragged():
     assert rel_err(o, r) <= 1e-2
     assert np.abs(lse - rl).max() <= 1e-3
 
+
+
+QUANT = [d for d in FORMATS if d != KvDtype.FP16]
+
+
+@pytest.mark.parametrize("expand", ["0", "1"], ids=["direct", "expand"])
+@pytest.mark.parametrize("dt", QUANT, ids=[d.name for d in QUANT])
+def test_prefill_quantised_direct_and_expand(dt, expand, monkeypatch):
+    """Both quantised K4 forms agree with the oracle: the direct tcgen05 kernel
+    (dequantising loaders) and expand-once (context -> fp16 scratch blocks, then
+    the FP16 kernel over an identity table), on layer 1 of a 2-layer key with
+    ragged, empty and whole-prompt chunks."""
+    monkeypatch.setenv("KVSLAB_PREFILL_EXPAND", expand)
+    _, _, _, _, o, lse, r, rl = run_prefill(dt, 2, 8, [(1500, 700), (129, 1), (64, 64), (40, 0), (333, 333)],
+                                            seed=51 + int(dt), layers=2, layer=1)
+    assert rel_err(o, r) <= TOL[dt]
+    assert np.abs(lse - rl).max() <= 1e-3
+
+
+def test_prefill_workspace_none_and_size():
+    """workspace=None runs the direct kernel; the size query is 0 for FP16 and
+    batch x bt_stride fp16 blocks (+ the K scale/zero arrays) otherwise."""
+    import ctypes as C
+    from paper_2509_06261_b200 import _lib as L
+    for dt, want in [(KvDtype.FP16, 0), (KvDtype.INT4, 3 * 10 * (2 * 4 * 16 * 128 * 2 + 4 * 128))]:
+        f = KvFormat(dt, 4, 16).to_c()
+        n = C.c_size_t()
+        assert L.lib.ks_paged_prefill_workspace_size(C.byref(f), 3, 10, C.byref(n)) == 0
+        assert n.value == want
+    fmt = KvFormat(KvDtype.INT8, 2, 8)
+    w = make_world(fmt, [600], seed=2)
+    append_gpu(w, fmt, 0)
+    q = torch.randn((600, 8, 128), dtype=torch.float16, device="cuda")
+    cu = dev(np.array([0, 600], np.int32))
+    a = kv.paged_prefill(w["pool"], fmt, 0, q, dev(w["table"]), cu, dev(w["ctx"]), 600, workspace=None)
+    b = kv.paged_prefill(w["pool"], fmt, 0, q, dev(w["table"]), cu, dev(w["ctx"]), 600)
+    torch.cuda.synchronize()
+    assert (a - b).abs().max().item() <= 2e-2 * b.abs().max().item()
