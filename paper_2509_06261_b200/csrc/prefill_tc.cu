@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
       // places it at rows 16*bi.. of the tile; 16 copies per 64-token tile
       const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
       const uint64_t pol = policy_evict_last();  // every query tile of the head re-reads them
+      pdl_wait();  // launched behind expand_kernel (PDL): its scratch blocks are complete
       for (uint32_t t = 0; t < ntiles; ++t) {
         const uint32_t st = t % kStages;
         if (t >= kStages) mbar_wait(&kv_empty[st], ((t / kStages) - 1) & 1);
@@ -667,6 +668,7 @@ __global__ void __launch_bounds__(256) expand_kernel(const PrefillParams p, uint
                                                      float* __restrict__ sz_out) {
   constexpr uint32_t kChunk = kTPB * kD * Fmt<FMT>::kBits / 8;
   constexpr uint32_t kParam = FMT == kINT8 ? kTPB * 2 : (FMT == kINT4 ? kTPB * 4 : 0);
+  pdl_launch_dependents();  // the attention kernel's prologue (TMEM, barriers, Q) overlaps this grid
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint32_t twoH = 2 * p.H;
@@ -679,61 +681,72 @@ __global__ void __launch_bounds__(256) expand_kernel(const PrefillParams p, uint
   const uint32_t kv = c / p.H;
   const uint8_t* blk = p.pool + block_offset(p.geom, static_cast<uint32_t>(
                                     __ldg(p.block_table + static_cast<uint64_t>(s) * p.bt_stride + b))) + p.layer_off;
-  const uint8_t* chunk = blk + static_cast<uint64_t>(c) * kChunk;
-  const uint8_t* prm = blk + static_cast<uint64_t>(twoH) * kChunk + static_cast<uint64_t>(c) * kParam;
+  const uint8_t* __restrict__ chunk = blk + static_cast<uint64_t>(c) * kChunk;
+  const uint8_t* __restrict__ prm = blk + static_cast<uint64_t>(twoH) * kChunk + static_cast<uint64_t>(c) * kParam;
   uint8_t* out = scratch + (static_cast<uint64_t>(s) * p.bt_stride + b) * (twoH * kTPB * kD * 2) +
                  static_cast<uint64_t>(c) * (kTPB * kD * 2);
   // INT8/INT4 K: exact integers (scale 1, zero 0); its per-token scale and
   // zero go to sz_out as fp32 x sm_scale_log2, applied to S by the kernel
   const bool exact = (FMT == kINT8 || FMT == kINT4) && kv == 0;
-  if ((FMT == kINT8 || FMT == kINT4) && kv == 0 && lane < 2 * kTPB) {
+  if ((FMT == kINT8 || FMT == kINT4) && kv == 0) {
     float v = 0.f;
     if constexpr (FMT == kINT8) {
-      if (lane < kTPB) v = __half2float(*reinterpret_cast<const __half*>(prm + 2 * lane));
+      if (lane < kTPB) v = __half2float(__ushort_as_half(__ldg(reinterpret_cast<const unsigned short*>(prm) + lane)));
     } else {
-      const __half2 sz = *reinterpret_cast<const __half2*>(prm + 4 * (lane & 15));
-      v = lane < kTPB ? __low2float(sz) : __high2float(sz);
+      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(prm) + (lane & 15));
+      v = __half2float(__ushort_as_half(static_cast<uint16_t>(lane < kTPB ? w & 0xffffu : w >> 16)));
     }
     sz_out[((static_cast<uint64_t>(s) * p.bt_stride + b) * p.H + c) * 32 + lane] = v * p.sm_scale_log2;
   }
+  // lane's outputs q = lane + 32 j: token t = q / 16 = 2j + lane / 16, dims 8 * (lane % 16) ..
+  const uint32_t gi = lane & 15;
+  // phase 1: every raw word and token parameter of the lane in flight at once
+  uint2 w8[8];
+  uint32_t pm[8];
 #pragma unroll
   for (uint32_t j = 0; j < 8; ++j) {
-    const uint32_t q = lane + 32 * j, t = q >> 4, gi = q & 15;  // token t, dims 8gi .. 8gi+7
-    uint32_t o[4];
+    const uint32_t t = 2 * j + (lane >> 4);
     if constexpr (FMT == kFP8 || FMT == kINT8) {
-      const uint2 w = *reinterpret_cast<const uint2*>(chunk + swz(t * 128 + 8 * gi));
-      if constexpr (FMT == kFP8) {
-        o[0] = e4m3x2_to_f16x2(static_cast<uint16_t>(w.x & 0xffff));
-        o[1] = e4m3x2_to_f16x2(static_cast<uint16_t>(w.x >> 16));
-        o[2] = e4m3x2_to_f16x2(static_cast<uint16_t>(w.y & 0xffff));
-        o[3] = e4m3x2_to_f16x2(static_cast<uint16_t>(w.y >> 16));
-      } else {
-        const uint32_t sc = exact ? 0x3C00u : *reinterpret_cast<const uint16_t*>(prm + 2 * t);
-        const uint32_t s2 = sc | (sc << 16);
-        const uint32_t x = w.x ^ 0x80808080u, y = w.y ^ 0x80808080u;  // exact 1152 + b, minus 1152, times s
-        o[0] = hmul2_u32(hsub2_u32(__byte_perm(x, 0x64646464u, 0x4140), 0x64806480u), s2);
-        o[1] = hmul2_u32(hsub2_u32(__byte_perm(x, 0x64646464u, 0x4342), 0x64806480u), s2);
-        o[2] = hmul2_u32(hsub2_u32(__byte_perm(y, 0x64646464u, 0x4140), 0x64806480u), s2);
-        o[3] = hmul2_u32(hsub2_u32(__byte_perm(y, 0x64646464u, 0x4342), 0x64806480u), s2);
-      }
-    } else {  // INT4: bytes 4gi .. 4gi+3 of token t (K rows / V token-pair lines)
-      uint32_t w;
-      if (kv == 0) {
-        w = *reinterpret_cast<const uint32_t*>(chunk + swz(t * 64 + 4 * gi));
-      } else {
-        const uint32_t t8 = t & 7, tp = (t8 & 1) | ((t8 >> 2) << 1), side = (t8 >> 1) & 1;
-        const uint32_t line = (2 * tp + (t >> 3)) * 128;
-        const uint32_t lo = *reinterpret_cast<const uint16_t*>(chunk + swz(line + 8 * gi + 2 * side));
-        const uint32_t hi = *reinterpret_cast<const uint16_t*>(chunk + swz(line + 8 * gi + 4 + 2 * side));
-        w = lo | (hi << 16);
-      }
-      const uint32_t sz = exact ? 0x3C00u : *reinterpret_cast<const uint32_t*>(prm + 4 * t);
+      w8[j] = __ldg(reinterpret_cast<const uint2*>(chunk + swz(t * 128 + 8 * gi)));
+    } else if (kv == 0) {
+      w8[j].x = __ldg(reinterpret_cast<const uint32_t*>(chunk + swz(t * 64 + 4 * gi)));
+    } else {  // V token-pair line: bytes 4gi .. 4gi+3 of token t
+      const uint32_t t8 = t & 7, tp = (t8 & 1) | ((t8 >> 2) << 1), side = (t8 >> 1) & 1;
+      const uint32_t line = (2 * tp + (t >> 3)) * 128;
+      const uint32_t lo = __ldg(reinterpret_cast<const unsigned short*>(chunk + swz(line + 8 * gi + 2 * side)));
+      const uint32_t hi = __ldg(reinterpret_cast<const unsigned short*>(chunk + swz(line + 8 * gi + 4 + 2 * side)));
+      w8[j].x = lo | (hi << 16);
+    }
+    if constexpr (FMT == kINT8) pm[j] = __ldg(reinterpret_cast<const unsigned short*>(prm) + t);
+    else if constexpr (FMT == kINT4) pm[j] = __ldg(reinterpret_cast<const uint32_t*>(prm) + t);
+    else pm[j] = 0;
+  }
+  // phase 2: convert and store 16-byte granules of the fp16 half-major chunk
+#pragma unroll
+  for (uint32_t j = 0; j < 8; ++j) {
+    const uint32_t t = 2 * j + (lane >> 4);
+    uint32_t o[4];
+    if constexpr (FMT == kFP8) {
+      o[0] = e4m3x2_to_f16x2(static_cast<uint16_t>(w8[j].x & 0xffff));
+      o[1] = e4m3x2_to_f16x2(static_cast<uint16_t>(w8[j].x >> 16));
+      o[2] = e4m3x2_to_f16x2(static_cast<uint16_t>(w8[j].y & 0xffff));
+      o[3] = e4m3x2_to_f16x2(static_cast<uint16_t>(w8[j].y >> 16));
+    } else if constexpr (FMT == kINT8) {
+      const uint32_t sc = exact ? 0x3C00u : pm[j];
+      const uint32_t s2 = sc | (sc << 16);
+      const uint32_t x = w8[j].x ^ 0x80808080u, y = w8[j].y ^ 0x80808080u;  // exact 1152 + b, minus 1152, times s
+      o[0] = hmul2_u32(hsub2_u32(__byte_perm(x, 0x64646464u, 0x4140), 0x64806480u), s2);
+      o[1] = hmul2_u32(hsub2_u32(__byte_perm(x, 0x64646464u, 0x4342), 0x64806480u), s2);
+      o[2] = hmul2_u32(hsub2_u32(__byte_perm(y, 0x64646464u, 0x4140), 0x64806480u), s2);
+      o[3] = hmul2_u32(hsub2_u32(__byte_perm(y, 0x64646464u, 0x4342), 0x64806480u), s2);
+    } else {
+      const uint32_t sz = exact ? 0x3C00u : pm[j];
       const uint32_t sc = sz & 0xffffu, z = sz >> 16;
       const uint32_t s2 = sc | (hmul2_u32(sc, 0x2C00u) << 16);  // (s, s/16): the high nibble enters as 16 n
       const uint32_t z2 = z | (z << 16);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint32_t y = __byte_perm(w, 0, k | (k << 8) | (k << 16) | (k << 24));
+        const uint32_t y = __byte_perm(w8[j].x, 0, k | (k << 8) | (k << 16) | (k << 24));
         const uint32_t n = hsub2_u32(lop3_and_or(y, 0x00F0000Fu, 0x64006400u), 0x64006400u);
         o[k] = hfma2_u32(n, s2, z2);
       }
@@ -747,7 +760,7 @@ __global__ void __launch_bounds__(256) expand_kernel(const PrefillParams p, uint
 }  // namespace dev
 
 template <int FMT, bool EXP = false>
-static cudaError_t launch_tc(const PrefillParams& p0, cudaStream_t stream) {
+static cudaError_t launch_tc(const PrefillParams& p0, cudaStream_t stream, bool pdl = false) {
   using namespace dev::tc;
   PrefillParams p = p0;
   const uint32_t tpc = 2 * kRows / p.G;  // tokens per CTA (two 128-row query tiles)
@@ -757,8 +770,17 @@ static cudaError_t launch_tc(const PrefillParams& p0, cudaStream_t stream) {
   auto kern = prefill_tc2_kernel<FMT, EXP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<dim3(p.batch * p.H, p.tiles), kThreadsOf<FMT, EXP>, smem, stream>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.batch * p.H, p.tiles);
+  cfg.blockDim = dim3(kThreadsOf<FMT, EXP>);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 // scratch: fp16 blocks [batch * bt_stride][2H chunks], then the K scale/zero
@@ -795,9 +817,9 @@ cudaError_t launch_paged_prefill_expand(const PrefillParams& p, int kv_dtype, ui
   q.block_table = nullptr;
   q.kv_scales = kv_dtype == kFP8 ? p.kv_scales : nullptr;
   q.exp_sz = sz;
-  if (kv_dtype == kINT8) return launch_tc<kINT8, true>(q, stream);
-  if (kv_dtype == kINT4) return launch_tc<kINT4, true>(q, stream);
-  return launch_tc<kFP16>(q, stream);  // FP8: exact in fp16, per-head scales in the kernel
+  if (kv_dtype == kINT8) return launch_tc<kINT8, true>(q, stream, true);
+  if (kv_dtype == kINT4) return launch_tc<kINT4, true>(q, stream, true);
+  return launch_tc<kFP16>(q, stream, true);  // FP8: exact in fp16, per-head scales in the kernel
 }
 
 cudaError_t launch_paged_prefill_tc(const PrefillParams& p, int kv_dtype, cudaStream_t stream) {
