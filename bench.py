@@ -58,6 +58,18 @@ LOCAL = int(os.environ.get("LOCAL_RANK", "0"))
 HQ, HKV, D = 32, 8, 128
 
 
+def cpu_model() -> str:
+    """The host CPU (CPU model and core count in every report)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -213,7 +225,8 @@ def run_reference():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16/fp8",
             "data": "synthetic", "config": config_dict(),
             "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": nthreads,
-                             "kind": "port", "sample": sample},
+                             "kind": "port", "sample": sample, "cpu_model": cpu_model(),
+                             "host_cpus": os.cpu_count()},
             "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -693,7 +706,8 @@ def run_ours():
     if not ARGS.no_cpu_baseline and WORLD == 1:  # rank 0 at N=1 only
         v, cores, sample = cpu_sample()
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "GB/s", "cores": cores,
-                                "kind": "port", "sample": sample}
+                                "kind": "port", "sample": sample, "cpu_model": cpu_model(),
+                                "host_cpus": os.cpu_count()}
     print(json.dumps(line), flush=True)
     if WORLD > 1:
         dist.barrier()
