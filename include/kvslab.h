@@ -281,8 +281,10 @@ ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t laye
  * (max_q_len x GQA group >= 1024), the context blocks are first expanded
  * once into fp16 scratch blocks (block b of sequence s at s*bt_stride + b,
  * laid out like FP16 slab blocks) and attended by the FP16 tcgen05 kernel.
- * d_workspace >= ks_paged_prefill_workspace_size bytes (0 for FP16); a null
- * workspace, FP16, or a short chunk runs exactly ks_paged_prefill. */
+ * ks_paged_prefill_workspace_size gives the bytes for the whole batch (0 for
+ * FP16); a smaller workspace holding at least one sequence's blocks
+ * (batch = 1) takes the sequences in groups.  A null or too-small workspace,
+ * FP16, or a short chunk runs exactly ks_paged_prefill. */
 ks_status ks_paged_prefill_workspace_size(const ks_kv_format* fmt, uint32_t batch, uint32_t bt_stride,
                                           size_t* bytes);
 ks_status ks_paged_prefill_ws(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,

@@ -851,14 +851,22 @@ static ks_status prefill_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t l
     if (const char* dbg = std::getenv("KVSLAB_PREFILL_DEBUG")) p.debug = std::atoi(dbg);
     const bool expand = d_workspace != nullptr && fmt->kv_dtype != KS_KV_FP16 && p.use_tc &&
                         prefill_expands(max_q_len, G);
-    if (expand) {
-      if (workspace_bytes < kvslab::prefill_expand_bytes(p.H, batch, bt_stride))
-        return fail(KS_INVALID_ARGUMENT, "prefill workspace too small");
-      cudaError_t e = kvslab::launch_paged_prefill_expand(p, static_cast<int>(fmt->kv_dtype),
-                                                          static_cast<uint8_t*>(d_workspace),
-                                                          static_cast<cudaStream_t>(stream));
-      if (e != cudaSuccess) return cuda_fail(e, "paged_prefill (expand) launch");
-      g_launches += 2;
+    const size_t per_seq = kvslab::prefill_expand_bytes(p.H, 1, bt_stride);
+    if (expand && per_seq > 0 && workspace_bytes >= per_seq) {
+      // a workspace smaller than the whole batch's takes the sequences in groups
+      const uint32_t group = static_cast<uint32_t>(std::min<size_t>(batch, workspace_bytes / per_seq));
+      for (uint32_t g0 = 0; g0 < batch; g0 += group) {
+        kvslab::PrefillParams q = p;
+        q.batch = std::min(group, batch - g0);
+        q.block_table = p.block_table + static_cast<size_t>(g0) * bt_stride;
+        q.cu_q = p.cu_q + g0;  // row offsets stay absolute
+        q.ctx_lens = p.ctx_lens + g0;
+        cudaError_t e = kvslab::launch_paged_prefill_expand(q, static_cast<int>(fmt->kv_dtype),
+                                                            static_cast<uint8_t*>(d_workspace),
+                                                            static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return cuda_fail(e, "paged_prefill (expand) launch");
+        g_launches += 2;
+      }
       return KS_OK;
     }
     cudaError_t e = kvslab::launch_paged_prefill(p, static_cast<int>(fmt->kv_dtype),

@@ -11,6 +11,7 @@ import ctypes as C
 import dataclasses
 import enum
 import math
+import os
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -254,18 +255,24 @@ def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
 _PF_WS: Dict[int, torch.Tensor] = {}
 
 
+PREFILL_WS_CAP = int(os.environ.get("KVSLAB_PREFILL_WS_CAP", 1 << 30))
+
+
 def prefill_workspace(pool: SlabPool, fmt: KvFormat, batch: int,
                       bt_stride: int) -> Optional[torch.Tensor]:
     """Expand scratch for K4 on a quantised format (None for FP16): one
-    per-device buffer, grown on demand and reused by every call."""
+    per-device buffer, grown on demand up to PREFILL_WS_CAP bytes (beyond,
+    the C side takes the batch in groups) and reused by every call."""
     f = fmt.to_c()
-    n = C.c_size_t()
+    n, one = C.c_size_t(), C.c_size_t()
     check(L.lib.ks_paged_prefill_workspace_size(C.byref(f), batch, bt_stride, C.byref(n)))
+    check(L.lib.ks_paged_prefill_workspace_size(C.byref(f), 1, bt_stride, C.byref(one)))
     if n.value == 0:
         return None
+    want = max(min(n.value, PREFILL_WS_CAP), one.value)
     buf = _PF_WS.get(pool.device)
-    if buf is None or buf.numel() < n.value:
-        buf = torch.empty(n.value, dtype=torch.uint8, device=f"cuda:{pool.device}")
+    if buf is None or buf.numel() < want:
+        buf = torch.empty(want, dtype=torch.uint8, device=f"cuda:{pool.device}")
         _PF_WS[pool.device] = buf
     return buf
 

@@ -169,3 +169,21 @@ def test_prefill_workspace_none_and_size():
     b = kv.paged_prefill(w["pool"], fmt, 0, q, dev(w["table"]), cu, dev(w["ctx"]), 600)
     torch.cuda.synchronize()
     assert (a - b).abs().max().item() <= 2e-2 * b.abs().max().item()
+
+
+def test_prefill_expand_in_sequence_groups():
+    """A workspace for one sequence takes the batch one sequence at a time."""
+    fmt = KvFormat(KvDtype.INT4, 2, 8)
+    cases = [(700, 300), (129, 129), (1000, 256), (40, 0)]
+    w, _, q, cu, o_full, _, r, _ = run_prefill(KvDtype.INT4, 2, 8, cases, seed=61)
+    import ctypes as C
+    from paper_2509_06261_b200 import _lib as L
+    one = C.c_size_t()
+    L.lib.ks_paged_prefill_workspace_size(C.byref(fmt.to_c()), 1, w["table"].shape[1], C.byref(one))
+    ws = torch.empty(one.value, dtype=torch.uint8, device="cuda")
+    o = kv.paged_prefill(w["pool"], fmt, 0, dev(q), dev(w["table"]), dev(cu), dev(w["ctx"]),
+                         max(n for _, n in cases), workspace=ws)
+    torch.cuda.synchronize()
+    o = o.cpu().numpy().astype(np.float64)
+    assert rel_err(o, r) <= 1e-2
+    assert np.abs(o - o_full).max() == 0.0  # the same kernels, sequence by sequence
