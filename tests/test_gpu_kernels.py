@@ -137,6 +137,36 @@ def test_fp8_conversion_special_values():
     assert (mine == want).all()
 
 
+@pytest.mark.parametrize("dt", [KvDtype.INT8, KvDtype.INT4], ids=["INT8", "INT4"])
+def test_integer_quantisation_rounding_ties(dt):
+    """K1 rounds x/s without a per-element division (reciprocal multiply, IEEE
+    division only near a tie): rows built so that x/s hits exact .5 ties, and
+    values one fp16 ulp either side of them, must give the oracle's bytes
+    (rint of the correctly rounded quotient, half to even)."""
+    fmt = KvFormat(dt, 1, 1, num_layers=1)
+    rows = []
+    for scale in (1.0, 0.25, 0.5, 2.0, 1.0 / 64):
+        top = (127.0 if dt == KvDtype.INT8 else 15.0) * scale
+        lo = -top if dt == KvDtype.INT8 else 0.0
+        base = np.arange(-130, 130, dtype=np.float64) + 0.5 if dt == KvDtype.INT8 else \
+            np.arange(0, 16, dtype=np.float64) + 0.5
+        ties = np.clip(base * scale, lo, top)
+        for nudge in (0, 1, -1):
+            t16 = ties.astype(np.float16)
+            if nudge:
+                t16 = np.nextafter(t16, np.float16(np.inf * nudge)).astype(np.float16)
+            r = np.resize(t16, 128).astype(np.float16)
+            r[0], r[1] = np.float16(top), np.float16(lo)  # pin the row's scale (and zero)
+            rows.append(r)
+    x = np.stack(rows).reshape(len(rows), 1, 128)
+    w = make_world(fmt, [len(rows)], seed=1, churn=False)
+    w["k"], w["v"] = x, (-x if dt == KvDtype.INT8 else x[::-1].copy())
+    append_gpu(w, fmt, 0)
+    img, _ = oracle_image(w, fmt, 0)
+    got = kv.kv_tensor(w["pool"]).cpu().numpy()
+    assert (got == img).all()
+
+
 def rel_err(o, r):
     o = o.reshape(-1, o.shape[-1]).astype(np.float64)
     r = r.reshape(-1, r.shape[-1])
