@@ -800,6 +800,16 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   // at every shape measured, B=1..64, ctx 2k..32k).  The quantised formats are
   // consumer-limited at large batch and keep every SM.
   if (FMT == kFP16 && p.max_ctas == 0) grid = std::max(1, grid * 3 / 4);
+  // FP8 is consumer-limited at large batch and keeps every SM, but its short
+  // launches gain from the same hand-over (B16 ctx 2k 19.0 -> 18.3 us, B4 ctx
+  // 8k 19.2 -> 18.4; INT8/INT4, whose consumers are slower, lose 5-15 % at
+  // B8-16 and keep the full grid).  The launch itself must be smaller -- an
+  // in-kernel early exit of the extra CTAs measured no gain: every launched
+  // CTA has to be resident before the next launch may start.  The host only
+  // knows the table bound batch x bt_stride (an overestimate keeps the full grid).
+  if (FMT == kFP8 && p.max_ctas == 0 &&
+      static_cast<uint64_t>(p.batch) * p.bt_stride * (p.H / hg) < static_cast<uint64_t>(grid) * 24)
+    grid = std::max(1, grid * 3 / 4);
   if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
