@@ -484,9 +484,9 @@ def run_ours():
     # budgets for their persistent K2 grids; the split is autotuned once.
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
 
-    def time_split(share):
-        kv.set_decode_sm_share(pool, models[0].key, share)
-        kv.set_decode_sm_share(pool, models[1].key, n_sm - share)
+    def time_split(split):
+        kv.set_decode_sm_share(pool, models[0].key, split[0])
+        kv.set_decode_sm_share(pool, models[1].key, split[1])
         gg = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
 
@@ -514,14 +514,18 @@ def run_ours():
         torch.cuda.synchronize()
         return a.elapsed_time(b)
 
-    cands = sorted({max(1, min(n_sm - 1, round(n_sm * f))) for f in (0.42, 0.47, 0.52, 0.57, 0.62)})
+    # candidates: the FP16 model's fraction of the budget, and a budget of all
+    # SMs or slightly fewer (free SMs let each model's next launch start while
+    # the current one drains; see decode.cu launch_fmt)
+    cands = sorted({(s16, tot - s16) for tot in (n_sm, round(n_sm * 0.92), round(n_sm * 0.84))
+                    for s16 in [max(1, min(tot - 1, round(tot * f))) for f in (0.42, 0.47, 0.52, 0.57, 0.62)]})
     if ARGS.profile:  # no autotune launches under the profiler
-        times = {n_sm // 2: 0.0}
+        times = {(n_sm // 2, n_sm - n_sm // 2): 0.0}
     else:
         times = {c: time_split(c) for c in cands}
-    share16 = min(times, key=times.get)
+    share16, share8 = min(times, key=times.get)
     kv.set_decode_sm_share(pool, models[0].key, 0 if ARGS.profile else share16)
-    kv.set_decode_sm_share(pool, models[1].key, 0 if ARGS.profile else n_sm - share16)
+    kv.set_decode_sm_share(pool, models[1].key, 0 if ARGS.profile else share8)
 
     if ARGS.profile:
         host_step()
@@ -688,8 +692,8 @@ def run_ours():
         "dtype": "fp16/fp8_e4m3 KV, fp32 accumulate", "data": "synthetic",
         "config": config_dict(),
         "decode_tok_s": round(tok_s, 1),
-        "sm_share": {"fp16_model": share16, "fp8_model": n_sm - share16,
-                     "autotune_ms": {str(k): round(v, 3) for k, v in times.items()}},
+        "sm_share": {"fp16_model": share16, "fp8_model": share8,
+                     "autotune_ms": {f"{k[0]}+{k[1]}": round(v, 3) for k, v in times.items()}},
         "frac_of_peak": round(value / WORLD / peak, 4),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
