@@ -74,3 +74,17 @@ def test_cpp_dropin_compiles_and_passes(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "all checks passed" in out.stdout
+
+
+def test_workspace_size_queries_need_no_gpu():
+    """The K2 / K4 workspace size queries are pure host arithmetic: K4's is 0
+    for FP16 and batch x bt_stride fp16 blocks (+ K scale/zero arrays) for the
+    quantised formats; a one-sequence query sizes the smallest usable buffer."""
+    from paper_2509_06261_b200.kv import KvDtype, KvFormat
+    n = C.c_size_t()
+    for dt in KvDtype:
+        f = KvFormat(dt, 8, 32).to_c()
+        assert L.lib.ks_paged_prefill_workspace_size(C.byref(f), 4, 100, C.byref(n)) == 0
+        block = 0 if dt == KvDtype.FP16 else 2 * 8 * 16 * 128 * 2 + 8 * 128
+        assert n.value == 4 * 100 * block
+    assert L.lib.ks_paged_prefill_workspace_size(None, 1, 1, C.byref(n)) != 0
