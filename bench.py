@@ -44,12 +44,32 @@ P.add_argument("--steps", type=int, default=20)
 P.add_argument("--warmup", type=int, default=5)
 P.add_argument("--impl", default="ours", choices=["ours", "reference"])
 P.add_argument("--layers", type=int, default=32)
-P.add_argument("--batch", type=int, default=16)
-P.add_argument("--ctx", type=int, default=2048)
+P.add_argument("--workload", default="c2", choices=["c2", "c3"],
+               help="c2 (default, the BASELINE metric): FP16 + FP8 co-located, B16 ctx 2k; "
+                    "c3: FP16 + INT4 co-located, B8 ctx 8k")
+P.add_argument("--batch", type=int, default=None)
+P.add_argument("--ctx", type=int, default=None)
 P.add_argument("--no-cpu-baseline", action="store_true")
 P.add_argument("--no-sweep", action="store_true", help="skip the per-format K2 / K4 sweep")
 P.add_argument("--profile", action="store_true", help="one eager step, no timing (for ncu)")
 ARGS = P.parse_args()
+# BASELINE.json configs[1] / configs[2]: the two co-located models' KV dtypes
+# (oracle/kernel codes: 0 FP16, 1 FP8-E4M3, 3 INT4), batch per model, context
+WORKLOADS = {
+    "c2": dict(dts=(0, 1), batch=16, ctx=2048,
+               text="c2: two co-located Llama-3-8B-shape models (32L, 32q/8kv, d128) on one slab pool, "
+                    "FP16 KV + FP8-E4M3 KV (64 B/layer params)"),
+    "c3": dict(dts=(0, 3), batch=8, ctx=8192,
+               text="c3: two co-located Llama-3-8B-shape models (32L, 32q/8kv, d128) on one slab pool, "
+                    "FP16 KV + INT4 KV (QoQ-style fp16 scale/zero per token and head), ctx 8k"),
+}
+WL = WORKLOADS[ARGS.workload]
+if ARGS.batch is None:
+    ARGS.batch = WL["batch"]
+if ARGS.ctx is None:
+    ARGS.ctx = WL["ctx"]
+DT_NAMES = {0: "fp16", 1: "fp8_e4m3", 2: "int8", 3: "int4"}
+NAMES = [DT_NAMES[d] for d in WL["dts"]]
 
 RANK = int(os.environ.get("RANK", "0"))
 WORLD = int(os.environ.get("WORLD_SIZE", "1"))
@@ -79,12 +99,11 @@ def peaks():
 
 
 def config_dict(extra=None):
-    d = {"workload": "c2: two co-located Llama-3-8B-shape models (32L, 32q/8kv, d128) on one "
-                     "slab pool, FP16 KV + FP8-E4M3 KV (64 B/layer params)",
+    d = {"workload": WL["text"],
          "layers": ARGS.layers, "batch_per_model": ARGS.batch, "ctx": ARGS.ctx,
-         "tokens_per_block": 16, "kv_dtypes": ["fp16", "fp8_e4m3"],
+         "tokens_per_block": 16, "kv_dtypes": NAMES,
          "parallelism": f"placement x{WORLD} (independent pool per GPU, no collective)",
-         "l2": "inputs larger than L2: each step streams ~6.4 GB of KV per GPU"}
+         "l2": "inputs larger than L2: each step streams several GB of KV per GPU (126 MB L2)"}
     if extra:
         d.update(extra)
     return d
@@ -93,6 +112,13 @@ def config_dict(extra=None):
 # ======================================================================
 # CPU legs (oracle port / reference allocator) -- bounded samples
 # ======================================================================
+def oracle_qparams(dt):
+    """Natural per-layer quant-param bytes of a block (precision.cpp:91-99 +
+    DESIGN.md section 3): FP8 fp32 scale per (K|V, head), INT8 fp16 scale and
+    INT4 fp16 (scale, zero) per (K|V, head, token)."""
+    return {0: 0, 1: 2 * HKV * 4, 2: 2 * HKV * 16 * 2, 3: 2 * HKV * 16 * 4}[dt]
+
+
 def cpu_sample(seconds_target=10.0, nthreads=None):
     """fp64 OpenMP oracle decode over one layer of both models (all 16 seqs),
     repeated until ~seconds_target.  Returns (GB/s, cores, sample text)."""
@@ -102,8 +128,8 @@ def cpu_sample(seconds_target=10.0, nthreads=None):
     rng = np.random.default_rng(0)
     B, ctx = ARGS.batch, ARGS.ctx
     res = []
-    for dt, qp in ((0, 0), (1, 2 * HKV * 4)):
-        f = oracle.fmt(dt, HKV, HQ, D, 1, 16, qp)
+    for dt in WL["dts"]:
+        f = oracle.fmt(dt, HKV, HQ, D, 1, 16, oracle_qparams(dt))
         key = oracle.lib.orc_fmt_key(C.byref(f))
         nb = (ctx + 15) // 16
         img = np.zeros(B * nb * key, dtype=np.uint8)
@@ -144,12 +170,12 @@ def run_reference():
     nthreads = oracle.NPROC
     rng = np.random.default_rng(1)
     models = []
-    k16 = 16 * HKV * D * 2 * 2
-    k8 = 16 * HKV * D * 2 + 2 * HKV * 4
-    slab = math.lcm(k16, k8)
+    fl = [oracle.fmt(dt, HKV, HQ, D, 1, 16, oracle_qparams(dt)) for dt in WL["dts"]]
+    kl = [int(oracle.lib.orc_fmt_key(C.byref(f))) for f in fl]
+    slab = math.lcm(*kl)
     nb_max = (ctx + ARGS.steps + ARGS.warmup + 16) // 16 + 1
-    nslabs = (B * nb_max * k16) // slab + (B * nb_max * k8) // slab + 4
-    keys = (C.c_uint64 * 2)(k16, k8)
+    nslabs = sum((B * nb_max * k) // slab for k in kl) + 4
+    keys = (C.c_uint64 * 2)(*kl)
     if ref is not None:
         rp = ref.ref_pool_create(nslabs * slab, slab, keys, 2, 1)
         kind = "reference"
@@ -159,7 +185,7 @@ def run_reference():
             assert ref.ref_try_alloc(rp, key, out) == 0
             return int(out[2])
     else:
-        op = oracle.OraclePool(nslabs * slab, slab, [k16, k8])
+        op = oracle.OraclePool(nslabs * slab, slab, kl)
         kind = "port"
 
         def alloc(key):
@@ -167,8 +193,7 @@ def run_reference():
             assert st == 0
             return h[2]
     img = np.zeros(nslabs * slab, dtype=np.uint8)
-    for dt, key in ((0, k16), (1, k8)):
-        f = oracle.fmt(dt, HKV, HQ, D, 1, 16, 0 if dt == 0 else 2 * HKV * 4)
+    for dt, f, key in zip(WL["dts"], fl, kl):
         models.append(dict(f=f, key=key, table=np.zeros((B, nb_max), np.int32),
                            nblk=[0] * B, cached=[0] * B,
                            sc=np.ones(2 * HKV, np.float32) if dt == 1 else None))
@@ -222,7 +247,7 @@ def run_reference():
     line = {"metric": "slab paged-decode attention HBM GB/s", "value": round(gbs, 3),
             "unit": "GB/s", "impl": "reference", "n_gpus": WORLD, "steps": ARGS.steps,
             "warmup": ARGS.warmup, "ms_per_step": round(dt / ARGS.steps * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16/fp8",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "/".join(NAMES),
             "data": "synthetic", "config": config_dict(),
             "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": nthreads,
                              "kind": "port", "sample": sample, "cpu_model": cpu_model(),
@@ -389,7 +414,7 @@ def run_ours():
             dist.init_process_group("gloo")
     dev = torch.device(f"cuda:{local}")
     L, B, ctx0 = ARGS.layers, ARGS.batch, ARGS.ctx
-    fmts = [KvFormat(KvDtype.FP16, HKV, HQ, D, L), KvFormat(KvDtype.FP8_E4M3, HKV, HQ, D, L)]
+    fmts = [KvFormat(KvDtype(dt), HKV, HQ, D, L) for dt in WL["dts"]]
     keys = [f.key for f in fmts]
     slab = math.lcm(*keys)
     total_steps = ARGS.warmup + ARGS.steps + 2
@@ -654,7 +679,7 @@ def run_ours():
         per_launch_ms = a.elapsed_time(b) / (reps * L)
         cl = [int(x) for x in ctxd.cpu().tolist()]
         by = m.fmt.decode_bytes(cl)
-        rl[["fp16", "fp8"][mi]] = (by, per_launch_ms)
+        rl[NAMES[mi]] = (by, per_launch_ms)
 
     # every KV precision's K2 alone (outside the timed region, rank 0 / N=1
     # only): the bench shape and a large batch, 8-layer graphs
@@ -678,7 +703,8 @@ def run_ours():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             prof = json.load(f)
-        traffic = prof.get("decode_fp16", {}).get("dram_bytes_per_launch")
+        if ARGS.workload == "c2":  # the committed capture is of the c2 FP16 launch
+            traffic = prof.get("decode_fp16", {}).get("dram_bytes_per_launch")
     except Exception:
         pass
     kernels = {k: {"bytes": v[0], "us": round(v[1] * 1e3, 2),
@@ -689,15 +715,15 @@ def run_ours():
         "value": round(value, 2), "unit": "GB/s", "n_gpus": WORLD, "steps": ARGS.steps,
         "warmup": ARGS.warmup, "ms_per_step": round(ms / ARGS.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp16/fp8_e4m3 KV, fp32 accumulate", "data": "synthetic",
+        "dtype": "/".join(NAMES) + " KV, fp32 accumulate", "data": "synthetic",
         "config": config_dict(),
         "decode_tok_s": round(tok_s, 1),
-        "sm_share": {"fp16_model": share16, "fp8_model": share8,
+        "sm_share": {f"{NAMES[0]}_model": share16, f"{NAMES[1]}_model": share8,
                      "autotune_ms": {f"{k[0]}+{k[1]}": round(v, 3) for k, v in times.items()}},
         "frac_of_peak": round(value / WORLD / peak, 4),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "paged_decode_kernel<FP16> (one layer, 16 seqs x ctx~2070, 8 kv heads)",
+                     "kernel": f"paged_decode_kernel<FP16> (one layer, {B} seqs x ctx~{ARGS.ctx + ARGS.warmup + ARGS.steps}, 8 kv heads)",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "frac_of_8TBps": round(achieved / 8000.0, 4)},
         "kernels": kernels,
