@@ -281,12 +281,16 @@ ks_status ks_paged_prefill(ks_pool* pool, const ks_kv_format* fmt, uint32_t laye
  * (max_q_len x GQA group >= 1024), the context blocks are first expanded
  * once into fp16 scratch blocks (block b of sequence s at s*bt_stride + b,
  * laid out like FP16 slab blocks) and attended by the FP16 tcgen05 kernel.
- * ks_paged_prefill_workspace_size gives the bytes for the whole batch (0 for
- * FP16); a smaller workspace holding at least one sequence's blocks
- * (batch = 1) takes the sequences in groups.  A null or too-small workspace,
- * FP16, or a short chunk runs exactly ks_paged_prefill. */
+ * The workspace also enables split-KV: when batch x kv heads x query tiles
+ * would leave SMs idle (short chunks over long contexts), each query tile's
+ * KV range is cut over up to 8 CTAs whose fp32 partials are merged by a
+ * second kernel.  ks_paged_prefill_workspace_size gives the bytes for both
+ * (partials first, then the expand scratch; FP16 needs only the partials); a
+ * smaller workspace drops the split first, then takes the expand in
+ * sequence groups (at least one sequence's blocks, batch = 1).  A null
+ * workspace runs exactly ks_paged_prefill. */
 ks_status ks_paged_prefill_workspace_size(const ks_kv_format* fmt, uint32_t batch, uint32_t bt_stride,
-                                          size_t* bytes);
+                                          uint32_t max_q_len, size_t* bytes);
 ks_status ks_paged_prefill_ws(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
                               void* d_out, float* d_lse, const int32_t* d_block_table,
                               uint32_t bt_stride, const int32_t* d_cu_q, const int32_t* d_ctx_lens,

@@ -121,7 +121,7 @@ _SIGS = {
                                     u32, C.c_float, P, P, C.c_size_t, P]),
     "ks_paged_prefill": (st, [P, C.POINTER(ks_kv_format), u32, P, P, P, P, u32, P, P, u32, u32,
                               C.c_float, P, P]),
-    "ks_paged_prefill_workspace_size": (st, [C.POINTER(ks_kv_format), u32, u32, C.POINTER(C.c_size_t)]),
+    "ks_paged_prefill_workspace_size": (st, [C.POINTER(ks_kv_format), u32, u32, u32, C.POINTER(C.c_size_t)]),
     "ks_paged_prefill_ws": (st, [P, C.POINTER(ks_kv_format), u32, P, P, P, P, u32, P, P, u32, u32,
                                  C.c_float, P, P, C.c_size_t, P]),
     "ks_set_decode_sm_share": (st, [P, u64, u32]),

@@ -792,10 +792,16 @@ ks_status ks_paged_decode_append(ks_pool* pool, const ks_kv_format* fmt, uint32_
                      workspace_bytes, stream);
 }
 
+static int prefill_sms(const ks_pool* pool) { return pool && pool->num_sms > 0 ? pool->num_sms : 148; }
+
+// Workspace layout: [split-KV partials][expand scratch]
 ks_status ks_paged_prefill_workspace_size(const ks_kv_format* fmt, uint32_t batch, uint32_t bt_stride,
-                                          size_t* bytes) {
+                                          uint32_t max_q_len, size_t* bytes) {
   if (!fmt || !bytes) return fail(KS_INVALID_ARGUMENT, "null argument");
-  *bytes = fmt->kv_dtype == KS_KV_FP16 ? 0 : kvslab::prefill_expand_bytes(fmt->num_kv_heads, batch, bt_stride);
+  const uint32_t H = fmt->num_kv_heads, G = H ? fmt->num_q_heads / H : 0;
+  const uint32_t splits = G ? kvslab::prefill_kv_splits(batch, H, G, max_q_len, prefill_sms(nullptr)) : 1;
+  *bytes = (G ? kvslab::prefill_partial_bytes(batch, H, G, max_q_len, splits) : 0) +
+           (fmt->kv_dtype == KS_KV_FP16 ? 0 : kvslab::prefill_expand_bytes(H, batch, bt_stride));
   return KS_OK;
 }
 
@@ -849,7 +855,22 @@ static ks_status prefill_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t l
     p.use_tc = 2;
     if (const char* tc = std::getenv("KVSLAB_PREFILL_TC")) p.use_tc = std::atoi(tc);
     if (const char* dbg = std::getenv("KVSLAB_PREFILL_DEBUG")) p.debug = std::atoi(dbg);
-    const bool expand = d_workspace != nullptr && fmt->kv_dtype != KS_KV_FP16 && p.use_tc &&
+    // split-KV when the query tiles alone would leave SMs idle (tcgen05 path),
+    // its partials at the start of the workspace
+    uint8_t* ws = static_cast<uint8_t*>(d_workspace);
+    if (ws && p.use_tc) {
+      const uint32_t splits = kvslab::prefill_kv_splits(batch, p.H, G, max_q_len, prefill_sms(pool));
+      const size_t pb = kvslab::prefill_partial_bytes(batch, p.H, G, max_q_len, splits);
+      if (splits > 1 && (std::getenv("KVSLAB_PREFILL_SPLIT") == nullptr ||
+                         std::atoi(std::getenv("KVSLAB_PREFILL_SPLIT")) != 0) &&
+          workspace_bytes >= pb) {
+        p.kv_splits = splits;
+        p.part = reinterpret_cast<float*>(ws);
+        ws += pb;
+        workspace_bytes -= pb;
+      }
+    }
+    const bool expand = ws != nullptr && fmt->kv_dtype != KS_KV_FP16 && p.use_tc &&
                         prefill_expands(max_q_len, G);
     const size_t per_seq = kvslab::prefill_expand_bytes(p.H, 1, bt_stride);
     if (expand && per_seq > 0 && workspace_bytes >= per_seq) {
@@ -861,8 +882,7 @@ static ks_status prefill_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t l
         q.block_table = p.block_table + static_cast<size_t>(g0) * bt_stride;
         q.cu_q = p.cu_q + g0;  // row offsets stay absolute
         q.ctx_lens = p.ctx_lens + g0;
-        cudaError_t e = kvslab::launch_paged_prefill_expand(q, static_cast<int>(fmt->kv_dtype),
-                                                            static_cast<uint8_t*>(d_workspace),
+        cudaError_t e = kvslab::launch_paged_prefill_expand(q, static_cast<int>(fmt->kv_dtype), ws,
                                                             static_cast<cudaStream_t>(stream));
         if (e != cudaSuccess) return cuda_fail(e, "paged_prefill (expand) launch");
         g_launches += 2;

@@ -60,6 +60,8 @@ struct PrefillParams {
   float sm_scale_log2;
   const float* kv_scales;  // FP8 [2][H]
   const float* exp_sz;     // expand scratch: K scale/zero per (seq, block, head) (EXP kernels)
+  uint32_t kv_splits;      // split-KV CTAs per query tile (tcgen05 kernel; needs part)
+  float* part;             // split-KV partials [row][split][kD + 4]
   uint32_t nt;  // query rows per warp / 8 (1 or 2; 0 = default: 1, or 2 when G > 8)
   int use_tc;   // tcgen05 kernel (prefill_tc.cu) unless 0 (then mma.sync, prefill.cu)
   int debug;    // probes: bit0 no KV loads after the first two tiles, bit1 no softmax math
@@ -99,6 +101,9 @@ cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStrea
 cudaError_t launch_paged_prefill_tc(const PrefillParams& p, int kv_dtype, cudaStream_t stream);  // tcgen05
 // quantised formats: expand the context once into fp16 scratch, then the FP16 kernel
 size_t prefill_expand_bytes(uint32_t H, uint32_t batch, uint32_t bt_stride);
+// split-KV: CTAs per query tile that fill the SMs (1 = none), and the partials' bytes
+uint32_t prefill_kv_splits(uint32_t batch, uint32_t H, uint32_t G, uint32_t max_q_len, int num_sms);
+size_t prefill_partial_bytes(uint32_t batch, uint32_t H, uint32_t G, uint32_t max_q_len, uint32_t splits);
 cudaError_t launch_paged_prefill_expand(const PrefillParams& p, int kv_dtype, uint8_t* scratch,
                                         cudaStream_t stream);
 cudaError_t launch_kv_append(const AppendParams& p, int kv_dtype, cudaStream_t stream);

@@ -294,7 +294,7 @@ cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStrea
   // measured faster (INT4, 16 x chunk 16 at ctx 4k: 142 vs 186 us; at chunk
   // 32 the tcgen05 kernel wins, 187 vs 295)
   const bool small = kv_dtype != kFP16 && p.max_q_len * p.G <= 64;
-  if (p.use_tc && !small) return launch_paged_prefill_tc(p, kv_dtype, stream);
+  if (p.use_tc == 1 || (p.use_tc && !small)) return launch_paged_prefill_tc(p, kv_dtype, stream);  // 1: forced
   const bool two = p.nt == 2 || p.G > 8;
   switch (kv_dtype) {
     case kFP16: return two ? launch_prefill_fmt<kFP16, 2>(p, stream) : launch_prefill_fmt<kFP16, 1>(p, stream);

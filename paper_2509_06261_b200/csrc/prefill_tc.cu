@@ -140,6 +140,7 @@ constexpr uint32_t kLoadersOf = (FMT == kFP16 || EXP) ? 96u : 224u;
 template <int FMT, bool EXP = false>
 constexpr uint32_t kThreadsOf = kLoadWarp0 * 32 + kLoadersOf<FMT, EXP>;
 constexpr uint32_t k2TmemCols = 512;
+constexpr uint32_t kPartStride = kD + 4;  // split-KV partial per row: acc[128], m, l (+pad)
 // Shared memory per format: Q (2 x 32 KB) | fp16 K/V operand ring | P (2 x
 // 16 KB) | raw ring.  FP16 chunks are operands as stored (3 operand stages,
 // no raw ring); FP8/INT8/INT4 chunks and their per-token params land raw
@@ -265,7 +266,7 @@ __device__ __forceinline__ void dequant_int4_vpair(uint8_t* tile, uint32_t row_a
   }
 }
 
-template <int FMT, bool EXP = false>
+template <int FMT, bool EXP = false, bool SPLIT = false>
 __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(const PrefillParams p) {
   using Cfg = TcCfg<FMT, EXP>;
   constexpr uint32_t kLoaders = kLoadersOf<FMT, EXP>;
@@ -287,6 +288,13 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
   const int tok_end = min(nq, tok0 + static_cast<int>(TPC));
   const int pos_last = pos0 + tok_end - 1;
   const uint32_t ntiles = static_cast<uint32_t>(pos_last) / kTile + 1;
+  // split-KV (gridDim.z > 1; short chunks over long contexts would leave SMs
+  // idle): CTA z of the query tile attends KV tiles [t0, t0 + niter) and
+  // leaves an fp32 partial (acc, m, l) per row for prefill_merge_kernel
+  // (a separate instantiation: the unsplit kernel keeps its exact code)
+  const uint32_t nsplit = SPLIT ? gridDim.z : 1u, z = SPLIT ? blockIdx.z : 0u;
+  const uint32_t t0 = SPLIT ? z * ntiles / nsplit : 0u;
+  const uint32_t niter = SPLIT ? (z + 1) * ntiles / nsplit - t0 : ntiles;
   const uint32_t nblk = (static_cast<uint32_t>(ctx) + kTPB - 1) / kTPB;
   const uint32_t Hq = p.H * G;
   const uint32_t sbase = smem_u32(smem);
@@ -346,7 +354,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
         mbar_expect_tx(&raw_full[rs], 4 * kRB);
         const uint64_t pol = policy_evict_last();
         for (uint32_t bi = 0; bi < 4; ++bi) {
-          const uint32_t b = t * 4 + bi;
+          const uint32_t b = (t0 + t) * 4 + bi;
           const uint32_t dst = raw0 + rs * Cfg::kRawBytes + bi * kRB;
           if (b < nblk) {
             const uint8_t* blk = p.pool + block_offset(p.geom, static_cast<uint32_t>(__ldg(bt + b))) + p.layer_off;
@@ -366,11 +374,11 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
         }
       };
       if (lt == 0)
-        for (uint32_t t = 0; t + 1 < RS && t < ntiles; ++t) issue_raw(t);
+        for (uint32_t t = 0; t + 1 < RS && t < niter; ++t) issue_raw(t);
       constexpr uint32_t kRowB = kD * Fmt<FMT>::kBits / 8;     // raw bytes per token row
       constexpr uint32_t kGran = 2 * 4 * kC / 16;               // raw 16-byte granules per tile
-      for (uint32_t t = 0; t < ntiles; ++t) {
-        if (lt == 0 && t + RS - 1 < ntiles) issue_raw(t + RS - 1);
+      for (uint32_t t = 0; t < niter; ++t) {
+        if (lt == 0 && t + RS - 1 < niter) issue_raw(t + RS - 1);
         const uint32_t rs = t % RS, st = t % kStages;
         mbar_wait(&raw_full[rs], (t / RS) & 1);
         if (t >= kStages) mbar_wait(&kv_empty[st], ((t / kStages) - 1) & 1);
@@ -428,14 +436,14 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
       const int32_t* bt = p.block_table + static_cast<uint64_t>(s) * p.bt_stride;
       const uint64_t pol = policy_evict_last();  // every query tile of the head re-reads them
       pdl_wait();  // launched behind expand_kernel (PDL): its scratch blocks are complete
-      for (uint32_t t = 0; t < ntiles; ++t) {
+      for (uint32_t t = 0; t < niter; ++t) {
         const uint32_t st = t % kStages;
         if (t >= kStages) mbar_wait(&kv_empty[st], ((t / kStages) - 1) & 1);
         const uint32_t kb = sbase + k2KV + st * 2 * kKVBytes;
         mbar_expect_tx(&kv_full[st], 2 * kKVBytes + (EXP ? kTile * 8 : 0u));
 #pragma unroll
         for (uint32_t bi = 0; bi < 4; ++bi) {
-          const uint32_t b = t * 4 + bi;
+          const uint32_t b = (t0 + t) * 4 + bi;
           // null table: the expand scratch, block b of sequence s at s * bt_stride + b
           const uint32_t gid = p.block_table ? static_cast<uint32_t>(__ldg(bt + b)) : s * p.bt_stride + b;
           const uint8_t* blk = b < nblk ? p.pool + block_offset(p.geom, gid) + p.layer_off : nullptr;
@@ -487,13 +495,15 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
       // softmax of t is still reading S(t):  S_A(t+1), PV_A(t), S_B(t+1), PV_B(t)
       mbar_wait(&q_full, 0);
       tc_fence_after();
-      mbar_wait(&kv_full[0], 0);
-      tc_fence_after();
-      mma_s(0, 0, 0);
-      mma_s(1, 0, 0);
-      for (uint32_t t = 0; t < ntiles; ++t) {
+      if (niter > 0) {
+        mbar_wait(&kv_full[0], 0);
+        tc_fence_after();
+        mma_s(0, 0, 0);
+        mma_s(1, 0, 0);
+      }
+      for (uint32_t t = 0; t < niter; ++t) {
         const uint32_t st = t % kStages, nst = (t + 1) % kStages;
-        const bool more = t + 1 < ntiles;
+        const bool more = t + 1 < niter;
         if (more) {  // both tiles' next S first: neither waits on the other's softmax
           mbar_wait(&kv_full[nst], ((t + 1) / kStages) & 1);
           tc_fence_after();
@@ -508,7 +518,8 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
         mma_pv(1, st, t == 0);
         umma_commit(&kv_empty[st]);
       }
-      umma_commit(&o_final);
+      if (niter > 0) umma_commit(&o_final);
+      else mbar_arrive(&o_final);  // empty split: nothing to wait for
     }
     __syncwarp();
   } else {
@@ -529,7 +540,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
     }
     uint8_t* prow = smem + k2P + x * kPBytes;
     float m = -INFINITY, l = 0.f, qsum = 0.f;
-    for (uint32_t t = 0; t < ntiles; ++t) {
+    for (uint32_t t = 0; t < niter; ++t) {
       mbar_wait(&s_full[x], t & 1);
       tc_fence_after();
       float sc[kTile];
@@ -538,7 +549,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
 #pragma unroll
         for (int j = 0; j < static_cast<int>(kTile); ++j) sc[j] = 0.f;
       }
-      const int kbase = static_cast<int>(t * kTile);
+      const int kbase = static_cast<int>((t0 + t) * kTile);
       if constexpr (FMT == kINT8 || FMT == kINT4) {
         if (t == 0 && FMT == kINT4) {  // sum of this row's (exact fp16) query, for the zero term
           const uint8_t* qr = smem + k2Q + x * kQBytes;
@@ -635,6 +646,23 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
     }
     mbar_wait(&o_final, 0);
     tc_fence_after();
+    if (SPLIT) {  // fp32 partial: acc * oscale (unnormalised), m (log2 domain), l
+      const uint64_t prow_g = static_cast<uint64_t>(q0 + (rvalid ? rtok : 0)) * Hq + h * G + rr % G;
+      float* part = p.part + (prow_g * nsplit + z) * kPartStride;
+#pragma unroll
+      for (uint32_t c = 0; c < kD; c += 32) {
+        float o[32];
+        if (niter > 0) tmem_ld32(tO + c, o);
+        if (rvalid) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(part + c + j) =
+                niter > 0 ? make_float4(o[j] * oscale, o[j + 1] * oscale, o[j + 2] * oscale, o[j + 3] * oscale)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      if (rvalid) *reinterpret_cast<float2*>(part + kD) = make_float2(niter > 0 ? m : -INFINITY, l);
+    } else {
     const float inv = oscale / l;
     __half* orow = p.out + (static_cast<uint64_t>(q0 + (rvalid ? rtok : 0)) * Hq + h * G + rr % G) * kD;
 #pragma unroll
@@ -655,10 +683,43 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
     }
     if (rvalid && p.lse)
       p.lse[static_cast<uint64_t>(q0 + rtok) * Hq + h * G + rr % G] = (m + __log2f(l)) * 0.69314718055994531f;
+    }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(k2TmemCols));
+}
+
+// ------------------------------------------------------------ split-KV merge
+// One warp per (query token, query head) row: O = sum_z 2^(m_z - M) acc_z /
+// sum_z 2^(m_z - M) l_z over the row's nsplit partials (4 dims per lane).
+__global__ void __launch_bounds__(256) prefill_merge_kernel(const PrefillParams p, uint32_t rows, uint32_t nsplit) {
+  // rows of this launch's sequences: [cu_q[0], cu_q[batch]) x Hq (a sequence group may start past 0)
+  const uint32_t Hq = p.H * p.G, r0 = static_cast<uint32_t>(p.cu_q[0]) * Hq;
+  const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const uint32_t row = r0 + i;
+  if (i >= rows || row >= static_cast<uint32_t>(p.cu_q[p.batch]) * Hq) return;
+  const float* part = p.part + static_cast<uint64_t>(row) * nsplit * kPartStride;
+  float M = -INFINITY;
+  for (uint32_t z = 0; z < nsplit; ++z) M = fmaxf(M, part[z * kPartStride + kD]);
+  float L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t z = 0; z < nsplit; ++z) {
+    const float* pz = part + z * kPartStride;
+    const float mz = pz[kD];
+    if (mz == -INFINITY) continue;  // empty split
+    const float w = ex2(mz - M);
+    L += w * pz[kD + 1];
+    const float4 a = *reinterpret_cast<const float4*>(pz + 4 * lane);
+    acc.x += w * a.x;
+    acc.y += w * a.y;
+    acc.z += w * a.z;
+    acc.w += w * a.w;
+  }
+  const float inv = 1.f / L;
+  __half* orow = p.out + static_cast<uint64_t>(row) * kD + 4 * lane;
+  *reinterpret_cast<uint2*>(orow) = make_uint2(pack_h2(acc.x * inv, acc.y * inv), pack_h2(acc.z * inv, acc.w * inv));
+  if (lane == 0 && p.lse) p.lse[row] = (M + __log2f(L)) * 0.69314718055994531f;
 }
 
 // ------------------------------------------------------------ K4 expand
@@ -776,11 +837,12 @@ static cudaError_t launch_tc(const PrefillParams& p0, cudaStream_t stream, bool 
   p.tiles = (p.max_q_len + tpc - 1) / tpc;
   if (p.tiles == 0) return cudaSuccess;
   const size_t smem = TcCfg<FMT, EXP>::kSmem + 1024;  // + alignment slack
-  auto kern = prefill_tc2_kernel<FMT, EXP>;
+  const uint32_t nsplit = p.kv_splits > 1 ? p.kv_splits : 1;
+  auto kern = nsplit > 1 ? prefill_tc2_kernel<FMT, EXP, true> : prefill_tc2_kernel<FMT, EXP, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.batch * p.H, p.tiles);
+  cfg.gridDim = dim3(p.batch * p.H, p.tiles, nsplit);
   cfg.blockDim = dim3(kThreadsOf<FMT, EXP>);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -789,11 +851,28 @@ static cudaError_t launch_tc(const PrefillParams& p0, cudaStream_t stream, bool 
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, p);
+  cudaError_t e2 = cudaLaunchKernelEx(&cfg, kern, p);
+  if (e2 != cudaSuccess || nsplit == 1) return e2;
+  const uint64_t rows = static_cast<uint64_t>(p.batch) * p.max_q_len * p.H * p.G;  // bound; exact count on device
+  prefill_merge_kernel<<<static_cast<uint32_t>((rows + 7) / 8), 256, 0, stream>>>(p, static_cast<uint32_t>(rows),
+                                                                                  nsplit);
+  return cudaGetLastError();
 }
 
 // scratch: fp16 blocks [batch * bt_stride][2H chunks], then the K scale/zero
 // arrays [batch * bt_stride][H][16 scales | 16 zeros] fp32
+uint32_t prefill_kv_splits(uint32_t batch, uint32_t H, uint32_t G, uint32_t max_q_len, int num_sms) {
+  const uint32_t tpc = 2 * dev::tc::kRows / G;
+  const uint64_t ctas = static_cast<uint64_t>(batch) * H * ((max_q_len + tpc - 1) / tpc);
+  if (ctas == 0) return 1;
+  const uint64_t s = static_cast<uint64_t>(num_sms) / ctas;
+  return static_cast<uint32_t>(s < 2 ? 1 : (s > 8 ? 8 : s));
+}
+
+size_t prefill_partial_bytes(uint32_t batch, uint32_t H, uint32_t G, uint32_t max_q_len, uint32_t splits) {
+  return splits > 1 ? static_cast<size_t>(batch) * max_q_len * H * G * splits * dev::tc::kPartStride * 4 : 0;
+}
+
 size_t prefill_expand_bytes(uint32_t H, uint32_t batch, uint32_t bt_stride) {
   return static_cast<size_t>(batch) * bt_stride * (2ull * H * dev::kTPB * dev::kD * 2 + H * 128ull);
 }

@@ -258,15 +258,16 @@ _PF_WS: Dict[int, torch.Tensor] = {}
 PREFILL_WS_CAP = int(os.environ.get("KVSLAB_PREFILL_WS_CAP", 1 << 30))
 
 
-def prefill_workspace(pool: SlabPool, fmt: KvFormat, batch: int,
-                      bt_stride: int) -> Optional[torch.Tensor]:
-    """Expand scratch for K4 on a quantised format (None for FP16): one
-    per-device buffer, grown on demand up to PREFILL_WS_CAP bytes (beyond,
-    the C side takes the batch in groups) and reused by every call."""
+def prefill_workspace(pool: SlabPool, fmt: KvFormat, batch: int, bt_stride: int,
+                      max_q_len: int) -> Optional[torch.Tensor]:
+    """K4 workspace (split-KV partials + the quantised formats' expand
+    scratch; None when neither applies): one per-device buffer, grown on
+    demand up to PREFILL_WS_CAP bytes (beyond, the C side drops the split and
+    takes the expand in sequence groups) and reused by every call."""
     f = fmt.to_c()
     n, one = C.c_size_t(), C.c_size_t()
-    check(L.lib.ks_paged_prefill_workspace_size(C.byref(f), batch, bt_stride, C.byref(n)))
-    check(L.lib.ks_paged_prefill_workspace_size(C.byref(f), 1, bt_stride, C.byref(one)))
+    check(L.lib.ks_paged_prefill_workspace_size(C.byref(f), batch, bt_stride, max_q_len, C.byref(n)))
+    check(L.lib.ks_paged_prefill_workspace_size(C.byref(f), 1, bt_stride, max_q_len, C.byref(one)))
     if n.value == 0:
         return None
     want = max(min(n.value, PREFILL_WS_CAP), one.value)
@@ -300,7 +301,7 @@ def paged_prefill(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
     f = fmt.to_c()
     scale = 0.0 if sm_scale is None else float(sm_scale)
     if isinstance(workspace, str):
-        workspace = prefill_workspace(pool, fmt, ctx_lens.shape[0], block_table.stride(0))
+        workspace = prefill_workspace(pool, fmt, ctx_lens.shape[0], block_table.stride(0), int(max_q_len))
     ws_bytes = 0 if workspace is None else workspace.numel()
     check(L.lib.ks_paged_prefill_ws(pool.handle, C.byref(f), layer, _ptr(q), _ptr(out), _ptr(lse),
                                     _ptr(block_table), block_table.stride(0), _ptr(cu_q),

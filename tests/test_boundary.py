@@ -77,14 +77,18 @@ def test_cpp_dropin_compiles_and_passes(tmp_path):
 
 
 def test_workspace_size_queries_need_no_gpu():
-    """The K2 / K4 workspace size queries are pure host arithmetic: K4's is 0
-    for FP16 and batch x bt_stride fp16 blocks (+ K scale/zero arrays) for the
-    quantised formats; a one-sequence query sizes the smallest usable buffer."""
+    """The K4 workspace size query is pure host arithmetic: split-KV partials
+    when the chunk's query tiles alone would leave SMs idle, plus batch x
+    bt_stride fp16 blocks (+ K scale/zero arrays) for the quantised formats."""
     from paper_2509_06261_b200.kv import KvDtype, KvFormat
     n = C.c_size_t()
     for dt in KvDtype:
         f = KvFormat(dt, 8, 32).to_c()
-        assert L.lib.ks_paged_prefill_workspace_size(C.byref(f), 4, 100, C.byref(n)) == 0
+        # long chunks fill the GPU: no split-KV partials, only the expand scratch
+        assert L.lib.ks_paged_prefill_workspace_size(C.byref(f), 4, 100, 4096, C.byref(n)) == 0
         block = 0 if dt == KvDtype.FP16 else 2 * 8 * 16 * 128 * 2 + 8 * 128
         assert n.value == 4 * 100 * block
-    assert L.lib.ks_paged_prefill_workspace_size(None, 1, 1, C.byref(n)) != 0
+        # one 64-token chunk: 8 CTAs -> 8 KV splits of fp32 partials (rows x 132 floats)
+        assert L.lib.ks_paged_prefill_workspace_size(C.byref(f), 1, 100, 64, C.byref(n)) == 0
+        assert n.value == 64 * 32 * 8 * 132 * 4 + 100 * block
+    assert L.lib.ks_paged_prefill_workspace_size(None, 1, 1, 1, C.byref(n)) != 0

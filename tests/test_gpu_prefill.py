@@ -158,7 +158,7 @@ def test_prefill_workspace_none_and_size():
     for dt, want in [(KvDtype.FP16, 0), (KvDtype.INT4, 3 * 10 * (2 * 4 * 16 * 128 * 2 + 4 * 128))]:
         f = KvFormat(dt, 4, 16).to_c()
         n = C.c_size_t()
-        assert L.lib.ks_paged_prefill_workspace_size(C.byref(f), 3, 10, C.byref(n)) == 0
+        assert L.lib.ks_paged_prefill_workspace_size(C.byref(f), 3, 10, 8192, C.byref(n)) == 0
         assert n.value == want
     fmt = KvFormat(KvDtype.INT8, 2, 8)
     w = make_world(fmt, [600], seed=2)
@@ -171,15 +171,17 @@ def test_prefill_workspace_none_and_size():
     assert (a - b).abs().max().item() <= 2e-2 * b.abs().max().item()
 
 
-def test_prefill_expand_in_sequence_groups():
+def test_prefill_expand_in_sequence_groups(monkeypatch):
     """A workspace for one sequence takes the batch one sequence at a time."""
+    monkeypatch.setenv("KVSLAB_PREFILL_SPLIT", "0")  # same kernels both ways -> identical bits
     fmt = KvFormat(KvDtype.INT4, 2, 8)
     cases = [(700, 300), (129, 129), (1000, 256), (40, 0)]
     w, _, q, cu, o_full, _, r, _ = run_prefill(KvDtype.INT4, 2, 8, cases, seed=61)
     import ctypes as C
     from paper_2509_06261_b200 import _lib as L
     one = C.c_size_t()
-    L.lib.ks_paged_prefill_workspace_size(C.byref(fmt.to_c()), 1, w["table"].shape[1], C.byref(one))
+    # one sequence's expand scratch only (max_q_len large enough that no split is sized)
+    L.lib.ks_paged_prefill_workspace_size(C.byref(fmt.to_c()), 1, w["table"].shape[1], 1 << 16, C.byref(one))
     ws = torch.empty(one.value, dtype=torch.uint8, device="cuda")
     o = kv.paged_prefill(w["pool"], fmt, 0, dev(q), dev(w["table"]), dev(cu), dev(w["ctx"]),
                          max(n for _, n in cases), workspace=ws)
@@ -187,3 +189,28 @@ def test_prefill_expand_in_sequence_groups():
     o = o.cpu().numpy().astype(np.float64)
     assert rel_err(o, r) <= 1e-2
     assert np.abs(o - o_full).max() == 0.0  # the same kernels, sequence by sequence
+
+
+SPLIT_CASES = [
+    # (dtype, H, Hq, cases): short chunks over long contexts -> few query tiles, split-KV
+    (KvDtype.FP16, 2, 8, [(3000, 16), (1500, 64), (64, 64), (900, 0)]),
+    (KvDtype.FP8_E4M3, 2, 8, [(2500, 40), (333, 33)]),
+    (KvDtype.INT8, 2, 16, [(2000, 64), (17, 17)]),
+    (KvDtype.INT4, 2, 8, [(4100, 64), (700, 1)]),
+    (KvDtype.INT4, 1, 4, [(1000, 300)]),
+]
+
+
+@pytest.mark.parametrize("split", ["0", "1"], ids=["nosplit", "split"])
+@pytest.mark.parametrize("dt,H,Hq,cases", SPLIT_CASES,
+                         ids=[f"{c[0].name}-{c[1]}x{c[2]}-{len(c[3])}" for c in SPLIT_CASES])
+def test_prefill_split_kv(dt, H, Hq, cases, split, monkeypatch):
+    """Split-KV K4 (query tiles x KV ranges over up to 8 CTAs, fp32 partials,
+    merge kernel) and the unsplit kernel both match the oracle, including
+    empty splits (ranges past a short context) and the direct / expand forms
+    of the quantised formats."""
+    monkeypatch.setenv("KVSLAB_PREFILL_SPLIT", split)
+    monkeypatch.setenv("KVSLAB_PREFILL_TC", "1")  # tcgen05 even for the shortest chunks
+    _, _, _, _, o, lse, r, rl = run_prefill(dt, H, Hq, cases, seed=71 + int(dt) + H)
+    assert rel_err(o, r) <= TOL[dt]
+    assert np.abs(lse - rl).max() <= 1e-3
