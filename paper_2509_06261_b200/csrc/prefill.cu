@@ -294,7 +294,10 @@ cudaError_t launch_paged_prefill(const PrefillParams& p, int kv_dtype, cudaStrea
   // measured faster (INT4, 16 x chunk 16 at ctx 4k: 142 vs 186 us; at chunk
   // 32 the tcgen05 kernel wins, 187 vs 295)
   const bool small = kv_dtype != kFP16 && p.max_q_len * p.G <= 64;
-  if (p.use_tc == 1 || (p.use_tc && !small)) return launch_paged_prefill_tc(p, kv_dtype, stream);  // 1: forced
+  // ... unless the tcgen05 kernel splits the KV range (few CTAs: small batch,
+  // long context), which wins there (B=1 INT4 chunk 16 at ctx 8k: 258 -> 61 us)
+  if (p.use_tc == 1 || (p.use_tc && (!small || p.kv_splits > 1)))  // 1: forced
+    return launch_paged_prefill_tc(p, kv_dtype, stream);
   const bool two = p.nt == 2 || p.G > 8;
   switch (kv_dtype) {
     case kFP16: return two ? launch_prefill_fmt<kFP16, 2>(p, stream) : launch_prefill_fmt<kFP16, 1>(p, stream);
