@@ -389,6 +389,22 @@ def format_sweep(peak):
                                            "us": round(ms * 1e3, 1), "tflops": round(tf, 1),
                                            "frac": round(tf / tpeak, 4), "bound": "tensor"}
         del pool
+        # chunked prefill's steady state: a 64-token chunk per sequence at the end
+        # of an 8k context (4 seqs; split-KV)
+        Bc, cc, nc = 4, 8192, 64
+        fmt, pool, m = world(dt, Bc, cc)
+        ctx = torch.full((Bc,), cc, dtype=torch.int32, device="cuda")
+        cu = torch.arange(0, (Bc + 1) * nc, nc, dtype=torch.int32, device="cuda")
+        q = torch.randn(Bc * nc, HQ, D, dtype=torch.float16, device="cuda")
+        out = torch.empty_like(q)
+        ms = timed(lambda: kv.paged_prefill(pool, fmt, 0, q, m.table, cu, ctx, nc, out=out,
+                                            kv_scales=sc), 10)
+        flops = 4.0 * D * HQ * Bc * sum(cc - nc + i + 1 for i in range(nc))
+        tf = flops / (ms / 1e3) / 1e12
+        res["prefill"][dt.name.lower() + "_chunk64_ctx8k"] = {
+            "workload": f"{Bc} seqs, 64-token chunk at ctx 8192, causal", "us": round(ms * 1e3, 1),
+            "tflops": round(tf, 1), "frac": round(tf / tpeak, 4), "bound": "tensor"}
+        del pool
     res["decode"]["note"] = ("K2 alone per KV precision: 8-layer graph of fused append+decode, "
                              "per-launch average, algorithmic bytes / measured HBM copy peak")
     return res
