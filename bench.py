@@ -733,7 +733,7 @@ def run_ours():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "/".join(NAMES) + " KV, fp32 accumulate", "data": "synthetic",
         "config": config_dict(),
-        "decode_tok_s": round(tok_s, 1),
+        "decode_tok_s": round(tok_s, 1), "decode_tok_s_per_gpu": round(tok_s / WORLD, 1),
         "sm_share": {f"{NAMES[0]}_model": share16, f"{NAMES[1]}_model": share8,
                      "autotune_ms": {f"{k[0]}+{k[1]}": round(v, 3) for k, v in times.items()}},
         "frac_of_peak": round(value / WORLD / peak, 4),
