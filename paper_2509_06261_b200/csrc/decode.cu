@@ -361,20 +361,30 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
   __syncthreads();
   const uint32_t total = pre[p.batch];
 
-  // CTA 0 writes empty outputs for sequences with no context (after the
-  // predecessor finished).
-  if (blockIdx.x == 0) {
+  // Sequences with no context (empty slots of a fixed-size batch) get zero
+  // outputs and -inf LSE, after the predecessor finished: spread over the
+  // grid, one sequence per CTA at a time, 16-byte stores by the whole CTA
+  // (one thread per sequence writing 2-byte zeros made a 64-slot batch with
+  // 8 live sequences 10x slower).
+  {
     bool waited = false;
-    for (uint32_t s = threadIdx.x; s < p.batch; s += blockDim.x) {
-      if (pre[s + 1] != pre[s]) continue;
+    const uint32_t hq = p.H * p.G;
+    const bool v16 = (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
+    for (uint32_t s = blockIdx.x; s < p.batch; s += gridDim.x) {
+      if (pre[s + 1] != pre[s]) continue;  // uniform: pre is in shared memory
       if (!waited) {
         pdl_wait();
         waited = true;
       }
-      for (uint32_t i = 0; i < p.H * p.G * kD; ++i)
-        p.out[(static_cast<uint64_t>(s) * p.H * p.G) * kD + i] = __float2half(0.f);
+      __half* orow = p.out + static_cast<uint64_t>(s) * hq * kD;
+      if (v16) {
+        for (uint32_t i = threadIdx.x; i < hq * kD / 8; i += blockDim.x)
+          reinterpret_cast<uint4*>(orow)[i] = make_uint4(0u, 0u, 0u, 0u);
+      } else {
+        for (uint32_t i = threadIdx.x; i < hq * kD; i += blockDim.x) orow[i] = __float2half(0.f);
+      }
       if (p.lse)
-        for (uint32_t i = 0; i < p.H * p.G; ++i) p.lse[s * p.H * p.G + i] = -INFINITY;
+        for (uint32_t i = threadIdx.x; i < hq; i += blockDim.x) p.lse[static_cast<uint64_t>(s) * hq + i] = -INFINITY;
     }
   }
 
