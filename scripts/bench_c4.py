@@ -32,6 +32,7 @@ MAXB = int(os.environ.get("MAXB", 64))
 PHASES = int(os.environ.get("PHASES", 8))
 STEPS = int(os.environ.get("STEPS", 8))
 WAVE = [MAXB, 8]  # square wave of the batch per model
+TRIGGER = float(os.environ.get("TRIGGER", 0.25))  # stranded free-block fraction
 
 fmts = [KvFormat(dt, HKV, HQ, D, L) for dt in (KvDtype.FP16, KvDtype.FP8_E4M3, KvDtype.INT8, KvDtype.INT4)]
 keys = [f.key for f in fmts]
@@ -121,7 +122,7 @@ for ph in range(PHASES):
     st = pool.snapshot_stats()
     stranded = st.free_block_bytes / max(1, st.allocated_bytes + st.free_block_bytes)
     trace.append(round(stranded, 3))
-    if stranded > 0.25:
+    if stranded > TRIGGER or (ph == PHASES - 1 and compactions == 0):  # at least one K3 pass measured
         a, b = ev(), ev()
         a.record()
         for m in models:
@@ -169,7 +170,8 @@ print(json.dumps({
     "frac_of_peak": round(gbs / peak, 4), "decode_tok_s": round(tokens / (dec_ms / 1e3), 1),
     "config": {"workload": "c4: four co-located Llama-3-8B-shape models (32L, 32q/8kv, d128), FP16 / FP8-E4M3 / "
                            "INT8 / INT4 KV, one relaxed 8 MiB-slab pool, batch square wave "
-                           f"{WAVE} per model, {PHASES} phases x {STEPS} decode steps, compaction at > 25 % stranded",
+                           f"{WAVE} per model, {PHASES} phases x {STEPS} decode steps, compaction at > {TRIGGER:.0%} stranded "
+                           "(and once in the last phase if it never triggered)",
                "data": "synthetic, KV not prefilled (timing only)",
                "sm_share": None if os.environ.get("NO_SHARE") else SHARE},
     "compaction": {"note": "K3 moves + table remap, host plan included in the time", "runs": compactions, "moves": moves_total, "slabs_freed": slabs_freed,
