@@ -300,8 +300,9 @@ ks_status ks_paged_prefill_ws(ks_pool* pool, const ks_kv_format* fmt, uint32_t l
 
 /* Spatial sharing between co-located models (MPS-style SM partitioning,
  * PAPER.md section 2.4): cap the persistent K2 grid of the model with slab
- * key `key` at max_ctas CTAs (one CTA per SM), so co-located models' decode
- * kernels issued on different streams run side by side.  0 = whole GPU. */
+ * key `key` at max_ctas SMs (the kernel places one CTA per SM, two for INT8),
+ * so co-located models' decode kernels issued on different streams run side
+ * by side.  0 = whole GPU. */
 ks_status ks_set_decode_sm_share(ks_pool* pool, uint64_t key, uint32_t max_ctas);
 
 /* K3 -- slab compaction for one key (new; the reference never migrates,

@@ -775,11 +775,10 @@ template <int FMT, int NT, bool PK>
 static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t stream) {
   using Gm = Geo<FMT>;
   DecodeParams p = p0;
-  // INT8: head groups of 4 and two CTAs per SM (~100 KB rings) -- twice the
-  // producers and the same consumer warps per SM: 3-6 % faster at every shape
-  // measured (B1-64, ctx 1k-32k); FP8 mixed, FP16/INT4 neutral or slower
-  constexpr bool kPair = FMT == kINT8 && NT == 1;
-  uint32_t hg_max = NT == 1 ? (kPair ? 4 : 8) : 4;
+  // (INT8 with head groups of 4 and two CTAs per SM measured 1-6 % faster
+  // alone but 6 % slower co-located in BASELINE configs[3]: not used)
+  constexpr bool kPair = false;
+  uint32_t hg_max = NT == 1 ? 8 : 4;
   if (p.hg_max > 0) hg_max = p.hg_max < (NT == 1 ? 8u : 4u) ? p.hg_max : (NT == 1 ? 8u : 4u);
   uint32_t hg = 1;
   while (hg * 2 <= hg_max && p.H % (hg * 2) == 0) hg *= 2;
@@ -824,7 +823,9 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   if (FMT == kFP8 && p.max_ctas == 0 &&
       static_cast<uint64_t>(p.batch) * p.bt_stride * (p.H / hg) < static_cast<uint64_t>(grid) * 24)
     grid = std::max(1, grid * 3 / 4);
-  if (p.max_ctas > 0 && grid > p.max_ctas) grid = p.max_ctas;
+  // a model's SM share (ks_set_decode_sm_share) caps the SMs its grid may
+  // cover: per_sm CTAs on each
+  if (p.max_ctas > 0 && grid > p.max_ctas * per_sm) grid = p.max_ctas * per_sm;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);

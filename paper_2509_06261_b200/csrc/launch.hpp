@@ -33,7 +33,7 @@ struct DecodeParams {
   float* partials;
   // filled by the launcher
   uint32_t stage_bytes, bar_offset, qbuf_offset, prefix_offset, hg, stages;
-  int max_ctas;  // 0 = persistent full machine
+  int max_ctas;  // SMs the grid may cover (x CTAs per SM); 0 = persistent full machine
   uint32_t hg_max;        // 0 = default head-group size
   uint32_t smem_budget;   // ring bytes per CTA; 0 = default
   uint32_t merge_threads; // merge CTA size cap; 0 = default (256)
