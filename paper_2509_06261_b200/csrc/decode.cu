@@ -777,7 +777,6 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   DecodeParams p = p0;
   // (INT8 with head groups of 4 and two CTAs per SM measured 1-6 % faster
   // alone but 6 % slower co-located in BASELINE configs[3]: not used)
-  constexpr bool kPair = false;
   uint32_t hg_max = NT == 1 ? 8 : 4;
   if (p.hg_max > 0) hg_max = p.hg_max < (NT == 1 ? 8u : 4u) ? p.hg_max : (NT == 1 ? 8u : 4u);
   uint32_t hg = 1;
@@ -786,7 +785,7 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   p.stage_bytes = (2 * hg * (Gm::kChunk + Gm::kParam) + 127) / 128 * 128;
   const uint32_t qbytes = hg * p.G * kD * 2 + (p.k_new != nullptr ? 2 * hg * kD * 2 : 0);  // Q slot
   const size_t budget = p.smem_budget > 0 ? p.smem_budget
-                        : (kPair && p.hg_max == 0 ? 100000 : 220 * 1024 - (p.batch + 1) * 4 - 2 * qbytes - 512);
+                                          : 220 * 1024 - (p.batch + 1) * 4 - 2 * qbytes - 512;
   uint32_t stages = static_cast<uint32_t>(budget / p.stage_bytes);
   if (stages > 16) stages = 16;
   if (stages < 2) stages = 2;
