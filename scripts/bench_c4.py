@@ -76,9 +76,58 @@ def device_step():
 nsm = torch.cuda.get_device_properties(0).multi_processor_count
 w = [4096.0, 2048.0 + 64 / 16, 2048.0 + 64, 2 * (1024.0 + 64)]
 SHARE = [max(8, int(nsm * x / sum(w))) for x in w]
-if os.environ.get("NO_SHARE") is None:
-    for m, sh in zip(models, SHARE):
+
+def set_shares(shares):
+    for m, sh in zip(models, shares):
         kv.set_decode_sm_share(pool, m.key, sh)
+
+
+if os.environ.get("NO_SHARE") is None:
+    set_shares(SHARE)
+
+
+def tune_shares():
+    """Pick the SM split once, like bench.py's co-location autotune: a few
+    candidate splits (byte-proportional, INT4 weighted 1x/2x/3x, all SMs or
+    92 %) timed on an 8-layer eager pass at the full batch."""
+    for mi, m in enumerate(models):
+        for s_ in range(MAXB):
+            assert m.admit(s_, 1024)
+        m.sync()
+        ctx[mi].fill_(1024)
+    cands = []
+    for w4 in (1.0, 2.0, 3.0):
+        for tot in (nsm, int(nsm * 0.92)):
+            ww = [4096.0, 2052.0, 2112.0, w4 * 1088.0]
+            cands.append(tuple(max(8, int(tot * x / sum(ww))) for x in ww))
+    best, best_ms = None, None
+    for c in cands:
+        set_shares(c)
+        for _ in range(2):
+            a, b = ev(), ev()
+            a.record()
+            for layer in range(8):
+                for mi, m in enumerate(models):
+                    kv.paged_decode(pool, m.fmt, layer, q[mi][layer], m.table, ctx[mi], out=out[mi][layer],
+                                    kv_scales=scales, workspace=ws[mi], stream=streams[mi])
+            for st_ in streams:
+                torch.cuda.current_stream().wait_stream(st_)
+            b.record()
+            torch.cuda.synchronize()
+        t = a.elapsed_time(b)
+        if best_ms is None or t < best_ms:
+            best, best_ms = c, t
+    for mi, m in enumerate(models):
+        for s_ in range(MAXB):
+            m.release(s_)
+        ctx[mi].zero_()
+    return list(best)
+
+
+ev = lambda: torch.cuda.Event(enable_timing=True)
+if os.environ.get("NO_SHARE") is None and os.environ.get("NO_TUNE") is None:
+    SHARE = tune_shares()
+    set_shares(SHARE)
 
 # capture once: inactive rows have ctx 0 and cost nothing
 for mi, m in enumerate(models):  # a valid table for the warm-up launch
