@@ -214,3 +214,25 @@ def test_prefill_split_kv(dt, H, Hq, cases, split, monkeypatch):
     _, _, _, _, o, lse, r, rl = run_prefill(dt, H, Hq, cases, seed=71 + int(dt) + H)
     assert rel_err(o, r) <= TOL[dt]
     assert np.abs(lse - rl).max() <= 1e-3
+
+
+@pytest.mark.parametrize("dt", [KvDtype.FP16, KvDtype.INT4], ids=["FP16", "INT4"])
+def test_prefill_workspace_sizes_degrade_gracefully(dt):
+    """Any workspace size is valid: a buffer too small for the split-KV
+    partials drops the split (quantised formats then expand in sequence
+    groups if they fit one sequence, else run direct); every size gives the
+    oracle's answer."""
+    import ctypes as C
+    from paper_2509_06261_b200 import _lib as L
+    cases = [(3000, 64), (700, 1)]
+    w, fmt, q, cu, o_ref, _, r, _ = run_prefill(dt, 2, 8, cases, seed=81)
+    nq = max(n for _, n in cases)
+    full = C.c_size_t()
+    L.lib.ks_paged_prefill_workspace_size(C.byref(fmt.to_c()), len(cases), w["table"].shape[1], nq,
+                                          C.byref(full))
+    for nbytes in (0, 4096, full.value // 3, full.value):
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+        o = kv.paged_prefill(w["pool"], fmt, 0, dev(q), dev(w["table"]), dev(cu), dev(w["ctx"]), nq,
+                             workspace=ws if nbytes else None)
+        torch.cuda.synchronize()
+        assert rel_err(o.cpu().numpy().astype(np.float64), r) <= TOL[dt], nbytes
