@@ -369,3 +369,31 @@ def test_fused_append_decode_matches_separate_k1_k2(dt):
     torch.cuda.synchronize()
     assert torch.equal(img_fused, kv.kv_tensor(pool))
     assert torch.equal(fused, sep)
+
+
+@pytest.mark.parametrize("dt", [KvDtype.FP16, KvDtype.INT4], ids=["FP16", "INT4"])
+def test_decode_mostly_empty_slots(dt):
+    """A fixed-size batch with most slots empty (ctx 0): zero outputs and -inf
+    LSE for the empty slots (written by the whole grid over poisoned
+    buffers), oracle outputs for the live ones."""
+    ctx = [0] * 40
+    for i, c in ((3, 700), (17, 1), (22, 2048), (39, 64), (5, 333)):
+        ctx[i] = c
+    fmt = KvFormat(dt, 8, 32, num_layers=1)
+    w = make_world(fmt, ctx, seed=91)
+    append_gpu(w, fmt, 0)
+    img = kv.kv_tensor(w["pool"]).cpu().numpy()
+    q = w["rng"].standard_normal((len(ctx), 32, 128)).astype(np.float16)
+    out = torch.full((len(ctx), 32, 128), 7.0, dtype=torch.float16, device="cuda")  # poison
+    lse = torch.zeros((len(ctx), 32), dtype=torch.float32, device="cuda")
+    kv.paged_decode(w["pool"], fmt, 0, dev(q), dev(w["table"]), dev(w["ctx"]), out=out, lse=lse)
+    torch.cuda.synchronize()
+    f = oracle.fmt(int(dt), 8, 32, 128, 1, 16, fmt.qparams)
+    ref, _ = oracle.paged_decode(img, w["pool"].slab_size(), w["pool"].blocks_per_slab(fmt.key), f, 0,
+                                 q.view(np.uint16), w["table"], w["ctx"], 1 / math.sqrt(128), None,
+                                 nthreads=oracle.NPROC)
+    o = out.cpu().numpy()
+    live = w["ctx"] > 0
+    assert rel_err(o[live], ref[live]) <= TOL[dt]
+    assert (o[~live] == 0).all()
+    assert np.isneginf(lse.cpu().numpy()[~live]).all()
