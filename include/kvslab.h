@@ -236,8 +236,17 @@ ks_status ks_kv_append(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, c
 /* K2 -- slab-indexed paged decode attention.
  * d_q, d_out: fp16 [batch][Hq][d]; d_lse: fp32 [batch][Hq] natural-log
  * log-sum-exp (nullable); d_ctx_lens: int32 [batch]; sm_scale <= 0 means
- * 1/sqrt(d).  The workspace (>= ks_paged_decode_workspace_size bytes) must
- * be zero-filled once before first use; the kernel leaves it zeroed. */
+ * 1/sqrt(d).  The workspace (>= ks_paged_decode_workspace_size bytes) holds
+ * the fp32 partials of sequence-heads split across CTAs; it needs no
+ * initialisation, but launches that may run concurrently (different streams)
+ * need distinct workspaces.
+ * Programmatic dependent launch: each K2 grid lets the next kernel on its
+ * stream start early, and issues the bulk copies of its first KV blocks
+ * before waiting for its predecessor.  Back-to-back launches on the same
+ * stream must therefore not read a block the previous launch writes -- i.e.
+ * two ks_paged_decode_append calls in a row must target different layers (a
+ * decode step appends layer by layer, so this holds for one step per layer;
+ * with a 1-layer format put any other kernel between two steps). */
 ks_status ks_paged_decode_workspace_size(const ks_pool* pool, const ks_kv_format* fmt,
                                          uint32_t batch, size_t* bytes);
 ks_status ks_paged_decode(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, const void* d_q,
@@ -320,9 +329,80 @@ ks_status ks_compact_plan(ks_pool* pool, uint64_t key, uint32_t max_moves, ks_bl
 /* copies `key` bytes per move inside the KV tensor (K3 kernel) */
 ks_status ks_compact_apply(ks_pool* pool, uint64_t key, const ks_block_move* moves, uint32_t n,
                            void* stream);
-/* rewrites block-table entries equal to a moved src id to its dst id */
+/* rewrites block-table entries equal to a moved src id to its dst id (any
+ * number of moves; taken in chunks) */
 ks_status ks_block_table_remap(ks_pool* pool, int32_t* d_table, uint64_t n_entries,
                                const ks_block_move* moves, uint32_t n, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Engine block tables (simulator.cpp:33-40 LiveRequest::blocks)      */
+/* ------------------------------------------------------------------ */
+/* A sequence table is the engine-side logical block table of one model: a
+ * row per sequence slot holding its handles in logical-block order and its
+ * cached-token count, driven by the reference's three allocator call sites
+ * -- prefill claim with rollback (simulator.cpp:500-526), decode growth
+ * need = ceil((cached+1)/tpb) with per-request stall (:561-578), release on
+ * completion / eviction (:583-596, :621) -- and mirrored into the engine's
+ * int32 device table [max_seqs][row_stride] of global block ids by delta
+ * upload (ks_seq_table_sync).  Tables register with their pool, so
+ * ks_compact rewrites every table of the compacted key, whichever model owns
+ * it.  Destroying a table does not free its blocks (release rows first);
+ * destroying the pool detaches its tables (later calls fail). */
+typedef struct ks_seq_table ks_seq_table;
+typedef struct ks_seq_table_config {
+  uint64_t key;                  /* the model's slab key (kv_block_size) */
+  uint32_t max_seqs;
+  uint32_t max_blocks_per_seq;
+  uint32_t tokens_per_block;
+  uint32_t reserved;
+  uint64_t useful_token_bytes;   /* num_layers * token_size (simulator.cpp:210) */
+  uint64_t block_metadata_bytes; /* num_layers * quant params per block (:211-212) */
+  int32_t* d_table;              /* engine-owned device table; NULL = host only */
+  uint32_t row_stride;           /* entries per device row, >= max_blocks_per_seq */
+} ks_seq_table_config;
+typedef struct ks_seq_table_stats {
+  uint32_t live_seqs;            /* rows holding blocks */
+  uint64_t held_blocks;          /* held_blocks_total (simulator.cpp:75-79) */
+  uint64_t cached_tokens;        /* cached_total (simulator.cpp:70-74) */
+  uint64_t internal_frag_bytes;  /* internal_frag_bytes (simulator.cpp:80-89) */
+} ks_seq_table_stats;
+ks_status ks_seq_table_create(ks_pool* pool, const ks_seq_table_config* cfg, ks_seq_table** out);
+ks_status ks_seq_table_destroy(ks_seq_table* t);
+/* prefill claim: ceil(prompt/tpb) blocks or none; *ok = 0 when the pool cannot back it */
+ks_status ks_seq_table_admit(ks_seq_table* t, uint32_t seq, uint64_t prompt_tokens, int32_t* ok);
+/* growth to ceil(tokens/tpb) blocks; *ok = 0 = stalled (blocks claimed so far are kept) */
+ks_status ks_seq_table_ensure(ks_seq_table* t, uint32_t seq, uint64_t tokens, int32_t* ok);
+/* one decode step of a batch: each listed row grows for its next token and,
+ * if it got the block, advances by one; stalled[i] (nullable) = 1 otherwise */
+ks_status ks_seq_table_step(ks_seq_table* t, const uint32_t* seqs, uint32_t n, uint8_t* stalled,
+                            uint32_t* n_active);
+ks_status ks_seq_table_release(ks_seq_table* t, uint32_t seq);
+/* moves a sequence to an empty row (no allocator traffic), e.g. to keep the
+ * running batch in rows 0..B-1; the destination row is re-uploaded */
+ks_status ks_seq_table_move_row(ks_seq_table* t, uint32_t src, uint32_t dst);
+ks_status ks_seq_table_cached(const ks_seq_table* t, uint32_t seq, uint64_t* tokens);
+ks_status ks_seq_table_set_cached(ks_seq_table* t, uint32_t seq, uint64_t tokens);
+/* out[s] = cached(s) + plus for rows 0..n-1 that hold blocks, 0 for empty rows */
+ks_status ks_seq_table_ctx_lens(const ks_seq_table* t, int32_t* out, uint32_t n, int32_t plus);
+/* *n = blocks held by the row; the first min(*n, capacity) handles are written */
+ks_status ks_seq_table_blocks(const ks_seq_table* t, uint32_t seq, ks_block_handle* out,
+                              uint32_t capacity, uint32_t* n);
+ks_status ks_seq_table_get_stats(const ks_seq_table* t, ks_seq_table_stats* out);
+/* number of entries changed since the last sync */
+ks_status ks_seq_table_pending(const ks_seq_table* t, uint32_t* n);
+ks_status ks_seq_table_sync(ks_seq_table* t, void* stream);
+
+/* K3 as one transaction: plan (<= max_moves), move the bytes, and rewrite
+ * the handles and device entries of every registered table of `key`, all on
+ * `stream`.  On any failure the host slab table and the tables are restored
+ * and nothing is reported as moved.  `stream` must be ordered after every
+ * earlier launch that touches blocks of `key`; later launches through this
+ * library on other streams wait for the compaction automatically (eager
+ * launches; capture graphs after the compaction has been issued on the
+ * replay stream).  Tables that are not registered can be rewritten with
+ * ks_compact_plan / ks_compact_apply / ks_block_table_remap. */
+ks_status ks_compact(ks_pool* pool, uint64_t key, uint32_t max_moves, void* stream,
+                     uint32_t* n_moves, uint32_t* slabs_freed);
 
 /* Number of kernel launches this process issued through the library
  * (per kernel family); used by bench.py for its gpu_launches claim. */

@@ -68,6 +68,18 @@ class ks_block_move(C.Structure):
     _fields_ = [("src_global_block_id", C.c_uint64), ("dst_global_block_id", C.c_uint64)]
 
 
+class ks_seq_table_config(C.Structure):
+    _fields_ = [("key", C.c_uint64), ("max_seqs", C.c_uint32), ("max_blocks_per_seq", C.c_uint32),
+                ("tokens_per_block", C.c_uint32), ("reserved", C.c_uint32),
+                ("useful_token_bytes", C.c_uint64), ("block_metadata_bytes", C.c_uint64),
+                ("d_table", C.c_void_p), ("row_stride", C.c_uint32)]
+
+
+class ks_seq_table_stats(C.Structure):
+    _fields_ = [("live_seqs", C.c_uint32), ("held_blocks", C.c_uint64),
+                ("cached_tokens", C.c_uint64), ("internal_frag_bytes", C.c_uint64)]
+
+
 OP_LOG_FN = C.CFUNCTYPE(None, C.POINTER(ks_op_record), C.c_void_p)
 CLOCK_FN = C.CFUNCTYPE(C.c_double, C.c_void_p)
 
@@ -128,6 +140,21 @@ _SIGS = {
     "ks_compact_plan": (st, [P, u64, u32, C.POINTER(ks_block_move), pu32, pu32]),
     "ks_compact_apply": (st, [P, u64, C.POINTER(ks_block_move), u32, P]),
     "ks_block_table_remap": (st, [P, P, u64, C.POINTER(ks_block_move), u32, P]),
+    "ks_seq_table_create": (st, [P, C.POINTER(ks_seq_table_config), C.POINTER(P)]),
+    "ks_seq_table_destroy": (st, [P]),
+    "ks_seq_table_admit": (st, [P, u32, u64, pi32]),
+    "ks_seq_table_ensure": (st, [P, u32, u64, pi32]),
+    "ks_seq_table_step": (st, [P, pu32, u32, C.POINTER(C.c_uint8), pu32]),
+    "ks_seq_table_release": (st, [P, u32]),
+    "ks_seq_table_move_row": (st, [P, u32, u32]),
+    "ks_seq_table_cached": (st, [P, u32, pu64]),
+    "ks_seq_table_set_cached": (st, [P, u32, u64]),
+    "ks_seq_table_ctx_lens": (st, [P, pi32, u32, i32]),
+    "ks_seq_table_blocks": (st, [P, u32, C.POINTER(ks_block_handle), u32, pu32]),
+    "ks_seq_table_get_stats": (st, [P, C.POINTER(ks_seq_table_stats)]),
+    "ks_seq_table_pending": (st, [P, pu32]),
+    "ks_seq_table_sync": (st, [P, P]),
+    "ks_compact": (st, [P, u64, u32, P, pu32, pu32]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -15,12 +15,15 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
+#include "kvslab/seq_table.hpp"
 #include "kvslab/slab_pool.hpp"
 #include "launch.hpp"
 
 using kvslab::BlockHandle;
+using kvslab::SeqTable;
 using kvslab::SlabPool;
 
 namespace {
@@ -48,6 +51,8 @@ ks_status guarded(F&& f) {
   } catch (const kvslab::InvalidProfileError& e) {
     return fail(KS_INVALID_PROFILE, e.what());
   } catch (const std::out_of_range& e) {
+    return fail(KS_INVALID_ARGUMENT, e.what());
+  } catch (const std::invalid_argument& e) {
     return fail(KS_INVALID_ARGUMENT, e.what());
   } catch (const std::bad_alloc&) {
     return fail(KS_INTERNAL, "host allocation failed");
@@ -95,6 +100,34 @@ constexpr size_t kStageWords = 1u << 20;  // 4 MiB of uint32 staging
 
 }  // namespace
 
+namespace kvslab {
+Tuning Tuning::from_env() {
+  Tuning t;
+  auto num = [](const char* name, long dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::strtol(v, nullptr, 0) : dflt;
+  };
+  t.decode_max_ctas = static_cast<int>(num("KVSLAB_DECODE_MAX_CTAS", 0));
+  t.decode_hg = static_cast<uint32_t>(num("KVSLAB_DECODE_HG", 0));
+  t.decode_smem = static_cast<uint32_t>(num("KVSLAB_DECODE_SMEM", 0));
+  t.merge_threads = static_cast<uint32_t>(num("KVSLAB_MERGE_THREADS", 0));
+  t.merge_dc = static_cast<uint32_t>(num("KVSLAB_MERGE_DC", 0));
+  t.decode_pack = static_cast<uint32_t>(num("KVSLAB_DECODE_PACK", 0));
+  t.pdl = num("KVSLAB_NO_PDL", 0) ? 0 : 1;
+  t.prefill_nt = static_cast<uint32_t>(num("KVSLAB_PREFILL_NT", 0));
+  t.prefill_tc = static_cast<int>(num("KVSLAB_PREFILL_TC", 2));
+  t.prefill_expand = static_cast<int>(num("KVSLAB_PREFILL_EXPAND", -1));
+  t.prefill_split = static_cast<int>(num("KVSLAB_PREFILL_SPLIT", 1));
+  if (kProbes) {
+    t.decode_trace = reinterpret_cast<unsigned long long*>(
+        static_cast<uintptr_t>(std::strtoull(std::getenv("KVSLAB_DECODE_TRACE") ? std::getenv("KVSLAB_DECODE_TRACE") : "0", nullptr, 0)));
+    t.decode_debug = static_cast<int>(num("KVSLAB_DECODE_DEBUG", 0));
+    t.prefill_debug = static_cast<int>(num("KVSLAB_PREFILL_DEBUG", 0));
+  }
+  return t;
+}
+}  // namespace kvslab
+
 struct ks_pool {
   // Pinned host -> device staging ring for small control uploads (table
   // deltas, move lists).  A slot is reused only after the kernel that read it
@@ -123,10 +156,23 @@ struct ks_pool {
   void* clock_user = nullptr;
   std::vector<uint32_t> dirty;
   std::map<uint64_t, uint32_t> cta_budget;  // per key: K2 CTAs (SM share), 0 = all
+  // Engine tables registered on this pool (ks_seq_table_create); compaction
+  // remaps every table of the compacted key, whoever owns it.
+  std::vector<ks_seq_table*> tables;
+  // Compaction fence: source slabs return FREE on the host before their
+  // bytes leave on the compaction stream, so until that work completes every
+  // launch on another stream waits for it (wait_fence).
+  cudaEvent_t fence = nullptr;
+  cudaStream_t fence_stream = nullptr;
+  bool fence_pending = false;
+  // Tuning overrides, read from the environment once at pool creation.
+  kvslab::Tuning tuning;
 
-  ~ks_pool() {
+  ~ks_pool();
+  void destroy_device() {
     if (device >= 0) {
       DeviceGuard g(device);
+      if (fence) cudaEventSynchronize(fence), cudaEventDestroy(fence);
       for (int i = 0; i < kSlots; ++i)
         if (slot_ev[i]) cudaEventSynchronize(slot_ev[i]), cudaEventDestroy(slot_ev[i]);
       cudaFree(d_base);
@@ -160,7 +206,37 @@ struct ks_pool {
   }
 };
 
+struct ks_seq_table {
+  ks_pool* owner = nullptr;  // null once the pool is destroyed
+  std::unique_ptr<kvslab::SeqTable> t;
+  int32_t* d_table = nullptr;
+  uint32_t row_stride = 0;
+};
+
+ks_pool::~ks_pool() {
+  for (ks_seq_table* t : tables) t->owner = nullptr;
+  destroy_device();
+}
+
 namespace {
+
+// Orders `s` after a pending compaction (see ks_pool::fence).  Eager launches
+// only: a stream being captured into a graph is left alone (graphs are
+// replayed later, after the compaction stream's work was enqueued).
+cudaError_t wait_fence(ks_pool* p, cudaStream_t s) {
+  if (!p->fence_pending) return cudaSuccess;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(s, &cs);
+  if (e != cudaSuccess || cs != cudaStreamCaptureStatusNone) return e;
+  e = cudaEventQuery(p->fence);
+  if (e == cudaSuccess) {
+    p->fence_pending = false;
+    return cudaSuccess;
+  }
+  if (e != cudaErrorNotReady) return e;
+  if (s == p->fence_stream) return cudaSuccess;
+  return cudaStreamWaitEvent(s, p->fence, 0);
+}
 
 uint32_t fmt_bits(uint32_t dt) { return dt == KS_KV_FP16 ? 16 : (dt == KS_KV_INT4 ? 4 : 8); }
 
@@ -292,6 +368,9 @@ ks_status ks_pool_create(const ks_pool_config* cfg, int device, ks_pool** out) {
         e = cudaEventCreateWithFlags(&p->slot_ev[i], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
       }
+      e = cudaEventCreateWithFlags(&p->fence, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+      p->tuning = kvslab::Tuning::from_env();
       e = cudaDeviceSynchronize();
       if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
     }
@@ -685,6 +764,8 @@ ks_status ks_kv_append(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, c
     p.block_table = d_block_table;
     p.bt_stride = bt_stride;
     p.kv_scales = d_kv_scales;
+    cudaError_t fe = wait_fence(pool, static_cast<cudaStream_t>(stream));
+    if (fe != cudaSuccess) return cuda_fail(fe, "compaction fence");
     cudaError_t e = kvslab::launch_kv_append(p, static_cast<int>(fmt->kv_dtype),
                                              static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "kv_append launch");
@@ -746,22 +827,23 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
     if ((d_k_new == nullptr) != (d_v_new == nullptr))
       return fail(KS_INVALID_ARGUMENT, "k_new and v_new must both be set or both be null");
     p.partials = static_cast<float*>(d_workspace);
+    const kvslab::Tuning& tu = pool->tuning;
     p.max_ctas = 0;
-    if (const char* dbg = std::getenv("KVSLAB_DECODE_DEBUG")) p.debug = std::atoi(dbg);
     {
       auto it = pool->cta_budget.find(fi.key);
       if (it != pool->cta_budget.end()) p.max_ctas = static_cast<int>(it->second);
     }
-    if (const char* mc = std::getenv("KVSLAB_DECODE_MAX_CTAS")) p.max_ctas = std::atoi(mc);
-    if (const char* hg = std::getenv("KVSLAB_DECODE_HG")) p.hg_max = static_cast<uint32_t>(std::atoi(hg));
-    if (const char* sb = std::getenv("KVSLAB_DECODE_SMEM")) p.smem_budget = static_cast<uint32_t>(std::atoi(sb));
-    if (const char* mt = std::getenv("KVSLAB_MERGE_THREADS")) p.merge_threads = static_cast<uint32_t>(std::atoi(mt));
-    if (const char* md = std::getenv("KVSLAB_MERGE_DC")) p.merge_dc = static_cast<uint32_t>(std::atoi(md));
-    if (const char* pk = std::getenv("KVSLAB_DECODE_PACK")) p.pack_mode = static_cast<uint32_t>(std::atoi(pk));
-    p.pdl = 1;
-    if (const char* tr = std::getenv("KVSLAB_DECODE_TRACE"))
-      p.trace = reinterpret_cast<unsigned long long*>(std::strtoull(tr, nullptr, 0));
-    if (const char* np = std::getenv("KVSLAB_NO_PDL")) p.pdl = std::atoi(np) ? 0 : 1;
+    if (tu.decode_max_ctas) p.max_ctas = tu.decode_max_ctas;
+    p.hg_max = tu.decode_hg;
+    p.smem_budget = tu.decode_smem;
+    p.merge_threads = tu.merge_threads;
+    p.merge_dc = tu.merge_dc;
+    p.pack_mode = tu.decode_pack;
+    p.debug = tu.decode_debug;
+    p.pdl = tu.pdl;
+    p.trace = tu.decode_trace;  // probe builds only (Tuning::from_env)
+    cudaError_t fe = wait_fence(pool, static_cast<cudaStream_t>(stream));
+    if (fe != cudaSuccess) return cuda_fail(fe, "compaction fence");
     cudaError_t e = kvslab::launch_paged_decode(p, static_cast<int>(fmt->kv_dtype), pool->num_sms,
                                                 static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "paged_decode launch");
@@ -792,7 +874,15 @@ ks_status ks_paged_decode_append(ks_pool* pool, const ks_kv_format* fmt, uint32_
                      workspace_bytes, stream);
 }
 
-static int prefill_sms(const ks_pool* pool) { return pool && pool->num_sms > 0 ? pool->num_sms : 148; }
+static int prefill_sms(const ks_pool* pool) {
+  if (pool && pool->num_sms > 0) return pool->num_sms;
+  int dev = 0, n = 0;  // the size query has no pool: the current device's SMs
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+    return n;
+  cudaGetLastError();
+  return 148;
+}
 
 // Workspace layout: [split-KV partials][expand scratch]
 ks_status ks_paged_prefill_workspace_size(const ks_kv_format* fmt, uint32_t batch, uint32_t bt_stride,
@@ -807,8 +897,8 @@ ks_status ks_paged_prefill_workspace_size(const ks_kv_format* fmt, uint32_t batc
 
 // Expand-once pays off when each KV tile would otherwise be dequantised by
 // several query-tile CTAs of a head (two 128-row tiles per CTA).
-static bool prefill_expands(uint32_t max_q_len, uint32_t G) {
-  if (const char* e = std::getenv("KVSLAB_PREFILL_EXPAND")) return std::atoi(e) != 0;
+static bool prefill_expands(const kvslab::Tuning& tu, uint32_t max_q_len, uint32_t G) {
+  if (tu.prefill_expand >= 0) return tu.prefill_expand != 0;
   return static_cast<uint64_t>(max_q_len) * G >= 1024;
 }
 
@@ -851,27 +941,30 @@ static ks_status prefill_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t l
     const float scale = sm_scale > 0.f ? sm_scale : 1.0f / std::sqrt(static_cast<float>(fmt->head_dim));
     p.sm_scale_log2 = scale * 1.4426950408889634f;
     p.kv_scales = fmt->kv_dtype == KS_KV_FP8_E4M3 ? d_kv_scales : nullptr;
-    if (const char* nt = std::getenv("KVSLAB_PREFILL_NT")) p.nt = static_cast<uint32_t>(std::atoi(nt));
-    p.use_tc = 2;
-    if (const char* tc = std::getenv("KVSLAB_PREFILL_TC")) p.use_tc = std::atoi(tc);
-    if (const char* dbg = std::getenv("KVSLAB_PREFILL_DEBUG")) p.debug = std::atoi(dbg);
-    // split-KV when the query tiles alone would leave SMs idle (tcgen05 path),
-    // its partials at the start of the workspace
+    const kvslab::Tuning& tu = pool->tuning;
+    p.nt = tu.prefill_nt;
+    p.use_tc = tu.prefill_tc;
+    p.debug = tu.prefill_debug;
+    cudaError_t fe = wait_fence(pool, static_cast<cudaStream_t>(stream));
+    if (fe != cudaSuccess) return cuda_fail(fe, "compaction fence");
+    // Workspace use (kvslab.h): split-KV partials when the query tiles alone
+    // would leave SMs idle (tcgen05 path) and, for quantised formats with long
+    // chunks, the expand-once scratch.  A workspace too small for both drops
+    // the split first, then takes the expand in sequence groups.
     uint8_t* ws = static_cast<uint8_t*>(d_workspace);
-    if (ws && p.use_tc) {
+    const bool expand = ws != nullptr && fmt->kv_dtype != KS_KV_FP16 && p.use_tc &&
+                        prefill_expands(tu, max_q_len, G);
+    const size_t full_expand = expand ? kvslab::prefill_expand_bytes(p.H, batch, bt_stride) : 0;
+    if (ws && p.use_tc && tu.prefill_split != 0) {
       const uint32_t splits = kvslab::prefill_kv_splits(batch, p.H, G, max_q_len, prefill_sms(pool));
       const size_t pb = kvslab::prefill_partial_bytes(batch, p.H, G, max_q_len, splits);
-      if (splits > 1 && (std::getenv("KVSLAB_PREFILL_SPLIT") == nullptr ||
-                         std::atoi(std::getenv("KVSLAB_PREFILL_SPLIT")) != 0) &&
-          workspace_bytes >= pb) {
+      if (splits > 1 && workspace_bytes >= pb + full_expand) {
         p.kv_splits = splits;
         p.part = reinterpret_cast<float*>(ws);
         ws += pb;
         workspace_bytes -= pb;
       }
     }
-    const bool expand = ws != nullptr && fmt->kv_dtype != KS_KV_FP16 && p.use_tc &&
-                        prefill_expands(max_q_len, G);
     const size_t per_seq = kvslab::prefill_expand_bytes(p.H, 1, bt_stride);
     if (expand && per_seq > 0 && workspace_bytes >= per_seq) {
       // a workspace smaller than the whole batch's takes the sequences in groups
@@ -985,27 +1078,22 @@ ks_status ks_compact_apply(ks_pool* pool, uint64_t key, const ks_block_move* mov
   });
 }
 
-ks_status ks_block_table_remap(ks_pool* pool, int32_t* d_table, uint64_t n_entries,
-                               const ks_block_move* moves, uint32_t n, void* stream) {
-  return guarded([&] {
-    if (!pool || pool->device < 0) return fail(KS_INVALID_ARGUMENT, "pool has no device tensor");
-    if (n == 0 || n_entries == 0) return KS_OK;
-    if (!d_table || !moves) return fail(KS_INVALID_ARGUMENT, "null argument");
-    if (2ull * n > ks_pool::kSlotWords) return fail(KS_NOT_SUPPORTED, "too many moves for one remap");
-    std::vector<std::pair<uint32_t, uint32_t>> v(n);
-    for (uint32_t i = 0; i < n; ++i)
-      v[i] = {static_cast<uint32_t>(moves[i].src_global_block_id),
-              static_cast<uint32_t>(moves[i].dst_global_block_id)};
-    std::sort(v.begin(), v.end());
-    DeviceGuard g(pool->device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+// Rewrites table entries through the sorted move list, in chunks of one
+// staging slot.  Sources and destinations of one plan are disjoint (a slab
+// that received blocks is never evacuated, an evacuated slab never receives),
+// so chunked passes remap every entry at most once.
+static ks_status remap_table(ks_pool* pool, int32_t* d_table, uint64_t n_entries,
+                             const std::vector<std::pair<uint32_t, uint32_t>>& v, cudaStream_t s) {
+  const size_t per = ks_pool::kSlotWords / 2;
+  for (size_t i0 = 0; i0 < v.size(); i0 += per) {
+    const uint32_t n = static_cast<uint32_t>(std::min(per, v.size() - i0));
     int si = 0;
     ks_pool::Slot sl;
     cudaError_t e = pool->acquire(&si, &sl);
     if (e != cudaSuccess) return cuda_fail(e, "staging wait");
     for (uint32_t i = 0; i < n; ++i) {
-      sl.h[i] = v[i].first;
-      sl.h[n + i] = v[i].second;
+      sl.h[i] = v[i0 + i].first;
+      sl.h[n + i] = v[i0 + i].second;
     }
     e = pool->upload(sl, 2 * static_cast<size_t>(n), s);
     if (e != cudaSuccess) return cuda_fail(e, "staging upload");
@@ -1014,6 +1102,281 @@ ks_status ks_block_table_remap(ks_pool* pool, int32_t* d_table, uint64_t n_entri
     e = pool->release(si, s);
     if (e != cudaSuccess) return cuda_fail(e, "staging release");
     ++g_launches;
+  }
+  return KS_OK;
+}
+
+ks_status ks_block_table_remap(ks_pool* pool, int32_t* d_table, uint64_t n_entries,
+                               const ks_block_move* moves, uint32_t n, void* stream) {
+  return guarded([&] {
+    if (!pool || pool->device < 0) return fail(KS_INVALID_ARGUMENT, "pool has no device tensor");
+    if (n == 0 || n_entries == 0) return KS_OK;
+    if (!d_table || !moves) return fail(KS_INVALID_ARGUMENT, "null argument");
+    std::vector<std::pair<uint32_t, uint32_t>> v(n);
+    for (uint32_t i = 0; i < n; ++i)
+      v[i] = {static_cast<uint32_t>(moves[i].src_global_block_id),
+              static_cast<uint32_t>(moves[i].dst_global_block_id)};
+    std::sort(v.begin(), v.end());
+    DeviceGuard g(pool->device);
+    return remap_table(pool, d_table, n_entries, v, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// ------------------------------------------------------------- engine tables
+static ks_status seq_table_sync_impl(ks_seq_table* t, cudaStream_t s) {
+  ks_pool* pool = t->owner;
+  t->t->dedupe_pending();
+  const auto& pend = t->t->pending();
+  if (pend.empty()) return KS_OK;
+  if (!t->d_table || pool->device < 0) {  // host-only table: nothing to mirror
+    t->t->clear_pending();
+    return KS_OK;
+  }
+  DeviceGuard g(pool->device);
+  cudaError_t fe = wait_fence(pool, s);
+  if (fe != cudaSuccess) return cuda_fail(fe, "compaction fence");
+  size_t i = 0;
+  while (i < pend.size()) {
+    const size_t m = std::min(pend.size() - i, ks_pool::kSlotWords / 3);
+    int si = 0;
+    ks_pool::Slot sl;
+    cudaError_t e = pool->acquire(&si, &sl);
+    if (e != cudaSuccess) return cuda_fail(e, "staging wait");
+    std::memcpy(sl.h, pend.data() + i, m * sizeof(SeqTable::Delta));
+    e = pool->upload(sl, 3 * m, s);
+    if (e != cudaSuccess) return cuda_fail(e, "staging upload");
+    e = kvslab::launch_table_scatter(t->d_table, t->row_stride, reinterpret_cast<const int32_t*>(sl.d),
+                                     static_cast<uint32_t>(m), s);
+    if (e != cudaSuccess) return cuda_fail(e, "table scatter");
+    e = pool->release(si, s);
+    if (e != cudaSuccess) return cuda_fail(e, "staging release");
+    ++g_launches;
+    i += m;
+  }
+  t->t->clear_pending();
+  return KS_OK;
+}
+
+#define KS_TABLE_GUARD(t)                                                     \
+  if (!(t)) return fail(KS_INVALID_ARGUMENT, "null table");                   \
+  if (!(t)->owner) return fail(KS_INVALID_ARGUMENT, "table's pool was destroyed")
+
+ks_status ks_seq_table_create(ks_pool* pool, const ks_seq_table_config* cfg, ks_seq_table** out) {
+  return guarded([&] {
+    if (!pool || !cfg || !out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (cfg->d_table && cfg->row_stride < cfg->max_blocks_per_seq)
+      return fail(KS_INVALID_ARGUMENT, "row_stride < max_blocks_per_seq");
+    auto t = std::make_unique<ks_seq_table>();
+    t->t = std::make_unique<SeqTable>(pool->pool.get(), cfg->key, cfg->max_seqs,
+                                      cfg->max_blocks_per_seq, cfg->tokens_per_block,
+                                      cfg->useful_token_bytes, cfg->block_metadata_bytes);
+    t->owner = pool;
+    t->d_table = cfg->d_table;
+    t->row_stride = cfg->d_table ? cfg->row_stride : cfg->max_blocks_per_seq;
+    pool->tables.push_back(t.get());
+    *out = t.release();
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_destroy(ks_seq_table* t) {
+  if (!t) return KS_OK;
+  if (t->owner) {
+    auto& v = t->owner->tables;
+    v.erase(std::remove(v.begin(), v.end(), t), v.end());
+  }
+  delete t;
+  return KS_OK;
+}
+
+ks_status ks_seq_table_admit(ks_seq_table* t, uint32_t seq, uint64_t prompt_tokens, int32_t* ok) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    if (!ok) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *ok = t->t->admit(seq, prompt_tokens) ? 1 : 0;
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_ensure(ks_seq_table* t, uint32_t seq, uint64_t tokens, int32_t* ok) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    if (!ok) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *ok = t->t->ensure_capacity(seq, tokens) ? 1 : 0;
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_step(ks_seq_table* t, const uint32_t* seqs, uint32_t n, uint8_t* stalled,
+                            uint32_t* n_active) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    if ((!seqs && n) || !n_active) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *n_active = t->t->step(seqs, n, stalled);
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_release(ks_seq_table* t, uint32_t seq) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    t->t->release(seq);
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_move_row(ks_seq_table* t, uint32_t src, uint32_t dst) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    t->t->move_row(src, dst);
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_cached(const ks_seq_table* t, uint32_t seq, uint64_t* tokens) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    if (!tokens) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *tokens = t->t->cached(seq);
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_set_cached(ks_seq_table* t, uint32_t seq, uint64_t tokens) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    t->t->set_cached(seq, tokens);
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_ctx_lens(const ks_seq_table* t, int32_t* out, uint32_t n, int32_t plus) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    if (!out && n) return fail(KS_INVALID_ARGUMENT, "null argument");
+    if (n > t->t->max_seqs()) return fail(KS_INVALID_ARGUMENT, "more rows than the table has");
+    for (uint32_t s = 0; s < n; ++s)
+      out[s] = t->t->blocks(s).empty() ? 0 : static_cast<int32_t>(t->t->cached(s)) + plus;
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_blocks(const ks_seq_table* t, uint32_t seq, ks_block_handle* out,
+                              uint32_t capacity, uint32_t* n) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    if (!n || (!out && capacity)) return fail(KS_INVALID_ARGUMENT, "null argument");
+    const auto& hs = t->t->blocks(seq);
+    *n = static_cast<uint32_t>(hs.size());
+    const size_t m = std::min<size_t>(hs.size(), capacity);
+    for (size_t i = 0; i < m; ++i) out[i] = to_c(hs[i]);
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_get_stats(const ks_seq_table* t, ks_seq_table_stats* out) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    if (!out) return fail(KS_INVALID_ARGUMENT, "null argument");
+    const auto st = t->t->stats();
+    out->live_seqs = st.live_seqs;
+    out->held_blocks = st.held_blocks;
+    out->cached_tokens = st.cached_tokens;
+    out->internal_frag_bytes = st.internal_frag_bytes;
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_pending(const ks_seq_table* t, uint32_t* n) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    if (!n) return fail(KS_INVALID_ARGUMENT, "null argument");
+    *n = static_cast<uint32_t>(t->t->pending().size());
+    return KS_OK;
+  });
+}
+
+ks_status ks_seq_table_sync(ks_seq_table* t, void* stream) {
+  return guarded([&] {
+    KS_TABLE_GUARD(t);
+    return seq_table_sync_impl(t, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// K3 over every registered table of the key, all-or-nothing on the host.
+ks_status ks_compact(ks_pool* pool, uint64_t key, uint32_t max_moves, void* stream,
+                     uint32_t* n_moves, uint32_t* slabs_freed) {
+  return guarded([&] {
+    if (!pool) return fail(KS_INVALID_ARGUMENT, "null pool");
+    if (pool->device < 0) return fail(KS_INVALID_ARGUMENT, "pool has no device tensor");
+    if (key % 16 != 0 || pool->pool->slab_size() % 16 != 0)
+      return fail(KS_NOT_SUPPORTED, "key and slab size must be multiples of 16 bytes");
+    const uint64_t bps = pool->pool->blocks_per_slab(key);  // InvalidKeyError first
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<ks_seq_table*> mine;
+    for (ks_seq_table* t : pool->tables)
+      if (t->t->key() == key) mine.push_back(t);
+    // snapshot for rollback: the host table and the affected engine tables
+    SlabPool before(*pool->pool);
+    std::vector<SeqTable> rows_before;
+    rows_before.reserve(mine.size());
+    for (ks_seq_table* t : mine) rows_before.push_back(*t->t);
+    uint32_t freed = 0;
+    const auto mv = pool->pool->plan_compaction(key, max_moves, &freed);
+    auto rollback = [&](ks_status st) {
+      *pool->pool = before;
+      for (size_t i = 0; i < mine.size(); ++i) *mine[i]->t = rows_before[i];
+      return st;
+    };
+    if (!mv.empty()) {
+      DeviceGuard g(pool->device);
+      cudaError_t fe = wait_fence(pool, s);
+      if (fe != cudaSuccess) return rollback(cuda_fail(fe, "compaction fence"));
+      // bytes
+      const size_t per = ks_pool::kSlotWords / 2;
+      for (size_t i0 = 0; i0 < mv.size(); i0 += per) {
+        const uint32_t m = static_cast<uint32_t>(std::min(per, mv.size() - i0));
+        int si = 0;
+        ks_pool::Slot sl;
+        cudaError_t e = pool->acquire(&si, &sl);
+        if (e != cudaSuccess) return rollback(cuda_fail(e, "staging wait"));
+        for (uint32_t j = 0; j < m; ++j) {
+          sl.h[j] = static_cast<uint32_t>(mv[i0 + j].src.global_block_id);
+          sl.h[m + j] = static_cast<uint32_t>(mv[i0 + j].dst.global_block_id);
+        }
+        e = pool->upload(sl, 2 * static_cast<size_t>(m), s);
+        if (e != cudaSuccess) return rollback(cuda_fail(e, "staging upload"));
+        kvslab::CompactParams p{};
+        p.pool = pool->d_base;
+        p.geom.slab_size = pool->pool->slab_size();
+        p.geom.key = key;
+        p.geom.bps = kvslab::dev::make_fastdiv(static_cast<uint32_t>(bps));
+        p.src_gid = sl.d;
+        p.dst_gid = sl.d + m;
+        p.n_moves = m;
+        e = kvslab::launch_compact(p, pool->num_sms, s);
+        if (e != cudaSuccess) return rollback(cuda_fail(e, "compact launch"));
+        e = pool->release(si, s);
+        if (e != cudaSuccess) return rollback(cuda_fail(e, "staging release"));
+        ++g_launches;
+      }
+      // handles + device entries of every table of the key
+      std::unordered_map<uint64_t, BlockHandle> moved;
+      moved.reserve(mv.size() * 2);
+      for (const auto& m : mv) moved.emplace(m.src.global_block_id, m.dst);
+      for (ks_seq_table* t : mine) {
+        t->t->remap(moved);
+        ks_status st = seq_table_sync_impl(t, s);
+        if (st != KS_OK) return rollback(st);
+      }
+      cudaError_t e = cudaEventRecord(pool->fence, s);
+      if (e != cudaSuccess) return rollback(cuda_fail(e, "fence record"));
+      pool->fence_stream = s;
+      pool->fence_pending = true;
+    }
+    if (n_moves) *n_moves = static_cast<uint32_t>(mv.size());
+    if (slabs_freed) *slabs_freed = freed;
     return KS_OK;
   });
 }

@@ -32,6 +32,7 @@
 
 #include "attend.cuh"
 #include "kvslab_device.cuh"
+#include "func_cache.hpp"
 #include "launch.hpp"
 
 namespace kvslab {
@@ -109,7 +110,7 @@ template <int DC>  // dims split over DC CTAs per (sequence, head) (small batche
 __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, uint32_t grid) {
   constexpr int VW = 4 / DC;  // floats per lane
   pdl_launch_dependents();
-  const uint64_t tm0 = p.trace ? gtimer() : 0;
+  const uint64_t tm0 = (kProbes && p.trace) ? gtimer() : 0;
   extern __shared__ float4 msm[];  // WS > 1: o[G*WS][32], then m[G*WS], l[G*WS]
   __shared__ uint32_t red[2][32];
   const uint32_t unit = blockIdx.x / DC, dc = blockIdx.x % DC;
@@ -163,7 +164,7 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, 
   // and the first segment of every later CTA
   const uint32_t slot_a = cta_start(ca, sp) < U0 ? 1u : 0u;
   pdl_wait();  // partials come from the decode kernel
-  if (p.trace && threadIdx.x == 0) {  // probes: [2048] first merge CTA past the wait
+  if (kProbes && p.trace && threadIdx.x == 0) {  // probes: [2048] first merge CTA past the wait
     const uint64_t tw = gtimer();
     atomicMin(p.trace + 2048, static_cast<unsigned long long>(tw));
     p.trace[2050 + 3 * blockIdx.x] = tm0;
@@ -260,7 +261,7 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, 
   }
   if (p.lse && lane == 0 && dc == 0)
     p.lse[static_cast<uint64_t>(s) * Hq + h * G + q] = (M + __log2f(L)) * 0.69314718055994531f;
-  if (p.trace && lane == 0) {
+  if (kProbes && p.trace && lane == 0) {
     const uint64_t te = gtimer();
     atomicMax(p.trace + 2049, static_cast<unsigned long long>(te));
     p.trace[2052 + 3 * blockIdx.x] = te;
@@ -274,7 +275,7 @@ constexpr uint32_t kTrStage = 12288, kTrReady = kTrStage + 148 * 4 * 32;
 // per-block checks cost the consumer loop ~1 % even when p.trace is null.
 __device__ __forceinline__ void trace_ready(const DecodeParams& p, int warp, int lane, uint32_t k) {
 #ifdef KVSLAB_STAGE_PROBES
-  if (p.trace && warp == 0 && lane == 0 && k < 32) p.trace[kTrReady + blockIdx.x * 32 + k] = gtimer();
+  if (kProbes && p.trace && warp == 0 && lane == 0 && k < 32) p.trace[kTrReady + blockIdx.x * 32 + k] = gtimer();
 #else
   (void)p, (void)warp, (void)lane, (void)k;
 #endif
@@ -311,7 +312,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
   // PDL-enabled predecessor writes (ctx_lens, block tables, KV of other
   // layers); Q, new K/V, outputs and the workspace come after the wait.
   pdl_launch_dependents();
-  const uint64_t t0 = p.trace ? gtimer() : 0;
+  const uint64_t t0 = (kProbes && p.trace) ? gtimer() : 0;
 
   // ---- per-CTA prefix of blocks over sequences (x NG head groups) ----
   uint32_t* pre = reinterpret_cast<uint32_t*>(smem + p.prefix_offset);
@@ -407,7 +408,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
   uint8_t* ring = smem;
   uint8_t* qbuf = smem + p.qbuf_offset;
 
-  const bool compute_only = (p.debug & 4) != 0;  // probe: no copies; consumers reuse stage data
+  const bool compute_only = kProbes && (p.debug & 4) != 0;  // probe: no copies; consumers reuse stage data
   if (warp == static_cast<int>(HG)) {
     if (compute_only) return;
     // ============================ producer warp ============================
@@ -447,7 +448,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     uint64_t t_first = 0;
     const uint32_t ring_u = smem_u32(ring);
     for (uint32_t k = 0; k < n; ++k) {
-      if (k == 1 && p.trace) t_first = gtimer();
+      if (kProbes && k == 1 && p.trace) t_first = gtimer();
       if ((k & 31) == 0 && k > 0 && k + 32 < n) {
         if ((k >> 5) & 1) win0 = load_window(k + 32);
         else win1 = load_window(k + 32);
@@ -461,7 +462,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       const uint32_t g0 = gw & 0x7fffffffu;
       mbar_wait(&empty[st], ph ^ 1);
 #ifdef KVSLAB_STAGE_PROBES
-      if (p.trace && lane == 0 && k < 32) p.trace[kTrStage + blockIdx.x * 32 + k] = gtimer();
+      if (kProbes && p.trace && lane == 0 && k < 32) p.trace[kTrStage + blockIdx.x * 32 + k] = gtimer();
 #endif
       if (lane == 0) {
         const uint32_t sb = ring_u + st * p.stage_bytes;
@@ -506,7 +507,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         ph ^= 1;
       }
     }
-    if (p.trace && lane == 0) {
+    if (kProbes && p.trace && lane == 0) {
       unsigned long long* tr = p.trace + static_cast<uint64_t>(blockIdx.x) * 8;
       tr[0] = t0;
       tr[1] = t_first;
@@ -545,7 +546,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       sb = ring_u32;
     }
   };
-  if (p.trace && warp == 0 && lane == 0) p.trace[blockIdx.x * 8 + 4] = gtimer();
+  if (kProbes && p.trace && warp == 0 && lane == 0) p.trace[blockIdx.x * 8 + 4] = gtimer();
   const long long c_loop0 = clock64();
 
   for (uint32_t k = 0; k < n;) {
@@ -648,7 +649,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       } else {
         const uint32_t sbs[1] = {sb};
         const int valid[1] = {kTPB};
-        if (!(p.debug & 8))  // probe: stream only
+        if (!kProbes || !(p.debug & 8))  // probe: stream only
           attend<FMT, NT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
       }
       release();
@@ -762,7 +763,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     }
     cursor_next(cc, pre, p.batch, NG);
   }
-  if (p.trace && warp == 0 && lane == 0) {
+  if (kProbes && p.trace && warp == 0 && lane == 0) {
     p.trace[blockIdx.x * 8 + 5] = gtimer();
     p.trace[blockIdx.x * 8 + 6] = static_cast<unsigned long long>(clock64() - c_loop0);
     p.trace[blockIdx.x * 8 + 7] = n;
@@ -795,12 +796,11 @@ static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t 
   p.prefix_offset = p.bar_offset + (2 * stages + 4) * 8 + stages * 8;  // + stage block addresses
   const size_t smem = p.prefix_offset + (p.batch + 1) * 4;
   auto kern = paged_decode_kernel<FMT, NT, PK>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int threads = static_cast<int>((hg + 1) * 32);
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  e = cached_occupancy(reinterpret_cast<const void*>(kern), threads, smem, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   if (per_sm > 4) per_sm = 4;  // workspace partials are sized for <= 4 CTAs per SM

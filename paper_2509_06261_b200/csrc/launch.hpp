@@ -12,6 +12,35 @@ namespace kvslab {
 
 constexpr int kDecodeWarps = 4;
 
+// Probe builds (-DKVSLAB_PROBES) compile the per-warp timestamp hooks into
+// the decode kernels; release builds compile them out.
+#ifdef KVSLAB_PROBES
+constexpr bool kProbes = true;
+#else
+constexpr bool kProbes = false;
+#endif
+
+// Tuning overrides for experiments (scripts/ab_decode.py and friends).  Read
+// from KVSLAB_* environment variables once, when a pool is created -- never
+// on the launch path.  Zero / -1 = the library's default.
+struct Tuning {
+  int decode_max_ctas = 0;         // KVSLAB_DECODE_MAX_CTAS
+  uint32_t decode_hg = 0;          // KVSLAB_DECODE_HG
+  uint32_t decode_smem = 0;        // KVSLAB_DECODE_SMEM
+  uint32_t merge_threads = 0;      // KVSLAB_MERGE_THREADS
+  uint32_t merge_dc = 0;           // KVSLAB_MERGE_DC
+  uint32_t decode_pack = 0;        // KVSLAB_DECODE_PACK
+  int decode_debug = 0;            // KVSLAB_DECODE_DEBUG (probe builds only)
+  unsigned long long* decode_trace = nullptr;  // KVSLAB_DECODE_TRACE (probe builds only)
+  int pdl = 1;                     // KVSLAB_NO_PDL=1 -> 0
+  uint32_t prefill_nt = 0;         // KVSLAB_PREFILL_NT
+  int prefill_tc = 2;              // KVSLAB_PREFILL_TC
+  int prefill_debug = 0;           // KVSLAB_PREFILL_DEBUG (probe builds only)
+  int prefill_expand = -1;         // KVSLAB_PREFILL_EXPAND (-1 auto)
+  int prefill_split = 1;           // KVSLAB_PREFILL_SPLIT
+  static Tuning from_env();
+};
+
 struct DecodeParams {
   const uint8_t* pool;
   dev::SlabGeom geom;

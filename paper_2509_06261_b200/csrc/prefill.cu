@@ -21,6 +21,7 @@
 
 #include "attend.cuh"
 #include "kvslab_device.cuh"
+#include "func_cache.hpp"
 #include "launch.hpp"
 
 namespace kvslab {
@@ -273,8 +274,7 @@ static cudaError_t launch_prefill_fmt(const PrefillParams& p0, cudaStream_t stre
   p.bar_offset = p.qbuf_offset + qbytes;
   const size_t smem = p.bar_offset + 2 * stages * 8;
   auto kern = prefill_kernel<FMT, NT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const uint32_t qt = W * (8 * NT / p.G);  // tokens per tile
   p.tiles = (p.max_q_len + qt - 1) / qt;

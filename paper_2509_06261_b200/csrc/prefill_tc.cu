@@ -21,6 +21,7 @@
 
 #include "attend.cuh"
 #include "kvslab_device.cuh"
+#include "func_cache.hpp"
 #include "launch.hpp"
 
 namespace kvslab {
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
         const uint8_t* raw = smem + Cfg::kRaw + rs * Cfg::kRawBytes;
         uint8_t* kt = smem + k2KV + st * 2 * kKVBytes;
 #pragma unroll 4
-        for (uint32_t i = lt; i < ((p.debug & 4) ? 0u : kGran); i += kLoaders) {
+        for (uint32_t i = lt; i < ((kProbes && (p.debug & 4)) ? 0u : kGran); i += kLoaders) {
           const uint32_t kv = i / (4 * kC / 16), rem = i % (4 * kC / 16);
           const uint32_t bi = rem / (kC / 16), gi = rem % (kC / 16);  // physical granule of the chunk
           const uint32_t off = gi * 16, line = off >> 7;
@@ -545,7 +546,7 @@ __global__ void __launch_bounds__(kThreadsOf<FMT, EXP>, 1) prefill_tc2_kernel(co
       tc_fence_after();
       float sc[kTile];
       tmem_ld64_to(tS + (t & 1) * kTile, sc);
-      if (p.debug & 2) {
+      if (kProbes && (p.debug & 2)) {
 #pragma unroll
         for (int j = 0; j < static_cast<int>(kTile); ++j) sc[j] = 0.f;
       }
@@ -839,7 +840,7 @@ static cudaError_t launch_tc(const PrefillParams& p0, cudaStream_t stream, bool 
   const size_t smem = TcCfg<FMT, EXP>::kSmem + 1024;  // + alignment slack
   const uint32_t nsplit = p.kv_splits > 1 ? p.kv_splits : 1;
   auto kern = nsplit > 1 ? prefill_tc2_kernel<FMT, EXP, true> : prefill_tc2_kernel<FMT, EXP, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.batch * p.H, p.tiles, nsplit);

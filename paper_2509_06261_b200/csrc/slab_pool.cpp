@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <bit>
 #include <numeric>
+#include <set>
 
 namespace kvslab {
 
@@ -439,33 +440,34 @@ std::vector<BlockMove> SlabPool::plan_compaction(Bytes key, std::uint64_t max_mo
   std::sort(cand.begin(), cand.end(), [&](std::uint32_t a, std::uint32_t b) {
     return used_[a] != used_[b] ? used_[a] < used_[b] : a > b;
   });
-  std::vector<std::uint8_t> evac(nslabs_, 0), recv(nslabs_, 0);
-  // every slab formatted to the key (PARTIAL or FULL) is a potential target
-  std::vector<std::uint32_t> keyed;
+  // Targets: every slab of the key (PARTIAL or FULL) that is not evacuated.
+  // A move keeps the key's free-block count (dst -1, src +1), so the room
+  // available to a source is the running total minus the source's own free
+  // blocks; evacuating a (then empty) source removes its blocks.  Open
+  // targets sit in an ordered set by (used desc, id asc): the fill order of
+  // a fresh fullest-first sort, kept current move by move in O(log n).
+  std::uint64_t room = 0;
+  std::set<std::pair<std::int64_t, std::uint32_t>> open;
   for (std::uint32_t s = 0; s < nslabs_; ++s) {
-    if (kidx_[s] == k + 1) keyed.push_back(s);
+    if (kidx_[s] != k + 1) continue;
+    room += total_[s] - used_[s];
+    if (used_[s] < total_[s]) open.insert({-std::int64_t{used_[s]}, s});
   }
+  std::vector<std::uint8_t> recv(nslabs_, 0);
   for (std::uint32_t S : cand) {
     if (recv[S] || kidx_[S] != k + 1) continue;
     const std::uint32_t need = used_[S];
-    std::vector<std::uint32_t> dst;
-    std::uint64_t cap = 0;
-    for (std::uint32_t d : keyed) {
-      if (d == S || evac[d] || kidx_[d] != k + 1) continue;
-      cap += total_[d] - used_[d];
-      if (used_[d] < total_[d]) dst.push_back(d);
-    }
-    if (cap < need || moves.size() + need > max_moves) break;
-    std::stable_sort(dst.begin(), dst.end(), [&](std::uint32_t a, std::uint32_t b) {
-      return used_[a] != used_[b] ? used_[a] > used_[b] : a < b;
-    });
-    std::size_t di = 0;
+    const std::uint64_t own = total_[S] - used_[S];
+    if (room - own < need || moves.size() + need > max_moves) break;
+    open.erase({-std::int64_t{used_[S]}, S});
     const std::uint32_t bps = total_[S];
     for (std::uint32_t l = 0; l < bps && used_[S] > 0; ++l) {
       if (!((occ(S)[l / 64] >> (l % 64)) & 1u)) continue;
-      while (used_[dst[di]] == total_[dst[di]]) ++di;
-      const std::uint32_t D = dst[di];
+      const auto top = open.begin();
+      const std::uint32_t D = top->second;
+      open.erase(top);
       const std::uint32_t dl = take_first_free(D);
+      if (used_[D] < total_[D]) open.insert({-std::int64_t{used_[D]}, D});
       stats_.allocated_bytes += key;
       stats_.free_block_bytes -= key;
       ++allocated_blocks_;
@@ -483,8 +485,8 @@ std::vector<BlockMove> SlabPool::plan_compaction(Bytes key, std::uint64_t max_mo
       log_op("free", m.src);
       moves.push_back(m);
     }
+    room -= total_[S];
     unformat_slab(S);
-    evac[S] = 1;
     ++freed;
   }
   if (slabs_freed) *slabs_freed = freed;

@@ -12,6 +12,7 @@ import dataclasses
 import enum
 import math
 import os
+import weakref
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -197,19 +198,42 @@ def kv_append(pool: SlabPool, fmt: KvFormat, layer: int, k: torch.Tensor, v: tor
 
 
 class DecodeWorkspace:
-    """Zero-initialised K2 scratch (partials + per-unit counters), reusable."""
+    """K2 scratch (fp32 partials of sequence-heads split across CTAs).  Needs
+    no initialisation; concurrent launches need distinct workspaces."""
 
-    def __init__(self, pool: SlabPool, fmt: KvFormat, max_batch: int):
+    def __init__(self, pool: SlabPool, fmt: KvFormat, max_batch: int, stream=None):
         f = fmt.to_c()
         n = C.c_size_t()
         check(L.lib.ks_paged_decode_workspace_size(pool.handle, C.byref(f), max_batch,
                                                    C.byref(n)))
         self.nbytes = n.value
         self.max_batch = max_batch
-        self.buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=f"cuda:{pool.device}")
+        # allocated on the stream it is used on, so the caching allocator
+        # orders its reuse after the kernels of that stream
+        with torch.cuda.stream(_torch_stream(stream, pool.device)):
+            self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=f"cuda:{pool.device}")
 
 
-_WS: Dict[Tuple[int, int, int], DecodeWorkspace] = {}
+def _torch_stream(stream, device) -> torch.cuda.Stream:
+    if stream is None:
+        return torch.cuda.current_stream(device)
+    if isinstance(stream, torch.cuda.Stream):
+        return stream
+    return torch.cuda.ExternalStream(int(stream), device=f"cuda:{device}")
+
+
+# Default scratch, per pool (weakly: a dropped pool drops its buffers) and per
+# (format group, stream): co-located models or streams never share a buffer.
+_WS: "weakref.WeakKeyDictionary[SlabPool, Dict[Tuple[int, int], DecodeWorkspace]]" = weakref.WeakKeyDictionary()
+
+
+def _default_decode_ws(pool: SlabPool, fmt: KvFormat, B: int, stream) -> DecodeWorkspace:
+    per = _WS.setdefault(pool, {})
+    k = (fmt.key, _stream(stream))
+    ws = per.get(k)
+    if ws is None or ws.max_batch < B:
+        ws = per[k] = DecodeWorkspace(pool, fmt, B, stream)
+    return ws
 
 
 def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
@@ -231,10 +255,7 @@ def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
-        k = (id(pool), fmt.group, B)
-        workspace = _WS.get(k)
-        if workspace is None or workspace.max_batch < B:
-            workspace = _WS[k] = DecodeWorkspace(pool, fmt, B)
+        workspace = _default_decode_ws(pool, fmt, B, stream)
     f = fmt.to_c()
     scale = 0.0 if sm_scale is None else float(sm_scale)
     if k_new is None:
@@ -252,18 +273,20 @@ def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
     return out
 
 
-_PF_WS: Dict[int, torch.Tensor] = {}
+_PF_WS: "weakref.WeakKeyDictionary[SlabPool, Dict[int, torch.Tensor]]" = weakref.WeakKeyDictionary()
 
 
 PREFILL_WS_CAP = int(os.environ.get("KVSLAB_PREFILL_WS_CAP", 1 << 30))
 
 
 def prefill_workspace(pool: SlabPool, fmt: KvFormat, batch: int, bt_stride: int,
-                      max_q_len: int) -> Optional[torch.Tensor]:
+                      max_q_len: int, stream=None) -> Optional[torch.Tensor]:
     """K4 workspace (split-KV partials + the quantised formats' expand
-    scratch; None when neither applies): one per-device buffer, grown on
-    demand up to PREFILL_WS_CAP bytes (beyond, the C side drops the split and
-    takes the expand in sequence groups) and reused by every call."""
+    scratch; None when neither applies): one buffer per (pool, stream), grown
+    on demand up to PREFILL_WS_CAP bytes (beyond, the C side drops the split
+    and takes the expand in sequence groups) and reused by every call on that
+    stream.  A grown buffer replaces the old one through the caching
+    allocator, which orders the old one's reuse after that stream's kernels."""
     f = fmt.to_c()
     n, one = C.c_size_t(), C.c_size_t()
     check(L.lib.ks_paged_prefill_workspace_size(C.byref(f), batch, bt_stride, max_q_len, C.byref(n)))
@@ -271,10 +294,13 @@ def prefill_workspace(pool: SlabPool, fmt: KvFormat, batch: int, bt_stride: int,
     if n.value == 0:
         return None
     want = max(min(n.value, PREFILL_WS_CAP), one.value)
-    buf = _PF_WS.get(pool.device)
+    per = _PF_WS.setdefault(pool, {})
+    sk = _stream(stream)
+    buf = per.get(sk)
     if buf is None or buf.numel() < want:
-        buf = torch.empty(want, dtype=torch.uint8, device=f"cuda:{pool.device}")
-        _PF_WS[pool.device] = buf
+        with torch.cuda.stream(_torch_stream(stream, pool.device)):
+            buf = torch.empty(want, dtype=torch.uint8, device=f"cuda:{pool.device}")
+        per[sk] = buf
     return buf
 
 
@@ -301,7 +327,8 @@ def paged_prefill(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
     f = fmt.to_c()
     scale = 0.0 if sm_scale is None else float(sm_scale)
     if isinstance(workspace, str):
-        workspace = prefill_workspace(pool, fmt, ctx_lens.shape[0], block_table.stride(0), int(max_q_len))
+        workspace = prefill_workspace(pool, fmt, ctx_lens.shape[0], block_table.stride(0), int(max_q_len),
+                                      stream)
     ws_bytes = 0 if workspace is None else workspace.numel()
     check(L.lib.ks_paged_prefill_ws(pool.handle, C.byref(f), layer, _ptr(q), _ptr(out), _ptr(lse),
                                     _ptr(block_table), block_table.stride(0), _ptr(cu_q),
@@ -310,10 +337,22 @@ def paged_prefill(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
     return out
 
 
+def compact_key(pool: SlabPool, key: int, max_moves: int = 1 << 30, stream=None) -> Tuple[int, int]:
+    """K3 as one transaction (ks_compact): plan, move the bytes on the GPU and
+    rewrite every registered engine table of `key` (engine.SlabModel).
+    Returns (moves, slabs_freed)."""
+    n, freed = C.c_uint32(), C.c_uint32()
+    check(L.lib.ks_compact(pool.handle, key, min(int(max_moves), 0xFFFFFFFF), _stream(stream),
+                           C.byref(n), C.byref(freed)))
+    return n.value, freed.value
+
+
 def compact(pool: SlabPool, key: int, max_moves: int = 1 << 20,
             tables: Sequence[torch.Tensor] = (), stream=None) -> Tuple[List[Tuple[int, int]], int]:
-    """K3: plan (host, applied to the slab table), move the bytes on the GPU,
-    and remap the given device block tables.  Returns (moves, slabs_freed)."""
+    """K3 for engine-owned raw tables: plan (host, applied to the slab
+    table), move the bytes on the GPU, and remap the given device block
+    tables.  Returns (moves, slabs_freed).  Registered tables (SlabModel) use
+    compact_key, which also rolls back on failure."""
     moves, freed = pool.plan_compaction(key, max_moves)
     if moves:
         buf = (L.ks_block_move * len(moves))(*[L.ks_block_move(s, d) for s, d in moves])

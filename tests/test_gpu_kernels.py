@@ -397,3 +397,87 @@ def test_decode_mostly_empty_slots(dt):
     assert rel_err(o[live], ref[live]) <= TOL[dt]
     assert (o[~live] == 0).all()
     assert np.isneginf(lse.cpu().numpy()[~live]).all()
+
+
+def test_compact_key_remaps_every_owner_of_the_key():
+    """Two co-located models with the same KvFormat share one slab key
+    (ADVICE r1): ks_compact rewrites both models' handles and device tables,
+    the moved bytes decode identically, and the table validator passes."""
+    from paper_2509_06261_b200.engine import SlabModel
+    fmt = KvFormat(KvDtype.FP8_E4M3, 8, 32, num_layers=2)
+    slab = fmt.key * 8
+    pool = ks.SlabPool(ks.SlabPoolConfig(64 * slab, slab, [fmt.key]), device=0)
+    kv.kv_tensor(pool).zero_()
+    rng = np.random.default_rng(5)
+    a, b = SlabModel(pool, fmt, 16, 40), SlabModel(pool, fmt, 16, 40)
+    # interleaved claims so every slab holds both models' blocks
+    for step in range(12):
+        for m in (a, b):
+            for s in range(16):
+                if step == 0:
+                    assert m.admit(s, 16)
+                elif len(m.handles[s]) < 12:
+                    m.cached[s] = (len(m.handles[s])) * 16
+                    assert m.ensure_capacity(s, m.cached[s] + 1)
+    for m in (a, b):
+        for s in range(16):
+            m.cached[s] = len(m.handles[s]) * 16 - int(rng.integers(0, 16))
+        m.sync()
+    sc = dev(np.full(16, 0.5, np.float32))
+    outs = []
+    for m in (a, b):
+        ctx = torch.tensor(m.ctx_lens(), dtype=torch.int32, device="cuda")
+        T = int(ctx.sum())
+        seqs = torch.repeat_interleave(torch.arange(16, dtype=torch.int32, device="cuda"), ctx)
+        pos = torch.cat([torch.arange(int(c), dtype=torch.int32, device="cuda") for c in ctx])
+        k = torch.randn(T, 8, 128, dtype=torch.float16, device="cuda")
+        kv.kv_append(pool, fmt, 1, k, -k, seqs, pos, m.table, sc)
+        q = torch.randn(16, 32, 128, dtype=torch.float16, device="cuda")
+        outs.append((q, ctx))
+    # release most sequences of both models: holes everywhere
+    for m in (a, b):
+        for s in range(16):
+            if s % 4:
+                m.release(s)
+    live = [s for s in range(16) if s % 4 == 0]
+    ref = []
+    for m, (q, ctx) in zip((a, b), outs):
+        c = torch.tensor(m.ctx_lens(), dtype=torch.int32, device="cuda")
+        ref.append(kv.paged_decode(pool, fmt, 1, q, m.table, c, kv_scales=sc).clone())
+    st0 = pool.snapshot_stats()
+    n, freed = a.compact()
+    torch.cuda.synchronize()
+    assert n > 0 and freed > 0
+    assert pool.check_integrity()[0]
+    assert pool.snapshot_stats().allocated_bytes == st0.allocated_bytes
+    kv.slab_table_sync(pool)
+    for i, (m, (q, ctx)) in enumerate(zip((a, b), outs)):
+        host = m.table.cpu().numpy()
+        for s in live:
+            assert [h.global_block_id for h in m.handles[s]] == host[s, :len(m.handles[s])].tolist()
+        c = torch.tensor(m.ctx_lens(), dtype=torch.int32, device="cuda")
+        assert kv.block_table_validate(pool, fmt.key, m.table, c) == 0
+        got = kv.paged_decode(pool, fmt, 1, q, m.table, c, kv_scales=sc)
+        torch.cuda.synchronize()
+        assert torch.equal(got[live], ref[i][live])
+    for m in (a, b):  # every handle is still freeable exactly once
+        for s in live:
+            m.release(s)
+    assert pool.allocated_block_count() == 0 and pool.check_integrity()[0]
+
+
+def test_block_table_remap_beyond_one_staging_slot():
+    """More moves than one staging slot holds (65,536): the remap is chunked."""
+    fmt = KvFormat(KvDtype.INT4, 8, 8)
+    pool = ks.SlabPool(ks.SlabPoolConfig(8 * fmt.key * 64, fmt.key * 64, [fmt.key]), device=0)
+    n = 70000
+    src = np.arange(n, dtype=np.int64) * 2 + 1
+    dst = src - 1
+    table = torch.from_numpy(np.concatenate([src, dst, [7, 10**6]]).astype(np.int32)).cuda()
+    moves = (ks._lib.ks_block_move * n)(*[ks._lib.ks_block_move(int(s), int(d)) for s, d in zip(src, dst)])
+    ks.slab_pool.check(ks._lib.lib.ks_block_table_remap(pool.handle, table.data_ptr(), table.numel(),
+                                                        moves, n, None))
+    torch.cuda.synchronize()
+    got = table.cpu().numpy()
+    assert (got[:n] == dst).all() and (got[n:2 * n] == dst).all()
+    assert got[-2] == 6 and got[-1] == 10**6
