@@ -899,6 +899,7 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
     nbytes = tokens = h2d = d2h = 0
     n0 = kv.launch_count()
     graph_launches = 0
+    marks = []
     clk = Clocks(clocks_index) if clocks_index is not None else None
     if clk:
         clk.__enter__()
@@ -923,9 +924,13 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
                 e2e["src_dev"][:, :T].copy_(e2e["src_host"][:, :T], non_blocking=True)
                 h2d += 2 * T * grp.hkv * D * 2
                 return e2e["src_dev"]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(main)
         if B != grp.B:
             k1, k3 = grp.rebalance(B, src_fn)
             nbytes += k1 + k3
+        ev[1].record(main)
+        marks.append((B, ev))
         nbytes += grp.host_step()
         tokens += len(grp.models) * B
         if eager:
@@ -933,6 +938,7 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
         else:
             grp.graph(B, X if e2e else 0).replay()
             graph_launches += grp.n_launch_graph[(B, X if e2e else 0)]
+        ev[2].record(main)
         if e2e:
             done = torch.cuda.Event()
             done.record(main)
@@ -949,6 +955,12 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
         clk.__exit__()
     ms = e0.elapsed_time(e1)
     launches = kv.launch_count() - n0 + graph_launches
+    # device-time breakdown: phase changes (admission K1, compaction) vs steps per batch size
+    bd = {"phase_change_ms": round(sum(e[0].elapsed_time(e[1]) for _, e in marks), 3)}
+    for b in sorted({b for b, _ in marks}):
+        t = [e[1].elapsed_time(e[2]) for bb, e in marks if bb == b]
+        bd[f"step_ms_B{b}"] = round(float(np.mean(t)), 4)
+    time_steps.breakdown = bd
     return ms, nbytes, tokens, launches, h2d, d2h, (clk.summary() if clk else None)
 
 
@@ -1037,10 +1049,13 @@ def measure(name, dev, clocks_index, with_e2e=True, tune=True):
     st0 = len(grp.stranded_trace)
     ms, nbytes, tokens, launches, _, _, clk = time_steps(grp, timed, clocks_index=clocks_index)
     res = dict(ms=ms, bytes=nbytes, tokens=tokens, launches=launches, clocks=clk, shares=shares,
+               breakdown=time_steps.breakdown,
                compactions=grp.compactions - c0, moves=grp.moves - m0, slabs_freed=grp.slabs_freed - s0,
                stranded=grp.stranded_trace[st0:], frag=grp.frag_trace[st0:], B=timed)
     if with_e2e:
         e2e = make_e2e(grp)
+        for B in set(e2e_targets):  # pinned host buffers before the timed region
+            e2e["host"](B)
         r = time_steps(grp, e2e_targets, e2e=e2e)
         res["e2e"] = dict(ms=r[0], bytes=r[1], h2d=r[4] / len(e2e_targets), d2h=r[5] / len(e2e_targets))
         r = time_steps(grp, e2e_targets, e2e=e2e, eager=True)
@@ -1088,6 +1103,7 @@ def summarise(name, r, peak, peak_kind, world):
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "frac_of_8TBps": round(achieved / 8000.0, 4)},
         "kernels": kernels,
+        "breakdown": r.get("breakdown"),
         "sm_share": r["shares"],
         "gpu_launches": int(r["launches"]),
     }

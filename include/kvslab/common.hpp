@@ -1,43 +1,31 @@
 // kvslab/common.hpp -- value types, error classes and KV geometry.
 //
-// Error classes carry the reference's names (proj/core/include/slabsim/
-// common.hpp:31-59) so code written against slabsim keeps its catch
-// clauses; the C ABI maps them 1:1 onto ks_status codes.
+// The error classes are the reference's own hierarchy (proj/core/include/
+// slabsim/common.hpp:31-95, restated in this repo's slabsim/common.hpp), so
+// code written against slabsim keeps its catch clauses; the C ABI maps them
+// 1:1 onto ks_status codes.
 #pragma once
 
 #include <cstdint>
 #include <stdexcept>
 #include <string>
 
+#include "slabsim/common.hpp"
+
 namespace kvslab {
 
-using Bytes = std::uint64_t;
-using Tokens = std::uint64_t;
-
-class Error : public std::runtime_error {
- public:
-  using std::runtime_error::runtime_error;
-};
-class InvalidProfileError : public Error {
- public:
-  using Error::Error;
-};
-class InvalidConfigError : public Error {
- public:
-  using Error::Error;
-};
-class InvalidKeyError : public Error {
- public:
-  using Error::Error;
-};
-class InvalidFreeError : public Error {
- public:
-  using Error::Error;
-};
-class PoolExhaustedError : public Error {
- public:
-  using Error::Error;
-};
+// The value types and the exception hierarchy ARE slabsim's (one set of
+// classes, declared in slabsim/common.hpp): code written against the
+// reference catches exactly what this library throws.
+using slabsim::Bytes;
+using slabsim::Error;
+using slabsim::InvalidConfigError;
+using slabsim::InvalidFreeError;
+using slabsim::InvalidKeyError;
+using slabsim::InvalidProfileError;
+using slabsim::PoolExhaustedError;
+using slabsim::Seconds;
+using slabsim::Tokens;
 
 // The geometry subset of slabsim::ModelProfile that token_size and
 // kv_block_size read (precision.hpp:168-176).

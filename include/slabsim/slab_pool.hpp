@@ -1,13 +1,23 @@
-// slabsim/slab_pool.hpp -- drop-in shim: code written against the reference
-// allocator (proj/core/include/slabsim/slab_pool.hpp) compiles unchanged
-// against libkvslab.so by putting this repo's include/ first on the path.
-// slabsim::SlabPool, SlabPoolConfig, BlockHandle, FragmentationStats,
-// OpLogRecord, SlabState, write_op_log_line and the exception classes resolve
-// to the kvslab implementations (same signatures and semantics).
+// slabsim/slab_pool.hpp -- drop-in replacement for the reference allocator
+// header (proj/core/include/slabsim/slab_pool.hpp:26-202).
+//
+// With this repository's include/ first on the include path, code written
+// against slabsim::SlabPool compiles unchanged and links against
+// libkvslab.so: the names below resolve to the kvslab implementations, which
+// keep the reference's signatures and observable semantics (pinned by
+// tests/test_slab_pool_parity.py and, for the reference's own acceptance
+// suite, tests/test_dropin.py).
 #pragma once
 
 #include "kvslab/slab_pool.hpp"
+#include "slabsim/common.hpp"
 
 namespace slabsim {
-using namespace kvslab;  // NOLINT: deliberate alias of the whole API
+using kvslab::BlockHandle;
+using kvslab::FragmentationStats;
+using kvslab::OpLogRecord;
+using kvslab::SlabPool;
+using kvslab::SlabPoolConfig;
+using kvslab::SlabState;
+using kvslab::write_op_log_line;
 }  // namespace slabsim

@@ -12,7 +12,6 @@ import dataclasses
 import enum
 import math
 import os
-import weakref
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -222,13 +221,17 @@ def _torch_stream(stream, device) -> torch.cuda.Stream:
     return torch.cuda.ExternalStream(int(stream), device=f"cuda:{device}")
 
 
-# Default scratch, per pool (weakly: a dropped pool drops its buffers) and per
-# (format group, stream): co-located models or streams never share a buffer.
-_WS: "weakref.WeakKeyDictionary[SlabPool, Dict[Tuple[int, int], DecodeWorkspace]]" = weakref.WeakKeyDictionary()
+# Default scratch lives on the pool object (dropped with it), per (slab key,
+# stream): co-located models or streams never share a buffer.
+def _pool_cache(pool: SlabPool, name: str) -> dict:
+    d = pool.__dict__.get(name)
+    if d is None:
+        d = pool.__dict__[name] = {}
+    return d
 
 
 def _default_decode_ws(pool: SlabPool, fmt: KvFormat, B: int, stream) -> DecodeWorkspace:
-    per = _WS.setdefault(pool, {})
+    per = _pool_cache(pool, "_ks_decode_ws")
     k = (fmt.key, _stream(stream))
     ws = per.get(k)
     if ws is None or ws.max_batch < B:
@@ -273,9 +276,6 @@ def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
     return out
 
 
-_PF_WS: "weakref.WeakKeyDictionary[SlabPool, Dict[int, torch.Tensor]]" = weakref.WeakKeyDictionary()
-
-
 PREFILL_WS_CAP = int(os.environ.get("KVSLAB_PREFILL_WS_CAP", 1 << 30))
 
 
@@ -294,7 +294,7 @@ def prefill_workspace(pool: SlabPool, fmt: KvFormat, batch: int, bt_stride: int,
     if n.value == 0:
         return None
     want = max(min(n.value, PREFILL_WS_CAP), one.value)
-    per = _PF_WS.setdefault(pool, {})
+    per = _pool_cache(pool, "_ks_prefill_ws")
     sk = _stream(stream)
     buf = per.get(sk)
     if buf is None or buf.numel() < want:
