@@ -639,6 +639,7 @@ class Group:
             self.src = torch.randn(2, max_prompt_tokens, hkv, D, dtype=torch.float16, device=dev)
         self.compactions, self.moves, self.slabs_freed = 0, 0, 0
         self.stranded_trace, self.frag_trace = [], []
+        self.reb_marks = []  # (K1 bytes, K3 bytes, events) per phase change
 
     # ---- step buffers ----
     def buffers(self, B):
@@ -768,6 +769,9 @@ class Group:
         k1 = k3 = 0
         if target == self.B:
             return 0, 0
+        main = self.torch.cuda.current_stream(self.dev)
+        ev = [self.torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(main)
         for mi, m in enumerate(self.models):
             if target < self.B:
                 keep = sorted(self.rng.choice(self.B, size=target, replace=False).tolist())
@@ -781,9 +785,9 @@ class Group:
                 prompts = self.rng.integers(512, 2049, size=len(rows)).tolist()
                 k1 += self.admit_rows(mi, rows, prompts, src_fn)
         self.B = target
-        main = self.torch.cuda.current_stream(self.dev)
         for m in self.models:
             m.sync(main)
+        ev[1].record(main)
         strd = self.stranded()
         self.stranded_trace.append(round(strd, 3))
         if strd > C4_TRIGGER:
@@ -793,6 +797,8 @@ class Group:
                 self.slabs_freed += fr
                 k3 += 2 * n * m.key
             self.compactions += 1
+        ev[2].record(main)
+        self.reb_marks.append((k1, k3, ev))
         self.frag_trace.append(sum(m.internal_frag_bytes() for m in self.models))
         self.set_ctx()
         return k1, k3
@@ -957,6 +963,16 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
     launches = kv.launch_count() - n0 + graph_launches
     # device-time breakdown: phase changes (admission K1, compaction) vs steps per batch size
     bd = {"phase_change_ms": round(sum(e[0].elapsed_time(e[1]) for _, e in marks), 3)}
+    reb = [m for m in grp.reb_marks if m[2][0].query()]
+    grp.reb_marks = []
+    if reb:
+        adm = sum(e[0].elapsed_time(e[1]) for _, _, e in reb)
+        cmp_ = sum(e[1].elapsed_time(e[2]) for _, _, e in reb)
+        bd["admission_ms"] = round(adm, 3)
+        bd["admission_k1_gbs"] = round(sum(k for k, _, _ in reb) / max(adm, 1e-9) / 1e6, 1)
+        bd["compaction_ms"] = round(cmp_, 3)
+        k3b = sum(k for _, k, _ in reb)
+        bd["compaction_gbs"] = round(k3b / max(cmp_, 1e-9) / 1e6, 1) if k3b else None
     for b in sorted({b for b, _ in marks}):
         t = [e[1].elapsed_time(e[2]) for bb, e in marks if bb == b]
         bd[f"step_ms_B{b}"] = round(float(np.mean(t)), 4)
