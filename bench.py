@@ -925,9 +925,13 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
                 h2d += bs["inbuf"].numel() * 2
             main.wait_stream(up)
 
-            def src_fn(T):  # admitted prompts' K/V come from the host too
+            def src_fn(T):  # admitted prompts' K/V come from the host too (copy stream)
                 nonlocal h2d
-                e2e["src_dev"][:, :T].copy_(e2e["src_host"][:, :T], non_blocking=True)
+                with torch.cuda.stream(up):
+                    up.wait_stream(main)
+                    for i in range(2):  # K, V: contiguous pinned rows -> device
+                        e2e["src_dev"][i][:T].copy_(e2e["src_host"][i][:T], non_blocking=True)
+                main.wait_stream(up)
                 h2d += 2 * T * grp.hkv * D * 2
                 return e2e["src_dev"]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -1000,7 +1004,7 @@ def make_e2e(grp):
 
     e2e = {"host": host, "up": torch.cuda.Stream(grp.dev), "down": torch.cuda.Stream(grp.dev)}
     if grp.max_prompt_tokens:
-        e2e["src_host"] = grp.src.cpu().pin_memory()
+        e2e["src_host"] = [grp.src[i].cpu().pin_memory() for i in range(2)]
         e2e["src_dev"] = torch.empty_like(grp.src)
     return e2e
 
