@@ -630,13 +630,18 @@ class Group:
         self.rng = np.random.default_rng(seed)
         self.bufs, self.graphs = {}, {}
         self.shares = {}
-        self._keep = []
         self.B = 0
         self.n_launch_graph = {}
         # K1 prompt source (admissions): fp16 K and V rows, larger than L2
         self.max_prompt_tokens = max_prompt_tokens
         if max_prompt_tokens:
             self.src = torch.randn(2, max_prompt_tokens, hkv, D, dtype=torch.float16, device=dev)
+            n = len(self.fmts)
+            self.tok_host = torch.zeros(n, 2, max_prompt_tokens, dtype=torch.int32).pin_memory()
+            self.tok_dev = torch.zeros(n, 2, max_prompt_tokens, dtype=torch.int32, device=dev)
+            self.tok_ev = [torch.cuda.Event() for _ in range(n)]
+            for e in self.tok_ev:
+                e.record()
         self.compactions, self.moves, self.slabs_freed = 0, 0, 0
         self.stranded_trace, self.frag_trace = [], []
         self.reb_marks = []  # (K1 bytes, K3 bytes, events) per phase change
@@ -743,14 +748,15 @@ class Group:
         if T == 0:
             return 0
         assert T <= self.max_prompt_tokens
-        # token -> (row, position) lists through pinned memory, no host sync
-        hts = torch.from_numpy(np.repeat(np.asarray(rows, np.int32), np.asarray(prompts))).pin_memory()
-        htp = torch.from_numpy(np.concatenate([np.arange(p, dtype=np.int32) for p in prompts])).pin_memory()
-        ts = hts.to(self.dev, non_blocking=True)
-        tp = htp.to(self.dev, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(main)
-        self._keep = [x for x in self._keep if not x[0].query()] + [(ev, hts, htp)]
+        # token -> (row, position) lists through this model's pinned staging
+        # buffer (reused once its previous upload finished), no host sync
+        self.tok_ev[mi].synchronize()
+        self.tok_host[mi, 0, :T] = torch.from_numpy(np.repeat(np.asarray(rows, np.int32), np.asarray(prompts)))
+        self.tok_host[mi, 1, :T] = torch.from_numpy(np.concatenate([np.arange(p, dtype=np.int32) for p in prompts]))
+        for j in range(2):  # contiguous pinned rows: asynchronous DMA
+            self.tok_dev[mi, j, :T].copy_(self.tok_host[mi, j, :T], non_blocking=True)
+        self.tok_ev[mi].record(main)
+        ts, tp = self.tok_dev[mi, 0, :T], self.tok_dev[mi, 1, :T]
         src = self.src if src_fn is None else src_fn(T)
         for layer in range(self.L):
             kv.kv_append(self.pool, m.fmt, layer, src[0, :T], src[1, :T], ts, tp, m.table,

@@ -133,9 +133,9 @@ ks_status ks_kv_block_size(const ks_model_geometry* g, uint64_t* out);
 /* Slab pool -- slabsim::SlabPool (slab_pool.hpp:101-202)              */
 /* ------------------------------------------------------------------ */
 /* SlabPool(const SlabPoolConfig&) (slab_pool.cpp:51-98).  device >= 0 also
- * reserves the single KV tensor (usable capacity bytes) and the device slab
- * table on that GPU -- the only device allocation the pool ever makes
- * (SPEC.md:165,232).  device < 0 builds a host-only pool. */
+ * reserves the single KV tensor (usable capacity bytes, zero-filled once) and
+ * the device slab table on that GPU -- the only device allocation the pool
+ * ever makes.  device < 0 builds a host-only pool. */
 ks_status ks_pool_create(const ks_pool_config* cfg, int device, ks_pool** out);
 ks_status ks_pool_destroy(ks_pool* pool);
 ks_status ks_pool_get_info(const ks_pool* pool, ks_pool_info* out);

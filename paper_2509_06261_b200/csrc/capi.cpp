@@ -355,6 +355,12 @@ ks_status ks_pool_create(const ks_pool_config* cfg, int device, ks_pool** out) {
       p->d_bytes = p->pool->usable_capacity_bytes();
       e = cudaMalloc(&p->d_base, p->d_bytes);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(KV tensor)");
+      // Zero-filled once: the slots of a block past a sequence's context are
+      // read by the kernels and masked through P = 0, which would turn a NaN
+      // or Inf bit pattern left in fresh device memory into a NaN output.
+      // (Reused blocks hold earlier appended, finite values.)
+      e = cudaMemset(p->d_base, 0, p->d_bytes);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(KV tensor)");
       const size_t tbytes = static_cast<size_t>(p->pool->slab_count()) * 16;
       e = cudaMalloc(&p->d_slab_table, tbytes);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(slab table)");

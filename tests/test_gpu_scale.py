@@ -114,7 +114,8 @@ class Model:
                                          self.scales, nthreads=oracle.NPROC)
             o = out.reshape(-1, 128).astype(np.float64)
             r = ref.reshape(-1, 128)
-            err = (np.abs(o - r).max(1) / np.abs(r).max(1)).max()
+            assert np.isfinite(o).all(), (self.fmt.kv_dtype.name, layer, "non-finite output")
+            err = (np.abs(o - r).max(1) / np.maximum(np.abs(r).max(1), 1e-30)).max()
             assert err <= TOL[self.fmt.kv_dtype], (self.fmt.kv_dtype.name, layer, err)
             errs.append(err)
         return max(errs)
