@@ -1094,7 +1094,8 @@ def measure(name, dev, clocks_index, with_e2e=True, tune=True):
     res["names"] = grp.names
     res["internal_frag_bytes"] = sum(m.internal_frag_bytes() for m in grp.models)
     res["pool"] = dict(slab_bytes=grp.slab, slabs=grp.pool.slab_count(),
-                       residue_bytes=grp.pool.snapshot_stats().slab_residue_bytes)
+                       residue_bytes=grp.pool.snapshot_stats().slab_residue_bytes,
+                       scrubbed_bytes_total=grp.kv.scrubbed_bytes(grp.pool))
     del grp
     torch.cuda.synchronize(dev)
     return res

@@ -139,6 +139,15 @@ ks_status ks_kv_block_size(const ks_model_geometry* g, uint64_t* out);
 ks_status ks_pool_create(const ks_pool_config* cfg, int device, ks_pool** out);
 ks_status ks_pool_destroy(ks_pool* pool);
 ks_status ks_pool_get_info(const ks_pool* pool, ks_pool_info* out);
+/* Device bytes cleared so far because a slab was re-formatted to another key.
+ * A block's slots past a sequence's context are read and masked (P = 0), so
+ * they must not hold NaN patterns; fresh memory is zero-filled at creation,
+ * and a slab whose previous key's bytes (e.g. INT4 nibbles read as FP8) may
+ * form such patterns is cleared (one memset) by the next stream-taking call
+ * on the pool -- table upload, append, decode, prefill, compaction -- on that
+ * call's stream, before its own work.  Graph captures never include it:
+ * upload the new blocks' table entries eagerly before replaying a graph. */
+ks_status ks_pool_scrubbed_bytes(const ks_pool* pool, uint64_t* bytes);
 /* sorted, deduplicated keys (config().block_size_keys, slab_pool.cpp:58-61) */
 ks_status ks_pool_keys(const ks_pool* pool, uint64_t* keys_out, uint32_t capacity);
 

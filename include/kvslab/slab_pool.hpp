@@ -158,6 +158,11 @@ class SlabPool {
                                          std::uint32_t* slabs_freed = nullptr);
   // Slabs whose (key, blocks_total, state) changed since the last call.
   void drain_dirty_slabs(std::vector<std::uint32_t>* out);
+  // Slabs formatted to a key other than the one whose bytes they last held
+  // (device memory starts zero-filled, which is clean for every key): their
+  // stale bytes must be cleared before a kernel reads a block slot past a
+  // sequence's context (a foreign format's bytes can be NaN patterns).
+  void drain_scrub_slabs(std::vector<std::uint32_t>* out);
 
  private:
   int key_index(Bytes key) const;  // -1 if unregistered
@@ -192,6 +197,8 @@ class SlabPool {
   std::uint64_t op_seq_ = 0;
   std::vector<std::uint8_t> dirty_flag_;
   std::vector<std::uint32_t> dirty_;
+  std::vector<Bytes> bytes_key_;  // per slab: key whose format its device bytes hold, 0 = zeros
+  std::vector<std::uint32_t> scrub_;
   std::function<void(const OpLogRecord&)> op_log_;
   std::function<double()> clock_;
 };

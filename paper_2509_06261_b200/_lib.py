@@ -98,6 +98,7 @@ _SIGS = {
     "ks_pool_destroy": (st, [P]),
     "ks_pool_get_info": (st, [P, C.POINTER(ks_pool_info)]),
     "ks_pool_keys": (st, [P, pu64, u32]),
+    "ks_pool_scrubbed_bytes": (st, [P, pu64]),
     "ks_alloc_block": (st, [P, u64, C.POINTER(ks_block_handle)]),
     "ks_try_alloc_block": (st, [P, u64, C.POINTER(ks_block_handle), pi32]),
     "ks_alloc_blocks": (st, [P, u64, u32, C.POINTER(ks_block_handle), pu32]),

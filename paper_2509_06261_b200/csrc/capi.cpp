@@ -167,6 +167,8 @@ struct ks_pool {
   bool fence_pending = false;
   // Tuning overrides, read from the environment once at pool creation.
   kvslab::Tuning tuning;
+  std::vector<uint32_t> scrub;  // scratch for scrub_slabs
+  uint64_t scrubbed_bytes = 0;
 
   ~ks_pool();
   void destroy_device() {
@@ -236,6 +238,30 @@ cudaError_t wait_fence(ks_pool* p, cudaStream_t s) {
   if (e != cudaErrorNotReady) return e;
   if (s == p->fence_stream) return cudaSuccess;
   return cudaStreamWaitEvent(s, p->fence, 0);
+}
+
+// Clears the slabs the allocator re-formatted to a different key since the
+// last call (SlabPool::drain_scrub_slabs), on `s`, ahead of the launch that
+// follows.  Not while `s` is being captured: a graph must not replay it.
+cudaError_t scrub_slabs(ks_pool* p, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(s, &cs);
+  if (e != cudaSuccess || cs != cudaStreamCaptureStatusNone) return e;
+  p->pool->drain_scrub_slabs(&p->scrub);
+  const uint64_t slab = p->pool->slab_size();
+  for (uint32_t id : p->scrub) {
+    e = cudaMemsetAsync(p->d_base + static_cast<uint64_t>(id) * slab, 0, slab, s);
+    if (e != cudaSuccess) return e;
+  }
+  p->scrubbed_bytes += p->scrub.size() * slab;
+  return cudaSuccess;
+}
+
+// The launch prologue of every device entry point that reads or writes KV:
+// order after a pending compaction, then clear re-formatted slabs.
+cudaError_t prepare(ks_pool* p, cudaStream_t s) {
+  cudaError_t e = wait_fence(p, s);
+  return e != cudaSuccess ? e : scrub_slabs(p, s);
 }
 
 uint32_t fmt_bits(uint32_t dt) { return dt == KS_KV_FP16 ? 16 : (dt == KS_KV_INT4 ? 4 : 8); }
@@ -401,6 +427,12 @@ ks_status ks_pool_get_info(const ks_pool* pool, ks_pool_info* out) {
   out->allocated_blocks = p.allocated_block_count();
   out->device = pool->device;
   out->require_lcm_alignment = p.config().require_lcm_alignment ? 1 : 0;
+  return KS_OK;
+}
+
+ks_status ks_pool_scrubbed_bytes(const ks_pool* pool, uint64_t* bytes) {
+  if (!pool || !bytes) return fail(KS_INVALID_ARGUMENT, "null argument");
+  *bytes = pool->scrubbed_bytes;
   return KS_OK;
 }
 
@@ -681,6 +713,8 @@ ks_status ks_block_table_update(ks_pool* pool, int32_t* d_table, uint32_t row_st
     if (!d_table || !rows || !cols || !vals) return fail(KS_INVALID_ARGUMENT, "null argument");
     DeviceGuard g(pool->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t fe = prepare(pool, s);
+    if (fe != cudaSuccess) return cuda_fail(fe, "launch prologue (fence / slab scrub)");
     uint32_t i = 0;
     while (i < n) {
       const uint32_t m = static_cast<uint32_t>(std::min<size_t>(n - i, ks_pool::kSlotWords / 3));
@@ -770,8 +804,8 @@ ks_status ks_kv_append(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, c
     p.block_table = d_block_table;
     p.bt_stride = bt_stride;
     p.kv_scales = d_kv_scales;
-    cudaError_t fe = wait_fence(pool, static_cast<cudaStream_t>(stream));
-    if (fe != cudaSuccess) return cuda_fail(fe, "compaction fence");
+    cudaError_t fe = prepare(pool, static_cast<cudaStream_t>(stream));
+    if (fe != cudaSuccess) return cuda_fail(fe, "launch prologue (fence / slab scrub)");
     cudaError_t e = kvslab::launch_kv_append(p, static_cast<int>(fmt->kv_dtype),
                                              static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "kv_append launch");
@@ -848,8 +882,8 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
     p.debug = tu.decode_debug;
     p.pdl = tu.pdl;
     p.trace = tu.decode_trace;  // probe builds only (Tuning::from_env)
-    cudaError_t fe = wait_fence(pool, static_cast<cudaStream_t>(stream));
-    if (fe != cudaSuccess) return cuda_fail(fe, "compaction fence");
+    cudaError_t fe = prepare(pool, static_cast<cudaStream_t>(stream));
+    if (fe != cudaSuccess) return cuda_fail(fe, "launch prologue (fence / slab scrub)");
     cudaError_t e = kvslab::launch_paged_decode(p, static_cast<int>(fmt->kv_dtype), pool->num_sms,
                                                 static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "paged_decode launch");
@@ -951,8 +985,8 @@ static ks_status prefill_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t l
     p.nt = tu.prefill_nt;
     p.use_tc = tu.prefill_tc;
     p.debug = tu.prefill_debug;
-    cudaError_t fe = wait_fence(pool, static_cast<cudaStream_t>(stream));
-    if (fe != cudaSuccess) return cuda_fail(fe, "compaction fence");
+    cudaError_t fe = prepare(pool, static_cast<cudaStream_t>(stream));
+    if (fe != cudaSuccess) return cuda_fail(fe, "launch prologue (fence / slab scrub)");
     // Workspace use (kvslab.h): split-KV partials when the query tiles alone
     // would leave SMs idle (tcgen05 path) and, for quantised formats with long
     // chunks, the expand-once scratch.  A workspace too small for both drops
@@ -1052,6 +1086,8 @@ ks_status ks_compact_apply(ks_pool* pool, uint64_t key, const ks_block_move* mov
     const uint64_t bps = pool->pool->blocks_per_slab(key);
     DeviceGuard g(pool->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t fe = prepare(pool, s);
+    if (fe != cudaSuccess) return cuda_fail(fe, "launch prologue (fence / slab scrub)");
     uint32_t i = 0;
     while (i < n) {
       const uint32_t m = static_cast<uint32_t>(std::min<size_t>(n - i, ks_pool::kSlotWords / 2));
@@ -1139,8 +1175,8 @@ static ks_status seq_table_sync_impl(ks_seq_table* t, cudaStream_t s) {
     return KS_OK;
   }
   DeviceGuard g(pool->device);
-  cudaError_t fe = wait_fence(pool, s);
-  if (fe != cudaSuccess) return cuda_fail(fe, "compaction fence");
+  cudaError_t fe = prepare(pool, s);
+  if (fe != cudaSuccess) return cuda_fail(fe, "launch prologue (fence / slab scrub)");
   size_t i = 0;
   while (i < pend.size()) {
     const size_t m = std::min(pend.size() - i, ks_pool::kSlotWords / 3);
@@ -1320,6 +1356,11 @@ ks_status ks_compact(ks_pool* pool, uint64_t key, uint32_t max_moves, void* stre
       return fail(KS_NOT_SUPPORTED, "key and slab size must be multiples of 16 bytes");
     const uint64_t bps = pool->pool->blocks_per_slab(key);  // InvalidKeyError first
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    {  // before the snapshot: the rollback must not resurrect drained scrubs
+      DeviceGuard g(pool->device);
+      cudaError_t fe = prepare(pool, s);
+      if (fe != cudaSuccess) return cuda_fail(fe, "launch prologue (fence / slab scrub)");
+    }
     std::vector<ks_seq_table*> mine;
     for (ks_seq_table* t : pool->tables)
       if (t->t->key() == key) mine.push_back(t);
@@ -1337,8 +1378,6 @@ ks_status ks_compact(ks_pool* pool, uint64_t key, uint32_t max_moves, void* stre
     };
     if (!mv.empty()) {
       DeviceGuard g(pool->device);
-      cudaError_t fe = wait_fence(pool, s);
-      if (fe != cudaSuccess) return rollback(cuda_fail(fe, "compaction fence"));
       // bytes
       const size_t per = ks_pool::kSlotWords / 2;
       for (size_t i0 = 0; i0 < mv.size(); i0 += per) {

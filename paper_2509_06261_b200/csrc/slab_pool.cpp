@@ -118,6 +118,7 @@ SlabPool::SlabPool(const SlabPoolConfig& config) : config_(config) {
   partial_.resize(keys_.size());
   for (auto& p : partial_) p.resize(nslabs_);
   dirty_flag_.assign(nslabs_, 0);
+  bytes_key_.assign(nslabs_, 0);
   stats_.free_slab_bytes = usable_capacity_;
 }
 
@@ -174,6 +175,10 @@ void SlabPool::mark_dirty(std::uint32_t s) {
     dirty_.push_back(s);
   }
 }
+void SlabPool::drain_scrub_slabs(std::vector<std::uint32_t>* out) {
+  out->clear();
+  out->swap(scrub_);
+}
 void SlabPool::drain_dirty_slabs(std::vector<std::uint32_t>* out) {
   out->clear();
   out->swap(dirty_);
@@ -182,6 +187,8 @@ void SlabPool::drain_dirty_slabs(std::vector<std::uint32_t>* out) {
 
 // slab_pool.cpp:143-158
 void SlabPool::format_slab(std::uint32_t s, int k) {
+  if (bytes_key_[s] != 0 && bytes_key_[s] != keys_[k]) scrub_.push_back(s);
+  bytes_key_[s] = keys_[k];
   kidx_[s] = static_cast<std::uint16_t>(k + 1);
   total_[s] = bps_[k];
   used_[s] = 0;

@@ -143,6 +143,13 @@ def kv_tensor(pool: SlabPool) -> torch.Tensor:
     return torch.as_tensor(_CAI(base.value, nbytes.value), device=f"cuda:{pool.device}")
 
 
+def scrubbed_bytes(pool: SlabPool) -> int:
+    """Bytes cleared because slabs were re-formatted to another key (ks_pool_scrubbed_bytes)."""
+    out = C.c_uint64()
+    check(L.lib.ks_pool_scrubbed_bytes(pool.handle, C.byref(out)))
+    return out.value
+
+
 def validate_format(pool: SlabPool, fmt: KvFormat) -> None:
     f = fmt.to_c()
     check(L.lib.ks_validate_format(pool.handle, C.byref(f)))

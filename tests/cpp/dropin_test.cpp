@@ -89,12 +89,15 @@ int main() {
     pool.debug_flip_occupancy_bit(0, 1);
     CHECK(!pool.check_integrity(&why) && !why.empty());
   }
-  KvGeometry g;  // precision.cpp:76-99, test_precision.cpp:23-51
+  kvslab::KvGeometry g;  // precision.cpp:76-99, test_precision.cpp:23-51 (kvslab's geometry helpers)
   g.num_kv_heads = 8;
   g.head_dim = 128;
   g.kv_bits = 8;
   g.quant_param_bytes_per_block = 64;
-  CHECK(token_size(g) == 2048 && kv_block_size(g) == 32832);
+  CHECK(kvslab::token_size(g) == 2048 && kvslab::kv_block_size(g) == 32832);
+  // kvslab's errors ARE slabsim's: a reference-style catch clause sees them
+  CHECK(throws<slabsim::InvalidKeyError>([&] { SlabPool p(two); p.alloc_block(3); }));
+  CHECK(throws<slabsim::Error>([&] { SlabPool p(two); p.free_block(BlockHandle{}); }));
   std::printf(failures ? "dropin: %d failures\n" : "dropin: all checks passed\n", failures);
   return failures ? 1 : 0;
 }
