@@ -1092,6 +1092,7 @@ def measure(name, dev, clocks_index, with_e2e=True, tune=True):
     res["kernel_batch"] = grp.B
     res["kernel_ctx"] = int(np.mean(grp.models[0].ctx_lens(grp.B)))
     res["names"] = grp.names
+    res["hkv"] = grp.hkv
     res["internal_frag_bytes"] = sum(m.internal_frag_bytes() for m in grp.models)
     res["pool"] = dict(slab_bytes=grp.slab, slabs=grp.pool.slab_count(),
                        residue_bytes=grp.pool.snapshot_stats().slab_residue_bytes,
@@ -1126,7 +1127,7 @@ def summarise(name, r, peak, peak_kind, world):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": f"paged_decode_kernel<{dom.upper()}> fused append+decode, one layer of "
-                               f"{r['kernel_batch']} seqs x ctx~{r['kernel_ctx']}, 8 kv heads",
+                               f"{r['kernel_batch']} seqs x ctx~{r['kernel_ctx']}, {r.get('hkv', HKV)} kv heads",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "frac_of_8TBps": round(achieved / 8000.0, 4)},
         "kernels": kernels,
