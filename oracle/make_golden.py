@@ -158,6 +158,7 @@ def main():
     with open(os.path.join(OUT, "churn.json"), "w") as f:
         json.dump(meta, f, indent=1)
     c5()
+    pool_sizing()
     print("golden vectors written to", OUT)
 
 
@@ -182,8 +183,22 @@ def c5():
                    "models": models, "assign": assign, "requests": reqs}, f, indent=0)
 
 
+def pool_sizing():
+    """a4: the reference's per-group KV pool sizing (simulator.cpp:264-290) for
+    every shipped scenario, with its inputs, from oracle/_ref/ref_calib --pools."""
+    import glob
+    scen = sorted(glob.glob("/root/reference/proj/scenarios/*.json"))
+    out = subprocess.run([os.path.join(HERE, "_ref", "ref_calib"), "--pools", *scen], capture_output=True,
+                         text=True, check=True).stdout
+    with open(os.path.join(OUT, "pool_sizing.json"), "w") as f:
+        json.dump({"cite": "oracle/ref_calib.cpp --pools -> simulator.cpp:264-290, precision.cpp:119-127",
+                   "scenarios": json.loads(out)}, f, indent=0)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "c5":
         c5()
+    elif len(sys.argv) > 1 and sys.argv[1] == "pool_sizing":
+        pool_sizing()
     else:
         main()

@@ -56,6 +56,67 @@ def pool_config(models: Sequence[ModelDemand], headroom_slabs: int = 2,
     return SlabPoolConfig(nslabs * slab, slab, keys, True)
 
 
+@dataclass(frozen=True)
+class ResidentModel:
+    """The fields of slabsim::ModelProfile the pool sizing reads
+    (precision.hpp:57-76), per shard, at the model's operating batch."""
+    name: str
+    key: int                      # kv_block_size (precision.cpp:91-99)
+    weight_bytes: int
+    operating_batch: int          # operating_batch_size (precision.cpp:101-117)
+    tp_degree: int = 1
+    avg_activation_bytes: int = 0
+    avg_kv_bytes: int = 0
+
+
+def base_footprint(m: ResidentModel) -> int:
+    """precision.cpp:119-123: weights/tp + (activations + KV) x operating batch."""
+    return m.weight_bytes // m.tp_degree + (m.avg_activation_bytes + m.avg_kv_bytes) * m.operating_batch
+
+
+def kv_reservation(m: ResidentModel) -> int:
+    """precision.cpp:125-127: the KV part of the base footprint."""
+    return m.avg_kv_bytes * m.operating_batch
+
+
+def residual_pool_bytes(models: Sequence[ResidentModel], group_memory: int) -> int:
+    """simulator.cpp:264-276: the slab pool of a GPU group is what its memory
+    leaves after every resident's base footprint, plus back the KV those
+    footprints reserved (the pool replaces the per-model KV reservations)."""
+    charged = sum(base_footprint(m) for m in models)
+    if charged > group_memory:
+        raise ValueError("resident footprints exceed the group's memory")
+    return group_memory - charged + sum(kv_reservation(m) for m in models)
+
+
+def lcm_slab_bytes(keys: Sequence[int], multiplier: int = 1) -> int:
+    """simulator.cpp:281-290 (auto_lcm): slab = lcm(co-located keys) x multiplier."""
+    return math.lcm(*keys) * multiplier
+
+
+def device_pool_config(models: Sequence[ResidentModel], device: int = 0, group_memory: int = None,
+                       multiplier: int = 1, slab_bytes: int = None,
+                       reserve_bytes: int = 2 << 30) -> SlabPoolConfig:
+    """The KV pool of one GPU under the reference's sizing policy, bounded by
+    what the device can actually give: group memory defaults to the device's
+    total memory (torch.cuda.mem_get_info), and the pool never exceeds the
+    free memory minus `reserve_bytes` (workspaces, graphs).  The slab is the
+    keys' lcm x multiplier when that fits a few times in the pool, else the
+    caller's relaxed `slab_bytes` (residue slabs, require_lcm_alignment off)."""
+    import torch
+    free, total = torch.cuda.mem_get_info(device)
+    gm = total if group_memory is None else group_memory
+    pool = min(residual_pool_bytes(models, gm), free - reserve_bytes)
+    keys = sorted({m.key for m in models})
+    slab = lcm_slab_bytes(keys, multiplier)
+    aligned = slab_bytes is None
+    if not aligned:
+        slab = slab_bytes
+    if pool < slab:
+        raise ValueError(f"a {pool}-byte pool cannot hold one {slab}-byte slab")
+    return SlabPoolConfig(pool // slab * slab, slab, keys, aligned)
+
+
 def reduce_max(value: float) -> float:
     """Max over ranks (device-timed numbers are reported as the slowest rank)."""
     import torch
