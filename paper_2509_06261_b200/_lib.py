@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkvslab.so")
+LIB_PATH = os.environ.get("KVSLAB_LIB_PATH") or os.path.join(_HERE, "libkvslab.so")  # override: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
