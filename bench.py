@@ -851,8 +851,9 @@ class Group:
     def tune_shares(self, B):
         """MPS-style spatial split (ks_set_decode_sm_share): a few candidate
         splits of the SMs between the co-located models (KV bytes per token,
-        the consumer-bound INT4 weighted 1-3x; all SMs or 92 %), each timed on
-        an 8-layer eager pass at batch B; the fastest is kept."""
+        the consumer-bound INT4 weighted 1-3x; all SMs, 92 % or 84 %; or no
+        partition), each captured as an 8-layer graph at batch B and timed by
+        replay, as the step graphs will run it; the fastest is kept."""
         torch, kv = self.torch, self.kv
         n = len(self.models)
         if n == 1:
@@ -866,32 +867,42 @@ class Group:
                 for skew in (0.9, 1.0, 1.1) if n == 2 else (1.0,):
                     w0 = [ww[0] * skew] + ww[1:]
                     cands.add(tuple(max(8, min(tot - 8, int(tot * x / sum(w0)))) for x in w0))
+        cands.add(tuple([nsm] * n))  # no partition: every model's grid spans the GPU
         bs = self.buffers(B)[0]
         main = torch.cuda.current_stream(self.dev)
         times = {}
-        for c in sorted(cands):
+
+        def few():
+            cur = torch.cuda.current_stream(self.dev)  # the capture stream
+            for st in self.streams:
+                st.wait_stream(cur)
+            for layer in range(min(8, self.L)):
+                for mi, m in enumerate(self.models):
+                    kv.paged_decode(self.pool, m.fmt, layer, bs["q"][mi][layer], m.table,
+                                    self.ctx[mi][:B], out=bs["out"][mi][layer], kv_scales=self.scales,
+                                    workspace=self.ws[mi], stream=self.streams[mi])
+            for st in self.streams:
+                cur.wait_stream(st)
+        for c in sorted(cands):  # each split as the graphs will run it: captured, replayed
             for m, sh in zip(self.models, c):
                 kv.set_decode_sm_share(self.pool, m.key, sh)
-            best = None
-            for _ in range(2):
-                for st in self.streams:
-                    st.wait_stream(main)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(main)
-                for st in self.streams:
-                    st.wait_stream(main)
-                for layer in range(min(8, self.L)):
-                    for mi, m in enumerate(self.models):
-                        kv.paged_decode(self.pool, m.fmt, layer, bs["q"][mi][layer], m.table,
-                                        self.ctx[mi][:B], out=bs["out"][mi][layer], kv_scales=self.scales,
-                                        workspace=self.ws[mi], stream=self.streams[mi])
-                for st in self.streams:
-                    main.wait_stream(st)
-                b.record(main)
-                torch.cuda.synchronize(self.dev)
-                t = a.elapsed_time(b)
-                best = t if best is None else min(best, t)
-            times[c] = best
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(self.dev)
+            cap.wait_stream(main)
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(g, stream=cap):
+                    few()
+            main.wait_stream(cap)
+            g.replay()
+            torch.cuda.synchronize(self.dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(main)
+            for _ in range(3):
+                g.replay()
+            b.record(main)
+            torch.cuda.synchronize(self.dev)
+            times[c] = a.elapsed_time(b) / 3
+            del g
         pick = min(times, key=times.get)
         for m, sh in zip(self.models, pick):
             kv.set_decode_sm_share(self.pool, m.key, sh)
@@ -1057,15 +1068,16 @@ def measure(name, dev, clocks_index, with_e2e=True, tune=True):
     per-model kernel roofline.  Returns a dict of raw numbers."""
     import torch
     grp, targets, e2e_targets = build_group(name, dev, seed=1234 + RANK)
-    if tune:
-        grp.graph(targets[0])  # warm the kernels' function attributes
-        shares = grp.tune_shares(max(targets))
-    else:
-        shares = None
-    for B in sorted(set(targets + e2e_targets)):  # capture outside the timed region
+    # the SM split is baked into each captured graph (grid sizes): tune it
+    # per batch size of the schedule, then capture that size's graphs
+    shares = {}
+    for B in sorted(set(targets + e2e_targets), reverse=True):  # capture outside the timed region
+        if tune:
+            shares[f"B{B}"] = grp.tune_shares(B)
         grp.graph(B, 0)
         if with_e2e:
             grp.graph(B, 1)
+    shares = shares or None
     warm, timed = targets[:ARGS.warmup], targets[ARGS.warmup:]
     time_steps(grp, warm)
     if WORLD > 1:
