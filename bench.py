@@ -848,6 +848,31 @@ class Group:
             kv.set_decode_sm_share(self.pool, m.key, sh)
         return out
 
+    def k1_times(self, per_row=512, reps=5):
+        """Every model's K1 alone (ks_kv_append, one layer, per_row tokens of
+        each of rows 0..B-1 rewritten in place, the whole GPU): (bytes, ms)."""
+        torch, kv = self.torch, self.kv
+        B = self.B
+        T = min(B * per_row, self.max_prompt_tokens)
+        per_row = T // B
+        ts = torch.arange(B, dtype=torch.int32, device=self.dev).repeat_interleave(per_row)
+        tp = torch.arange(per_row, dtype=torch.int32, device=self.dev).repeat(B)
+        main = torch.cuda.current_stream(self.dev)
+        out = {}
+        for mi, m in enumerate(self.models):
+            fn = lambda: kv.kv_append(self.pool, m.fmt, 0, self.src[0, :B * per_row], self.src[1, :B * per_row],
+                                      ts, tp, m.table, self.scales, stream=main)
+            fn()
+            torch.cuda.synchronize(self.dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(main)
+            for _ in range(reps):
+                fn()
+            b.record(main)
+            torch.cuda.synchronize(self.dev)
+            out[self.names[mi]] = (m.fmt.append_bytes(B * per_row), a.elapsed_time(b) / reps)
+        return out
+
     def tune_shares(self, B):
         """MPS-style spatial split (ks_set_decode_sm_share): a few candidate
         splits of the SMs between the co-located models (KV bytes per token,
@@ -1101,6 +1126,7 @@ def measure(name, dev, clocks_index, with_e2e=True, tune=True):
     if max(targets) != grp.B:  # the kernels at the workload's largest batch
         grp.rebalance(max(targets))
     res["kernels"] = grp.kernel_times()
+    res["k1"] = grp.k1_times() if grp.max_prompt_tokens else {}
     res["kernel_batch"] = grp.B
     res["kernel_ctx"] = int(np.mean(grp.models[0].ctx_lens(grp.B)))
     res["names"] = grp.names
@@ -1143,6 +1169,9 @@ def summarise(name, r, peak, peak_kind, world):
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "frac_of_8TBps": round(achieved / 8000.0, 4)},
         "kernels": kernels,
+        "k1_append": {k: {"bytes": int(v[0]), "us": round(v[1] * 1e3, 2),
+                          "gbs": round(v[0] / (v[1] / 1e3) / 1e9, 1),
+                          "frac": round(v[0] / (v[1] / 1e3) / 1e9 / peak, 4)} for k, v in r.get("k1", {}).items()},
         "breakdown": r.get("breakdown"),
         "sm_share": r["shares"],
         "gpu_launches": int(r["launches"]),

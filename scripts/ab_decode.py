@@ -1,7 +1,7 @@
 """A/B timing of K2 launch configurations in ONE process (design probe).
 
 Each configuration (a dict of KVSLAB_* environment overrides, read by the C
-ABI at launch time) gets its own CUDA graph of L layers; rounds alternate the
+ABI when a pool is created) gets its own pool and CUDA graph of L layers; rounds alternate the
 configurations so box-to-box and drift effects cancel.  Usage:
   AB='{"a":{}, "b":{"KVSLAB_MERGE_THREADS":"128"}}' CASES=FP16:16:2048,INT4:32:1024 \
       python scripts/ab_decode.py
@@ -24,21 +24,22 @@ for dtn, bs, cs in cases:
     fmt = KvFormat(dt, 8, 32, 128, L)
     slab = fmt.key * 16
     nb = (ctx0 + 15) // 16 + 1
-    pool = ks.SlabPool(ks.SlabPoolConfig((B * nb // 16 + 4) * slab, slab, [fmt.key]), device=0)
-    m = SlabModel(pool, fmt, B, nb)
-    for s in range(B):
-        assert m.admit(s, ctx0)
-    m.sync()
     ctx = torch.full((B,), ctx0, dtype=torch.int32, device="cuda")
     qs = [torch.randn(B, 32, 128, dtype=torch.float16, device="cuda") for _ in range(L)]
     kn = torch.randn(B, 8, 128, dtype=torch.float16, device="cuda")
     sc = torch.ones(16, device="cuda")
-    ws = kv.DecodeWorkspace(pool, fmt, B)
     by = fmt.decode_bytes([ctx0] * B)
-    graphs = {}
+    graphs, keep = {}, []
     base_env = dict(os.environ)
     for name, env in configs.items():
+        # the tuning overrides are read when a pool is created: one pool per configuration
         os.environ.clear(); os.environ.update(base_env); os.environ.update(env)
+        pool = ks.SlabPool(ks.SlabPoolConfig((B * nb // 16 + 4) * slab, slab, [fmt.key]), device=0)
+        m = SlabModel(pool, fmt, B, nb)
+        for s in range(B):
+            assert m.admit(s, ctx0)
+        m.sync()
+        ws = kv.DecodeWorkspace(pool, fmt, B)
         g = torch.cuda.CUDAGraph()
         st = torch.cuda.Stream()
         def step():
@@ -50,6 +51,7 @@ for dtn, bs, cs in cases:
             with torch.cuda.graph(g, stream=st):
                 step()
         graphs[name] = g
+        keep.append((pool, m, ws))
     os.environ.clear(); os.environ.update(base_env)
     res = {n: [] for n in graphs}
     for r in range(rounds):
@@ -64,4 +66,4 @@ for dtn, bs, cs in cases:
     line = " | ".join(f"{n}: {np.median(v):6.2f} us ({by / np.median(v) / 1e3:6.0f} GB/s)"
                       for n, v in res.items())
     print(f"{dtn:9s} B={B:3d} ctx={ctx0:5d}  {line}", flush=True)
-    del pool
+    del graphs, keep
