@@ -413,6 +413,11 @@ ks_status ks_seq_table_sync(ks_seq_table* t, void* stream);
 ks_status ks_compact(ks_pool* pool, uint64_t key, uint32_t max_moves, void* stream,
                      uint32_t* n_moves, uint32_t* slabs_freed);
 
+/* Design probes only: in a -DKVSLAB_PROBES build, the following K2 launches
+ * write per-CTA globaltimer stamps to d_trace (NULL = off; scripts/
+ * probe_timeline.py).  KS_NOT_SUPPORTED in release builds. */
+ks_status ks_probe_set_decode_trace(ks_pool* pool, void* d_trace);
+
 /* Number of kernel launches this process issued through the library
  * (per kernel family); used by bench.py for its gpu_launches claim. */
 uint64_t ks_launch_count(void);

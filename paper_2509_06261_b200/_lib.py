@@ -138,6 +138,7 @@ _SIGS = {
     "ks_paged_prefill_ws": (st, [P, C.POINTER(ks_kv_format), u32, P, P, P, P, u32, P, P, u32, u32,
                                  C.c_float, P, P, C.c_size_t, P]),
     "ks_set_decode_sm_share": (st, [P, u64, u32]),
+    "ks_probe_set_decode_trace": (st, [P, P]),
     "ks_compact_plan": (st, [P, u64, u32, C.POINTER(ks_block_move), pu32, pu32]),
     "ks_compact_apply": (st, [P, u64, C.POINTER(ks_block_move), u32, P]),
     "ks_block_table_remap": (st, [P, P, u64, C.POINTER(ks_block_move), u32, P]),

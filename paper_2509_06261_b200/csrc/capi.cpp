@@ -119,8 +119,6 @@ Tuning Tuning::from_env() {
   t.prefill_expand = static_cast<int>(num("KVSLAB_PREFILL_EXPAND", -1));
   t.prefill_split = static_cast<int>(num("KVSLAB_PREFILL_SPLIT", 1));
   if (kProbes) {
-    t.decode_trace = reinterpret_cast<unsigned long long*>(
-        static_cast<uintptr_t>(std::strtoull(std::getenv("KVSLAB_DECODE_TRACE") ? std::getenv("KVSLAB_DECODE_TRACE") : "0", nullptr, 0)));
     t.decode_debug = static_cast<int>(num("KVSLAB_DECODE_DEBUG", 0));
     t.prefill_debug = static_cast<int>(num("KVSLAB_PREFILL_DEBUG", 0));
   }
@@ -1047,6 +1045,13 @@ ks_status ks_paged_prefill_ws(ks_pool* pool, const ks_kv_format* fmt, uint32_t l
                               void* stream) {
   return prefill_impl(pool, fmt, layer, d_q, d_out, d_lse, d_block_table, bt_stride, d_cu_q, d_ctx_lens,
                       batch, max_q_len, sm_scale, d_kv_scales, d_workspace, workspace_bytes, stream);
+}
+
+ks_status ks_probe_set_decode_trace(ks_pool* pool, void* d_trace) {
+  if (!pool) return fail(KS_INVALID_ARGUMENT, "null pool");
+  if (!kvslab::kProbes) return fail(KS_NOT_SUPPORTED, "timestamp probes need a -DKVSLAB_PROBES build");
+  pool->tuning.decode_trace = static_cast<unsigned long long*>(d_trace);
+  return KS_OK;
 }
 
 ks_status ks_set_decode_sm_share(ks_pool* pool, uint64_t key, uint32_t max_ctas) {

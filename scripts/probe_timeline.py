@@ -1,5 +1,8 @@
 """Timeline of L consecutive K2 layers (decode + merge, PDL, one CUDA graph) from
-globaltimer stamps -- design probe.  Per layer (us from the first decode CTA start):
+globaltimer stamps -- design probe; needs a probe build of the library:
+  make -C paper_2509_06261_b200/csrc BUILD=$PWD/build_ab/probe/obj OUT=$PWD/build_ab/probe/libkvslab.so \
+       NVFLAGS_EXTRA=-DKVSLAB_PROBES CXXFLAGS_EXTRA=-DKVSLAB_PROBES
+  KVSLAB_LIB_PATH=$PWD/build_ab/probe/libkvslab.so python scripts/probe_timeline.py  Per layer (us from the first decode CTA start):
 decode CTA start (min/max), consumer first data (median), consumer done (max),
 merge past its wait (min), merge done (max)."""
 import os, sys
@@ -33,11 +36,11 @@ for spec in os.environ.get("CASES", "FP8_E4M3:16:2048,INT4:8:8192").split(","):
     st = torch.cuda.Stream()
     def step():
         for l in range(L):
-            os.environ["KVSLAB_DECODE_TRACE"] = str(tr[l].data_ptr())
+            ks._lib.lib.ks_probe_set_decode_trace(pool.handle, tr[l].data_ptr())
             app = os.environ.get("APPEND", "1") == "1"
             kv.paged_decode(pool, fmt, l, qs[l], m.table, ctx, kv_scales=sc, workspace=ws,
                             k_new=kn if app else None, v_new=kn if app else None)
-        del os.environ["KVSLAB_DECODE_TRACE"]
+        ks._lib.lib.ks_probe_set_decode_trace(pool.handle, None)
     with torch.cuda.stream(st):
         step(); torch.cuda.synchronize()
         with torch.cuda.graph(g, stream=st):
