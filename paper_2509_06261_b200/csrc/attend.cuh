@@ -600,6 +600,287 @@ __device__ __forceinline__ void attend_pk(UnitState<1>& u, const uint32_t (&sbs)
   pk_update<FMT, NB, MASK>(u, d, sbs, valid, wK, wP, kvq, pq, fo, qsb, qst, kscale, sml2, g, t);
 }
 
+// ------------------------------------- integer QK step (INT8/INT4, G <= 4)
+// S^T = K.Q^T on IMMA (mma.sync m16n8k32, 8-bit A and B, s32 accumulate):
+// the codes enter the MMA as stored -- INT8 s8 directly, INT4 as two u8
+// registers per 32-bit word (w & 0x0F0F0F0F: even dims, (w >> 4) & 0x0F0F0F0F:
+// odd dims) -- so K costs 0 (INT8) or 3 instructions per 8 values instead of
+// the fp16 unpack's 5.  Q becomes 16-bit fixed point per query row,
+// v = rint(q / s_q) with s_q = max|q| / QM, split v = 256 hi + lo with hi, lo
+// in [-128, 127], and tile column n of the B operand is (query n >> 1, hi | lo):
+// thread (g, t) receives rows g, g+8 of query t as (hi, lo) in (c0, c1) and
+// (c2, c3), so S = 256 c0 + c1 needs no shuffle, and one 4-MMA chain per block
+// replaces 8 HMMAs; the INT4 score is s_k s_q S + z_k sum(q).  Q is rounded
+// to 1/32639 of its row maximum: with INT4's unsigned codes (mean 7.5) that
+// error is not centred, and the first form -- odd dims kept in place as 16 n
+// with 16 v on the even dims, QM = 2039 -- measured 1.6e-2 relative at ctx 16k
+// with 8-sigma outliers (the tolerance is 1e-2); one SHF per word buys the
+// 4 bits back (tests/test_gpu_kernels.py, scripts/acc_report.py).
+// PV stays on fp16 HMMA exactly as attend_pk (the per-token V scale must ride
+// in P).  The two packed column streams are kept in "score layout" during
+// the loop -- thread t holds (m, l, zb, zz) of query t for block parities 0
+// and 1 -- and moved to the accumulator's column layout (thread t owns
+// columns 2t, 2t+1 = query (2t)&3 (+1), parity t >> 1) by to_acc_cols.
+template <int FMT>
+__device__ __forceinline__ void imma16832(int* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                          uint32_t b0, uint32_t b1) {
+  if constexpr (FMT == kINT4)
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  else
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int FMT>
+struct IqQ {
+  static constexpr float kQM = 32639.f;  // |v| <= 32639: hi = (v + 128) >> 8 fits s8
+};
+
+// Q of the unit (rows of the group's head, G <= 4) -> IMMA B fragments of
+// column g: query g >> 1, byte half g & 1.  qsc / qz of query t for the score
+// epilogue: s_q * sml2 and sml2 * sum(q).
+template <int FMT>
+__device__ __forceinline__ void load_q_iq(uint32_t sQ, int g, int t, uint32_t G, float sml2,
+                                          uint32_t (&qi)[4][2], float& qsc, float& qz) {
+  const int qq = g >> 1;
+  const bool ok = qq < static_cast<int>(G);
+  const uint32_t row = sQ + qq * kD * 2;
+  uint4 v[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) v[c] = ok ? lds128(row + 64 * t + 16 * c) : make_uint4(0, 0, 0, 0);
+  float x[4][8];
+  float amax = 0.f, sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+      x[c][2 * e] = f.x;
+      x[c][2 * e + 1] = f.y;
+      amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+      sum += f.x + f.y;
+    }
+  }
+  amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+  amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+  sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+  sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+  const float inv = amax > 0.f ? IqQ<FMT>::kQM / amax : 0.f;
+  const bool lo_half = g & 1;
+  // byte of value v for this column's half: hi = (v + 128) >> 8, lo = v - 256 hi
+  auto half_byte = [&](float xf) -> uint32_t {
+    const int vv = __float2int_rn(xf * inv);
+    const int hi = (vv + 128) >> 8;
+    return static_cast<uint32_t>(lo_half ? vv - 256 * hi : hi) & 0xffu;
+  };
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {  // k-step c: dims 32t + 8c .. +7
+    uint32_t b0 = 0, b1 = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if constexpr (FMT == kINT4) {  // b0: even dims, b1: odd dims
+        b0 |= half_byte(x[c][2 * j]) << (8 * j);
+        b1 |= half_byte(x[c][2 * j + 1]) << (8 * j);
+      } else {  // b0: dims 0..3, b1: dims 4..7
+        b0 |= half_byte(x[c][j]) << (8 * j);
+        b1 |= half_byte(x[c][4 + j]) << (8 * j);
+      }
+    }
+    qi[c][0] = b0;
+    qi[c][1] = b1;
+  }
+  const float sq = amax / IqQ<FMT>::kQM;
+  // query t's values live in lanes g = 2t (any t'): broadcast to thread t
+  qsc = __shfl_sync(0xffffffffu, sq, (2 * t) * 4) * sml2;
+  qz = __shfl_sync(0xffffffffu, sum, (2 * t) * 4) * sml2;
+}
+
+// score layout (thread t: query t, parities 0/1, equal over g) -> the values
+// of this thread's accumulator columns 2t, 2t+1 (query (2t)&3 (+1), parity t >> 1)
+__device__ __forceinline__ void to_acc_cols(const float (&v)[2], int g, int t, float (&o)[2]) {
+  const int q0 = (2 * t) & 3;
+  const bool b = t >> 1;
+  const float a0 = __shfl_sync(0xffffffffu, v[0], g * 4 + q0);
+  const float a1 = __shfl_sync(0xffffffffu, v[1], g * 4 + q0);
+  const float c0 = __shfl_sync(0xffffffffu, v[0], g * 4 + q0 + 1);
+  const float c1 = __shfl_sync(0xffffffffu, v[1], g * 4 + q0 + 1);
+  o[0] = b ? a1 : a0;
+  o[1] = b ? c1 : c0;
+}
+
+// bias flush of the integer step: zb (score layout) summed over the 16 token
+// rows and added to the accumulator columns
+template <int FMT>
+__device__ __forceinline__ void flush_bias_iq(UnitState<1>& u, int g, int t) {
+  float z[2];
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    float s = u.zb[0][b];
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 8);
+    s += __shfl_xor_sync(0xffffffffu, s, 16);
+    z[b] = s;
+    u.zb[0][b] = 0.f;
+  }
+  float zc[2];
+  to_acc_cols(z, g, t, zc);
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      u.acc[mt][0][c] += zc[c];
+      u.acc[mt][0][2 + c] += zc[c];
+    }
+}
+
+// segment end: (m, l, zb, zz) from score layout to accumulator columns (the
+// layout fold_halves and the epilogue expect); l/zb/zz stay per-row partials
+__device__ __forceinline__ void iq_state_to_acc(UnitState<1>& u, int g, int t) {
+  float o[2];
+  to_acc_cols(u.m[0], g, t, o);
+  u.m[0][0] = o[0]; u.m[0][1] = o[1];
+  to_acc_cols(u.l[0], g, t, o);
+  u.l[0][0] = o[0]; u.l[0][1] = o[1];
+  to_acc_cols(u.zb[0], g, t, o);
+  u.zb[0][0] = o[0]; u.zb[0][1] = o[1];
+  to_acc_cols(u.zz[0], g, t, o);
+  u.zz[0][0] = o[0]; u.zz[0][1] = o[1];
+}
+
+template <int FMT, int NB, bool MASK>
+__device__ __forceinline__ void attend_iq(UnitState<1>& u, const uint32_t (&sbs)[2], const int (&valid)[2],
+                                          uint32_t wK, uint32_t wP, uint32_t kvq, uint32_t pq,
+                                          const FragOff& fo, const uint32_t (&qi)[4][2], float qsc,
+                                          float qz, int g, int t) {
+  using Gm = Geo<FMT>;
+  // ---- scores of query t, rows g, g+8, both blocks ----
+  float x[2][2], sv[2][2], zv[2][2];
+#pragma unroll
+  for (int bi = 0; bi < 2; ++bi) {
+    if (bi >= NB) {
+      x[bi][0] = x[bi][1] = -INFINITY;
+      sv[bi][0] = sv[bi][1] = zv[bi][0] = zv[bi][1] = 0.f;
+      continue;
+    }
+    const uint32_t sK = sbs[bi] + wK;
+    int c[4] = {0, 0, 0, 0};
+    if constexpr (FMT == kINT4) {
+      const uint4 lo = lds128(sK + fo.k[0]);  // row g: dims 32t .. 32t+31
+      const uint4 hi = lds128(sK + fo.k[1]);  // row g+8
+      const uint32_t wl[4] = {lo.x, lo.y, lo.z, lo.w}, wh[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        imma16832<FMT>(c, wl[i] & 0x0F0F0F0Fu, wh[i] & 0x0F0F0F0Fu, (wl[i] >> 4) & 0x0F0F0F0Fu,
+                       (wh[i] >> 4) & 0x0F0F0F0Fu, qi[i][0], qi[i][1]);
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint4 lo = lds128(sK + fo.k[h]);
+        const uint4 hi = lds128(sK + fo.k[h] + 1024);
+        imma16832<FMT>(c, lo.x, hi.x, lo.y, hi.y, qi[2 * h][0], qi[2 * h][1]);
+        imma16832<FMT>(c, lo.z, hi.z, lo.w, hi.w, qi[2 * h + 1][0], qi[2 * h + 1][1]);
+      }
+    }
+    const uint32_t sKp = sbs[bi] + wP, sVp = sKp + pq;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      float sk, zk = 0.f;
+      if constexpr (FMT == kINT4) {
+        const uint32_t kp = lds32(sKp + 4 * (g + 8 * r)), vp = lds32(sVp + 4 * (g + 8 * r));
+        const float2 kf = __half22float2(*reinterpret_cast<const __half2*>(&kp));
+        const float2 vf = __half22float2(*reinterpret_cast<const __half2*>(&vp));
+        sk = kf.x;
+        zk = kf.y;
+        sv[bi][r] = vf.x;
+        zv[bi][r] = vf.y;
+      } else {
+        sk = __half2float(__ushort_as_half(lds16(sKp + 2 * (g + 8 * r))));
+        sv[bi][r] = __half2float(__ushort_as_half(lds16(sVp + 2 * (g + 8 * r))));
+        zv[bi][r] = 0.f;
+      }
+      const float s = static_cast<float>(c[2 * r] * 256 + c[2 * r + 1]);
+      float xv = s * (sk * qsc);
+      if constexpr (FMT == kINT4) xv = fmaf(zk, qz, xv);
+      x[bi][r] = (MASK && !(g + 8 * r < valid[bi])) ? -INFINITY : xv;
+    }
+  }
+  // ---- online softmax per parity stream (lazy rescale, as in attend) ----
+  bool grow = false;
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) grow |= x[b][r] > u.m[0][b] + kRescaleSlack;
+  if (__any_sync(0xffffffffu, grow)) {
+    float al[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      float mx = fmaxf(x[b][0], x[b][1]);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      const float mn = fmaxf(u.m[0][b], mx);
+      al[b] = ex2(u.m[0][b] - mn);
+      u.m[0][b] = mn;
+      u.l[0][b] *= al[b];
+      u.zb[0][b] *= al[b];
+      u.zz[0][b] *= al[b];
+    }
+    float ac[2];
+    to_acc_cols(al, g, t, ac);
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        u.acc[mt][0][c] *= ac[c];
+        u.acc[mt][0][2 + c] *= ac[c];
+      }
+  }
+  float pr[2][2];
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) pr[b][r] = ex2(x[b][r] - u.m[0][b]);
+  // P' = p * s_v per token, one half2 per row holding both parities
+  const uint32_t hr0 = pack_h2(pr[0][0] * sv[0][0], pr[1][0] * sv[1][0]);  // row g
+  const uint32_t hr1 = pack_h2(pr[0][1] * sv[0][1], pr[1][1] * sv[1][1]);  // row g+8
+  {
+    const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&hr0));
+    const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&hr1));
+    u.zb[0][0] -= Gm::kBias * (f0.x + f1.x);  // the bias term of the exact fp16 P' the MMA sees
+    u.zb[0][1] -= Gm::kBias * (f0.y + f1.y);
+  }
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    u.l[0][b] += pr[b][0] + pr[b][1];
+    if constexpr (FMT == kINT4) u.zz[0][b] = fmaf(pr[b][0], zv[b][0], fmaf(pr[b][1], zv[b][1], u.zz[0][b]));
+  }
+  // ---- P'^T B fragments: column g = (query g & 3, parity g >> 2) ----
+  const int q = g & 3;
+  const int sa = tok_a<FMT>(t) * 4 + q, sb = tok_b<FMT>(t) * 4 + q;
+  const uint32_t ya0 = __shfl_sync(0xffffffffu, hr0, sa), yb0 = __shfl_sync(0xffffffffu, hr0, sb);
+  const uint32_t ya1 = __shfl_sync(0xffffffffu, hr1, sa), yb1 = __shfl_sync(0xffffffffu, hr1, sb);
+  const uint32_t sel = (g >> 2) ? 0x7632u : 0x5410u;
+  const uint32_t pb0 = __byte_perm(ya0, yb0, sel), pb1 = __byte_perm(ya1, yb1, sel);
+  // ---- O^T += V^T . P^T: block bi feeds only its own columns ----
+#pragma unroll
+  for (int bi = 0; bi < NB; ++bi) {
+    const bool mine = (g >> 2) == bi;
+    const uint32_t b0 = mine ? pb0 : 0u, b1 = mine ? pb1 : 0u;
+    uint32_t va[8][4];
+    load_v_frags<FMT>(sbs[bi] + kvq + wK, fo, va);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) mma16816(u.acc[mt][0], va[mt][0], va[mt][1], va[mt][2], va[mt][3], b0, b1);
+  }
+}
+
 // Folds the two packed streams (columns c and c + 4 = lanes t and t ^ 2) of
 // every query into one online-softmax state, as the merge kernel does.
 // Afterwards threads t < 2 hold the unit segment's state of queries 2t, 2t+1.

@@ -283,8 +283,11 @@ __device__ __forceinline__ void trace_ready(const DecodeParams& p, int warp, int
 
 // Formats whose consumer step runs two full blocks at a time (measured per format
 // with scripts/microbench_consumer.cu and in the kernel).
-template <int FMT, int NT, bool PK>
-constexpr bool kPairs = NT == 1 && (PK || FMT != kFP16);  // FP16 unpacked: no gain, spills
+template <int FMT, int NT, int PK>
+constexpr bool kPairs = NT == 1 && (PK != 0 || FMT != kFP16);  // FP16 unpacked: no gain, spills
+// PK = 2: the packed step with the integer QK (attend_iq; INT8/INT4 only)
+template <int FMT, int PK>
+constexpr bool kIQ = PK == 2 && (FMT == kINT8 || FMT == kINT4);
 
 // ------------------------------------------------------------------ kernel
 // CTA = HG consumer warps (one KV head each, a head group) + 1 producer warp.
@@ -299,9 +302,10 @@ constexpr bool kPairs = NT == 1 && (PK || FMT != kFP16);  // FP16 unpacked: no g
 // partial that merge_kernel (the PDL-launched successor) combines.
 // <= 152 registers for the 9-warp CTA: three warps on one SM sub-partition
 // then leave room for a merge warp (<= 56 registers) of a co-resident merge CTA
-// PK: packed step for G <= 4 (attend_pk): tile columns 0-3 and 4-7 attend
-// alternate blocks of the segment, folded at the segment end.
-template <int FMT, int NT, bool PK>
+// PK: packed step for G <= 4 (1: attend_pk, 2: attend_iq -- IMMA QK for the
+// integer formats): tile columns 0-3 and 4-7 attend alternate blocks of the
+// segment, folded at the segment end.
+template <int FMT, int NT, int PK>
 __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const DecodeParams p) {
   using Gm = Geo<FMT>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -522,7 +526,9 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
   // a segment's full blocks is just wait -> attend -> release; the unit's last
   // (partial, possibly freshly appended) block is peeled off.
   const FragOff fo = make_offsets<FMT>(g, t);
-  uint32_t qf[NT][8][2];
+  uint32_t qf[kIQ<FMT, PK> ? 1 : NT][kIQ<FMT, PK> ? 1 : 8][2];
+  uint32_t qi[4][2];
+  float qsc = 0.f, qzs = 0.f;  // integer QK: query t's score scale and zero term
   UnitState<NT> us;
   float qsb[NT][2], qst[NT][2];
   float kscale = 1.f, vscale = 1.f;
@@ -559,7 +565,10 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
     {  // ---- unit segment start: Q fragments, state ----
       const uint32_t qs = ui & 1;
       if (!compute_only) mbar_wait(&qfull[qs], (ui >> 1) & 1);
-      load_q_frags<FMT, NT, PK>(smem_u32(qbuf + qs * qslot) + warp * p.G * kD * 2, g, t, p.G, qf);
+      if constexpr (kIQ<FMT, PK>)
+        load_q_iq<FMT>(smem_u32(qbuf + qs * qslot) + warp * p.G * kD * 2, g, t, p.G, sml2, qi, qsc, qzs);
+      else
+        load_q_frags<FMT, NT, PK != 0>(smem_u32(qbuf + qs * qslot) + warp * p.G * kD * 2, g, t, p.G, qf);
       if (p.k_new != nullptr && has_last) {  // staged with Q by the producer
         const uint32_t nk = smem_u32(qbuf + qs * qslot + qbytes) + warp * kD * 2 + lane * 8;
         new_k = lds64(nk);
@@ -570,7 +579,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       ++ui;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        if constexpr (Gm::kBiased) {
+        if constexpr (Gm::kBiased && !kIQ<FMT, PK>) {
           // lo: k-slots 2t, 2t+1; hi: 2t+8, 2t+9 (carry 1/16 for INT4)
           float lo = 0.f, hi = 0.f;
 #pragma unroll
@@ -591,7 +600,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
           qst[nt][1] = __shfl_sync(0xffffffffu, stq, (2 * t + 1) * 4);
         }
         // packed: finite so a column stream that sees no block stays NaN-free
-        us.m[nt][0] = us.m[nt][1] = PK ? -1e30f : -INFINITY;
+        us.m[nt][0] = us.m[nt][1] = PK != 0 ? -1e30f : -INFINITY;
         us.l[nt][0] = us.l[nt][1] = 0.f;
         us.zb[nt][0] = us.zb[nt][1] = 0.f;
         us.zz[nt][0] = us.zz[nt][1] = 0.f;
@@ -630,22 +639,30 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         trace_ready(p, warp, lane, k + i + 1);
         const uint32_t sbs[2] = {sb, sb1};
         const int valid[2] = {kTPB, kTPB};
-        if constexpr (PK)
+        if constexpr (kIQ<FMT, PK>)
+          attend_iq<FMT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qi, qsc, qzs, g, t);
+        else if constexpr (PK != 0)
           attend_pk<FMT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
         else
           attend<FMT, NT, 2, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
         release();
         release();
-        if ((i % kFlush) == kFlush - 2) flush_bias<FMT, NT>(us);  // every kFlush blocks
+        if ((i % kFlush) == kFlush - 2) {  // every kFlush blocks
+          if constexpr (kIQ<FMT, PK>) flush_bias_iq<FMT>(us, g, t);
+          else flush_bias<FMT, NT>(us);
+        }
       }
     }
     for (; i < nfull; ++i) {
       if (!compute_only) mbar_wait_s(full_s + 8 * st, ph);
       trace_ready(p, warp, lane, k + i);
-      if constexpr (PK) {
+      if constexpr (PK != 0) {
         const uint32_t sbs[2] = {sb, sb};
         const int valid[2] = {kTPB, 0};
-        attend_pk<FMT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+        if constexpr (kIQ<FMT, PK>)
+          attend_iq<FMT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qi, qsc, qzs, g, t);
+        else
+          attend_pk<FMT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
       } else {
         const uint32_t sbs[1] = {sb};
         const int valid[1] = {kTPB};
@@ -653,7 +670,10 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
           attend<FMT, NT, 1, false>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
       }
       release();
-      if (i % kFlush == kFlush - 1) flush_bias<FMT, NT>(us);
+      if (i % kFlush == kFlush - 1) {
+        if constexpr (kIQ<FMT, PK>) flush_bias_iq<FMT>(us, g, t);
+        else flush_bias<FMT, NT>(us);
+      }
     }
     // ---- the unit's last block (partial; holds the appended token) ----
     if (has_last) {
@@ -680,10 +700,13 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         __syncwarp();
       }
       const int vlast = ctx_cur - static_cast<int>(cc.nblk - 1) * kTPB;
-      if constexpr (PK) {
+      if constexpr (PK != 0) {
         const uint32_t sbs[2] = {sb, sb};
         const int valid[2] = {vlast, 0};
-        attend_pk<FMT, 1, true>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
+        if constexpr (kIQ<FMT, PK>)
+          attend_iq<FMT, 1, true>(us, sbs, valid, wK, wP, kvq, pq, fo, qi, qsc, qzs, g, t);
+        else
+          attend_pk<FMT, 1, true>(us, sbs, valid, wK, wP, kvq, pq, fo, qf, qsb, qst, kscale, sml2, g, t);
       } else {
         const uint32_t sbs[1] = {sb};
         const int valid[1] = {vlast};
@@ -691,7 +714,8 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
       }
       release();
     }
-    if constexpr (PK) fold_halves(us);
+    if constexpr (kIQ<FMT, PK>) iq_state_to_acc(us, g, t);
+    if constexpr (PK != 0) fold_halves(us);
     const bool first_seg = k == 0;  // the segment opens this CTA's range
     k += seg_len;
     cc.b = seg_b0 + seg_len - 1;  // last block consumed
@@ -772,7 +796,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
 
 // Ring depth per format: ~150-200 KB in flight per SM with one CTA (HG
 // consumer warps + a producer) per SM.
-template <int FMT, int NT, bool PK>
+template <int FMT, int NT, int PK>
 static cudaError_t launch_fmt(const DecodeParams& p0, int num_sms, cudaStream_t stream) {
   using Gm = Geo<FMT>;
   DecodeParams p = p0;
@@ -869,14 +893,28 @@ cudaError_t launch_paged_decode(const DecodeParams& p, int kv_dtype, int num_sms
                                 cudaStream_t stream) {
   using namespace dev;
   const bool two = p.G > 8;
-  // packed G <= 4 step: INT4 by default (measured: INT4 B64 ctx4k 69.5 -> 66.5 us;
-  // FP8/INT8 neutral at large batch and ~0.5 us slower at B16, FP16 neutral)
-  const bool pk = p.G <= 4 && p.pack_mode != 1 && (kv_dtype == kINT4 || p.pack_mode == 2);
+  // packed G <= 4 step.  Default (pack_mode 0): the integer-QK packed step
+  // (attend_iq) for INT4 -- B64 ctx 4k 62.8 -> 57.1 us, B64 ctx 1300 28.4 ->
+  // 27.0 against the packed HMMA step -- and the plain step for the rest:
+  // INT8 on attend_iq measured neutral at B64 (HBM-bound) and 0.4 us slower at
+  // B16 (the per-segment Q split), packed HMMA neutral at large batch and
+  // ~0.5 us slower at B16 for FP8/INT8, neutral for FP16.  A/B switches:
+  // pack_mode 1 plain everywhere; 2 packed HMMA for every format; 3 packed
+  // HMMA for INT4 only (the previous default); 4 attend_iq for INT8 and INT4.
+  const bool small_g = p.G <= 4;
+  const bool integer = kv_dtype == kINT8 || kv_dtype == kINT4;
+  const int pk = !small_g || p.pack_mode == 1 ? 0
+                 : p.pack_mode == 0           ? (kv_dtype == kINT4 ? 2 : 0)
+                 : p.pack_mode == 2           ? 1
+                 : p.pack_mode == 3           ? (kv_dtype == kINT4 ? 1 : 0)
+                                              : (integer ? 2 : 0);
 #define KVSLAB_DECODE_CASE(F)                                          \
   case F:                                                              \
-    if (two) return launch_fmt<F, 2, false>(p, num_sms, stream);       \
-    if (pk) return launch_fmt<F, 1, true>(p, num_sms, stream);         \
-    return launch_fmt<F, 1, false>(p, num_sms, stream);
+    if (two) return launch_fmt<F, 2, 0>(p, num_sms, stream);           \
+    if (pk == 1) return launch_fmt<F, 1, 1>(p, num_sms, stream);       \
+    if constexpr (F == kINT8 || F == kINT4)                            \
+      if (pk == 2) return launch_fmt<F, 1, 2>(p, num_sms, stream);     \
+    return launch_fmt<F, 1, 0>(p, num_sms, stream);
   switch (kv_dtype) {
     KVSLAB_DECODE_CASE(kFP16)
     KVSLAB_DECODE_CASE(kFP8)

@@ -67,7 +67,7 @@ struct DecodeParams {
   uint32_t smem_budget;   // ring bytes per CTA; 0 = default
   uint32_t merge_threads; // merge CTA size cap; 0 = default (256)
   uint32_t merge_dc;      // probe override of the merge's dims split (0 = auto)
-  uint32_t pack_mode;     // packed G<=4 step: 0 = auto (INT4), 1 = off, 2 = all formats
+  uint32_t pack_mode;     // packed G<=4 step: 0 = auto, 1 = off, 2-4 A/B forms (decode.cu)
   int debug;     // bit0: skip math, bit1: skip partial merge (probes only)
   int pdl;       // launch with programmatic stream serialization
   unsigned long long* trace;  // probes: per-warp globaltimer stamps (nullable)

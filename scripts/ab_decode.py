@@ -19,6 +19,7 @@ L = int(os.environ.get("LAYERS", 8))
 configs = json.loads(os.environ.get("AB", '{"base": {}}'))
 cases = [c.split(":") for c in os.environ.get("CASES", "FP16:16:2048").split(",")]
 rounds = int(os.environ.get("ROUNDS", 5))
+noapp = os.environ.get("NOAPP") == "1"  # probe builds' compute-only mode cannot append
 for dtn, bs, cs in cases:
     dt, B, ctx0 = KvDtype[dtn], int(bs), int(cs)
     fmt = KvFormat(dt, 8, 32, 128, L)
@@ -45,7 +46,7 @@ for dtn, bs, cs in cases:
         def step():
             for l in range(L):
                 kv.paged_decode(pool, fmt, l, qs[l], m.table, ctx, kv_scales=sc, workspace=ws,
-                                k_new=kn, v_new=kn)
+                                k_new=None if noapp else kn, v_new=None if noapp else kn)
         with torch.cuda.stream(st):
             step(); torch.cuda.synchronize()
             with torch.cuda.graph(g, stream=st):

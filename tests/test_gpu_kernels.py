@@ -233,13 +233,14 @@ PACK_CASES = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["1", "2"], ids=["unpacked", "packed"])
+@pytest.mark.parametrize("mode", ["0", "1", "2", "4"], ids=["default", "unpacked", "packed_hmma", "packed_imma"])
 @pytest.mark.parametrize("dt,Hkv,Hq,ctx", PACK_CASES,
                          ids=[f"{c[0].name}-{c[1]}x{c[2]}" for c in PACK_CASES])
 def test_decode_packed_and_unpacked_steps(dt, Hkv, Hq, ctx, mode, monkeypatch):
-    """Both K2 inner steps for G <= 4 -- the packed one (tile columns 0-3 and
-    4-7 attend alternate blocks, folded per segment) and the plain one --
-    match the oracle for every format (the default picks one per format)."""
+    """Every K2 inner step for G <= 4 -- the packed ones (tile columns 0-3 and
+    4-7 attend alternate blocks, folded per segment; the default for INT8/INT4
+    computes QK on IMMA with 16-bit fixed-point Q) and the plain one -- match
+    the oracle for every format."""
     monkeypatch.setenv("KVSLAB_DECODE_PACK", mode)
     fmt = KvFormat(dt, Hkv, Hq, num_layers=1)
     sc = list(np.linspace(0.5, 1.5, 2 * Hkv)) if dt == KvDtype.FP8_E4M3 else None
