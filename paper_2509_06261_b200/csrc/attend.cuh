@@ -755,6 +755,37 @@ __device__ __forceinline__ void iq_state_to_acc(UnitState<1>& u, int g, int t) {
   u.zz[0][0] = o[0]; u.zz[0][1] = o[1];
 }
 
+// INT4 V for the integer step: row g (low-nibble dim) is fed the whole byte,
+// 1024 + 16 h + l (one PRMT per two values, no shift), row g+8 the high
+// nibble in place, 1024 + 16 h (LOP3); the epilogue recovers the low dim as
+// acc(g) - acc(g+8) (K2's o_lo for kIQ), so a word costs 4 instructions
+// instead of 5.  The other formats load as load_v_frags.
+template <int FMT>
+__device__ __forceinline__ void load_v_frags_iq(uint32_t sV, const FragOff& o, uint32_t (&a)[8][4]) {
+  if constexpr (FMT == kINT4) {
+    const uint4 va = lds128(sV + o.v[0]);  // tokens ta, tb
+    const uint4 vc = lds128(sV + o.v[1]);  // tokens ta+8, tb+8
+    const uint32_t A[4] = {va.x, va.y, va.z, va.w}, C[4] = {vc.x, vc.y, vc.z, vc.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t x0 = __byte_perm(A[j], 0x64646464u, 0x4240);  // [b0 64 b2 64]: m-tile 2j
+      const uint32_t x1 = __byte_perm(A[j], 0x64646464u, 0x4341);  // [b1 64 b3 64]: m-tile 2j+1
+      const uint32_t y0 = __byte_perm(C[j], 0x64646464u, 0x4240);
+      const uint32_t y1 = __byte_perm(C[j], 0x64646464u, 0x4341);
+      a[2 * j][0] = x0;
+      a[2 * j][1] = x0 & 0xFFF0FFF0u;
+      a[2 * j][2] = y0;
+      a[2 * j][3] = y0 & 0xFFF0FFF0u;
+      a[2 * j + 1][0] = x1;
+      a[2 * j + 1][1] = x1 & 0xFFF0FFF0u;
+      a[2 * j + 1][2] = y1;
+      a[2 * j + 1][3] = y1 & 0xFFF0FFF0u;
+    }
+  } else {
+    load_v_frags<FMT>(sV, o, a);
+  }
+}
+
 template <int FMT, int NB, bool MASK>
 __device__ __forceinline__ void attend_iq(UnitState<1>& u, const uint32_t (&sbs)[2], const int (&valid)[2],
                                           uint32_t wK, uint32_t wP, uint32_t kvq, uint32_t pq,
@@ -875,7 +906,7 @@ __device__ __forceinline__ void attend_iq(UnitState<1>& u, const uint32_t (&sbs)
     const bool mine = (g >> 2) == bi;
     const uint32_t b0 = mine ? pb0 : 0u, b1 = mine ? pb1 : 0u;
     uint32_t va[8][4];
-    load_v_frags<FMT>(sbs[bi] + kvq + wK, fo, va);
+    load_v_frags_iq<FMT>(sbs[bi] + kvq + wK, fo, va);
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) mma16816(u.acc[mt][0], va[mt][0], va[mt][1], va[mt][2], va[mt][3], b0, b1);
   }

@@ -741,6 +741,8 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         }
       // O rows g (lo) and g+8 (hi) of m-tile mt for query column c, unnormalised
       auto o_lo = [&](int mt, int nt, int c) {
+        // kIQ INT4: row g carried the whole byte (load_v_frags_iq)
+        if constexpr (kIQ<FMT, PK> && FMT == kINT4) return us.acc[mt][nt][c] - us.acc[mt][nt][2 + c] + zzf[nt][c];
         return us.acc[mt][nt][c] * vscale + zbf[nt][c] + zzf[nt][c];
       };
       auto o_hi = [&](int mt, int nt, int c) {
