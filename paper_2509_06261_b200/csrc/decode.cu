@@ -749,42 +749,81 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
         if constexpr (FMT == kINT4) return (us.acc[mt][nt][2 + c] + zbf[nt][c]) * 0.0625f + zzf[nt][c];
         else return us.acc[mt][nt][2 + c] * vscale + zbf[nt][c] + zzf[nt][c];
       };
+      // Vector stores: a lane's O values of one query column are the
+      // contiguous dims vdim(mt, g, r8) -- m-tiles 4h..4h+3 form 8 dims (one
+      // 16-byte fp16 store), m-tiles 2j, 2j+1 four (one 16-byte fp32 piece).
+      // After fold_halves (PK) lanes t and t^2 hold the same two columns, so
+      // each writes half of them and all 32 lanes store (the STG.64 form cost
+      // ~1 us per segment end at B16: 16 scattered stores per active lane).
+      auto half_run = [&](int nt, int c, int h, float inv) {
+        auto w = [&](int k) { return pack_h2(o_lo(4 * h + k, nt, c) * inv, o_hi(4 * h + k, nt, c) * inv); };
+        return make_uint4(w(0), w(1), w(2), w(3));
+      };
+      auto piece = [&](int nt, int c, int j) {
+        return make_float4(o_lo(2 * j, nt, c), o_hi(2 * j, nt, c), o_lo(2 * j + 1, nt, c), o_hi(2 * j + 1, nt, c));
+      };
       if (whole) {
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        if constexpr (PK != 0) {
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const int q = nt * 8 + 2 * t + c;
+            const int q = 2 * (t & 1) + c, h = t >> 1;
             if (q >= static_cast<int>(p.G)) continue;
-            const float inv = 1.f / lf[nt][c];
+            const float inv = 1.f / lf[0][c];
             __half* orow = p.out + (static_cast<uint64_t>(cc.s) * Hq + head * p.G + q) * kD;
-#pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-              const int d0 = vdim<FMT>(mt, g, 0);
-              *reinterpret_cast<__half2*>(orow + d0) =
-                  __floats2half2_rn(o_lo(mt, nt, c) * inv, o_hi(mt, nt, c) * inv);
-            }
-            if (p.lse && g == 0)
+            const uint4 r0 = half_run(0, c, 0, inv), r1 = half_run(0, c, 1, inv);  // static indices
+            *reinterpret_cast<uint4*>(orow + vdim<FMT>(4 * h, g, 0)) =
+                h ? r1 : r0;
+            if (p.lse && g == 0 && t < 2)
               p.lse[static_cast<uint64_t>(cc.s) * Hq + head * p.G + q] =
-                  (us.m[nt][c] + __log2f(lf[nt][c])) * 0.69314718055994531f;
+                  (us.m[0][c] + __log2f(lf[0][c])) * 0.69314718055994531f;
           }
+        } else {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int q = nt * 8 + 2 * t + c;
+              if (q >= static_cast<int>(p.G)) continue;
+              const float inv = 1.f / lf[nt][c];
+              __half* orow = p.out + (static_cast<uint64_t>(cc.s) * Hq + head * p.G + q) * kD;
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                *reinterpret_cast<uint4*>(orow + vdim<FMT>(4 * h, g, 0)) = half_run(nt, c, h, inv);
+              if (p.lse && g == 0)
+                p.lse[static_cast<uint64_t>(cc.s) * Hq + head * p.G + q] =
+                    (us.m[nt][c] + __log2f(lf[nt][c])) * 0.69314718055994531f;
+            }
+        }
       } else {
         // partial slot: (2*cta + [0 first | 1 last segment of the CTA]) * HG + warp
         float* ps = p.partials + ((2ull * blockIdx.x + (first_seg ? 0 : 1)) * HG + warp) * slot_f;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        if constexpr (PK != 0) {
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const int q = nt * 8 + 2 * t + c;
+            const int q = 2 * (t & 1) + c;
             if (q >= static_cast<int>(p.G)) continue;
-            if (g == 0) *reinterpret_cast<float2*>(ps + 2 * q) = make_float2(us.m[nt][c], lf[nt][c]);
+            if (g == 0 && t < 2) *reinterpret_cast<float2*>(ps + 2 * q) = make_float2(us.m[0][c], lf[0][c]);
+            // pieces 2i + (t >> 1): lanes t, t^2 fill adjacent 16 bytes (one 32-byte sector)
 #pragma unroll
-            for (int mt = 0; mt < 8; ++mt) {
-              const int d0 = vdim<FMT>(mt, g, 0);
-              *reinterpret_cast<float2*>(ps + slot_hdr + q * kD + d0) =
-                  make_float2(o_lo(mt, nt, c), o_hi(mt, nt, c));
+            for (int i = 0; i < 2; ++i) {
+              const int j = 2 * i + (t >> 1);
+              const float4 a0 = piece(0, c, 2 * i), a1 = piece(0, c, 2 * i + 1);  // static indices
+              *reinterpret_cast<float4*>(ps + slot_hdr + q * kD + vdim<FMT>(2 * j, g, 0)) = (t >> 1) ? a1 : a0;
             }
           }
+        } else {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int q = nt * 8 + 2 * t + c;
+              if (q >= static_cast<int>(p.G)) continue;
+              if (g == 0) *reinterpret_cast<float2*>(ps + 2 * q) = make_float2(us.m[nt][c], lf[nt][c]);
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<float4*>(ps + slot_hdr + q * kD + vdim<FMT>(2 * j, g, 0)) = piece(nt, c, j);
+            }
+        }
       }
     }
     cursor_next(cc, pre, p.batch, NG);
