@@ -733,10 +733,13 @@ class Group:
             self.ctx[mi][:self.B].copy_(self.ctx_host[mi, :self.B], non_blocking=True)
         self.ctx_ev.record(main)
 
-    def admit_rows(self, mi, rows, prompts, src_fn=None):
+    def admit_rows(self, mi, rows, prompts, src_fn=None, stream=None):
         """Prefill claim (simulator.cpp:500-526) + K1 append of the prompts'
-        K/V for every layer (src_fn(T): the e2e leg's copy of the T prompt
-        tokens' K/V from host memory).  Returns the K1 algorithmic bytes."""
+        K/V for every layer (src_fn(T, mi): the e2e leg's copy of the T prompt
+        tokens' K/V from host memory).  The K1 launches go to `stream` (the
+        model's own: co-located engines prefill side by side, as they decode)
+        after the claim's table upload on the main stream.  Returns the K1
+        algorithmic bytes."""
         torch, kv = self.torch, self.kv
         m = self.models[mi]
         main = torch.cuda.current_stream(self.dev)
@@ -757,10 +760,13 @@ class Group:
             self.tok_dev[mi, j, :T].copy_(self.tok_host[mi, j, :T], non_blocking=True)
         self.tok_ev[mi].record(main)
         ts, tp = self.tok_dev[mi, 0, :T], self.tok_dev[mi, 1, :T]
-        src = self.src if src_fn is None else src_fn(T)
+        src = self.src if src_fn is None else src_fn(T, mi)
+        st = main if stream is None else stream
+        if st is not main:
+            st.wait_stream(main)
         for layer in range(self.L):
             kv.kv_append(self.pool, m.fmt, layer, src[0, :T], src[1, :T], ts, tp, m.table,
-                         self.scales, stream=main)
+                         self.scales, stream=st)
         return self.L * m.fmt.append_bytes(T)
 
     def stranded(self):
@@ -789,7 +795,9 @@ class Group:
             else:
                 rows = list(range(self.B, target))
                 prompts = self.rng.integers(512, 2049, size=len(rows)).tolist()
-                k1 += self.admit_rows(mi, rows, prompts, src_fn)
+                k1 += self.admit_rows(mi, rows, prompts, src_fn, stream=self.streams[mi])
+        for st in self.streams:  # every model's admission K1 done before compaction / the step
+            main.wait_stream(st)
         self.B = target
         for m in self.models:
             m.sync(main)
@@ -967,15 +975,16 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
                 h2d += bs["inbuf"].numel() * 2
             main.wait_stream(up)
 
-            def src_fn(T):  # admitted prompts' K/V come from the host too (copy stream)
+            def src_fn(T, mi):  # admitted prompts' K/V come from the host too (copy stream)
                 nonlocal h2d
+                dst = e2e["src_dev"][mi]  # per model: the models' K1 run concurrently
                 with torch.cuda.stream(up):
                     up.wait_stream(main)
                     for i in range(2):  # K, V: contiguous pinned rows -> device
-                        e2e["src_dev"][i][:T].copy_(e2e["src_host"][i][:T], non_blocking=True)
+                        dst[i][:T].copy_(e2e["src_host"][i][:T], non_blocking=True)
                 main.wait_stream(up)
                 h2d += 2 * T * grp.hkv * D * 2
-                return e2e["src_dev"]
+                return dst
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(main)
         if B != grp.B:
@@ -1047,7 +1056,7 @@ def make_e2e(grp):
     e2e = {"host": host, "up": torch.cuda.Stream(grp.dev), "down": torch.cuda.Stream(grp.dev)}
     if grp.max_prompt_tokens:
         e2e["src_host"] = [grp.src[i].cpu().pin_memory() for i in range(2)]
-        e2e["src_dev"] = torch.empty_like(grp.src)
+        e2e["src_dev"] = [torch.empty_like(grp.src) for _ in grp.models]
     return e2e
 
 

@@ -451,6 +451,10 @@ static void quant_row(const orc_fmt* f, const uint16_t* x16, float fp8_scale, ui
     }
     uint16_t sh = orc_f32_to_f16((mx - mn) / 15.0f);
     uint16_t zh = orc_f32_to_f16(mn);
+    /* a NaN parameter (an all-NaN row, or inf - inf) is stored as the one
+       encoding 0x7e00: the sign of a generated NaN is platform-defined */
+    if ((sh & 0x7fffu) > 0x7c00u) sh = 0x7e00u;
+    if ((zh & 0x7fffu) > 0x7c00u) zh = 0x7e00u;
     float sf = orc_f16_to_f32(sh), zf = orc_f16_to_f32(zh);
     for (uint32_t i = 0; i < d; i += 2) {
       int q[2];

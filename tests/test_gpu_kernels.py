@@ -167,6 +167,55 @@ def test_integer_quantisation_rounding_ties(dt):
     assert (got == img).all()
 
 
+@pytest.mark.parametrize("dt", [KvDtype.INT8, KvDtype.INT4], ids=["INT8", "INT4"])
+@pytest.mark.parametrize("H", [8, 4])
+def test_integer_quantisation_special_rows(dt, H):
+    """K1's fast path rounds by a magic-number add with no clamp; the rows it
+    must hand to the IEEE path are exactly those where that is unsafe: NaN /
+    +-inf elements, and scales that round to fp16 subnormals (tiny rows).
+    Every such row (and ordinary ones around them) must give the oracle's
+    bytes, on the H = 8 compile-time path and the generic one."""
+    fmt = KvFormat(dt, H, H, num_layers=1)
+    rng = np.random.default_rng(11)
+    rows = []
+    for kind in range(12):
+        r = rng.standard_normal(128).astype(np.float32)
+        if kind == 1:
+            r[rng.integers(128)] = np.nan
+        elif kind == 2:
+            r[rng.integers(128)] = np.inf
+        elif kind == 3:
+            r[rng.integers(128)] = -np.inf
+        elif kind == 4:
+            r *= 1e-6  # scale below 2^-14: subnormal fp16
+        elif kind == 5:
+            r *= 3e-4  # around the normal / subnormal scale boundary
+        elif kind == 6:
+            r[:] = 0.0
+        elif kind == 7:
+            r[:] = 1.25
+        elif kind == 8:
+            r = np.where(r > 0, 65504.0, -65504.0).astype(np.float32)
+        elif kind == 9:
+            r *= 2.0 ** -20  # fp16 subnormal inputs
+        elif kind == 10:
+            r[:] = np.nan
+        elif kind == 11:
+            r[::2] = -0.0
+        rows.append(r.astype(np.float16))
+    x = np.stack(rows)  # [12, 128]
+    T = 2 * 16
+    k = np.stack([x[(t + np.arange(H)) % len(rows)] for t in range(T)])  # [T, H, 128]
+    v = np.stack([x[(3 * t + 5 + np.arange(H)) % len(rows)] for t in range(T)])
+    w = make_world(fmt, [T], seed=2, churn=False)
+    w["k"], w["v"] = k, v
+    append_gpu(w, fmt, 0)
+    img, _ = oracle_image(w, fmt, 0)
+    got = kv.kv_tensor(w["pool"]).cpu().numpy()
+    bad = np.nonzero(got != img)[0]
+    assert bad.size == 0, f"{bad.size} bytes differ, first at {bad[:8]}"
+
+
 def rel_err(o, r):
     o = o.reshape(-1, o.shape[-1]).astype(np.float64)
     r = r.reshape(-1, r.shape[-1])
