@@ -216,6 +216,42 @@ def test_integer_quantisation_special_rows(dt, H):
     assert bad.size == 0, f"{bad.size} bytes differ, first at {bad[:8]}"
 
 
+@pytest.mark.parametrize("H", [8, 4])
+def test_fp8_special_rows_and_scales(H):
+    """FP8 K1 fast path: select-free division with the sign of x OR-ed in
+    (exact for positive scales); non-finite elements and zero / negative /
+    non-finite scales go to the IEEE path.  Bytes must equal the oracle's."""
+    fmt = KvFormat(KvDtype.FP8_E4M3, H, H, num_layers=1)
+    rng = np.random.default_rng(12)
+    rows = []
+    for kind in range(6):
+        r = (rng.standard_normal(128) * 40).astype(np.float32)
+        if kind == 1:
+            r[rng.integers(128)] = np.nan
+        elif kind == 2:
+            r[rng.integers(128)] = np.inf
+        elif kind == 3:
+            r[rng.integers(128)] = -np.inf
+        elif kind == 4:
+            r[::3] = -0.0
+            r[1::3] = 0.0
+        elif kind == 5:
+            r *= 1e-7
+        rows.append(r.astype(np.float16))
+    x = np.stack(rows)
+    T = 16
+    k = np.stack([x[(t + np.arange(H)) % len(rows)] for t in range(T)])
+    v = np.stack([x[(2 * t + 1 + np.arange(H)) % len(rows)] for t in range(T)])
+    scales = np.array([0.5, -1.0, 2.0, 0.0, 1.0, -0.25, 3.0, 1e-3] * 2, np.float32)[:2 * H]
+    w = make_world(fmt, [T], seed=3, churn=False, fp8_scale=scales)
+    w["k"], w["v"] = k, v
+    append_gpu(w, fmt, 0)
+    img, _ = oracle_image(w, fmt, 0)
+    got = kv.kv_tensor(w["pool"]).cpu().numpy()
+    bad = np.nonzero(got != img)[0]
+    assert bad.size == 0, f"{bad.size} bytes differ, first at {bad[:8]}: {got[bad[:8]]} vs {img[bad[:8]]}"
+
+
 def rel_err(o, r):
     o = o.reshape(-1, o.shape[-1]).astype(np.float64)
     r = r.reshape(-1, r.shape[-1])
