@@ -37,10 +37,10 @@ for spec in os.environ.get("CASES", "FP8_E4M3:16:2048").split(","):
     st = torch.cuda.Stream()
     def step():
         for l in range(L):
-            os.environ["KVSLAB_DECODE_TRACE"] = str(tr[l].data_ptr())
+            ks._lib.lib.ks_probe_set_decode_trace(pool.handle, tr[l].data_ptr())
             kv.paged_decode(pool, fmt, l, qs[l], m.table, ctx, kv_scales=sc, workspace=ws,
                             k_new=kn, v_new=kn)
-        del os.environ["KVSLAB_DECODE_TRACE"]
+        ks._lib.lib.ks_probe_set_decode_trace(pool.handle, None)
     with torch.cuda.stream(st):
         step(); torch.cuda.synchronize()
         with torch.cuda.graph(g, stream=st):
@@ -64,9 +64,17 @@ for spec in os.environ.get("CASES", "FP8_E4M3:16:2048").split(","):
     print(f"{dtn} B={B} ctx={ctx0}: {live.sum()} CTAs, {nst} stages/CTA; prev merge done {prev_merge_done:.2f}; "
           f"CTA start p50 {np.median(us(cta[live,0])):.2f}; cons done p50/max {np.median(us(cta[live,5])):.2f}/{us(cta[live,5]).max():.2f}")
     pc = lambda x: "/".join("%6.2f" % np.percentile(x, q) for q in (10, 50, 90))
-    for k in range(min(nst, 32)):
-        ok = (iss[:, k] > 0) & (rdy[:, k] > 0)
-        if not ok.any():
-            continue
-        print(f"  stage {k:2d}: issue {pc(us(iss[ok, k]))}  ready {pc(us(rdy[ok, k]))}  lat {pc((rdy[ok,k]-iss[ok,k])/1e3)}")
+    # CTAs whose block range holds a unit start past its first block (two segments)
+    C = int(live.sum())
+    nblk = (ctx0 + 15) // 16
+    T = B * nblk  # one head group of 8
+    bnd = np.array([any(c * T // C < u * nblk < (c + 1) * T // C for u in range(1, B)) for c in range(C)])
+    for name, sel in (("interior", ~bnd), ("boundary", bnd)):
+        print(f" {name} CTAs ({sel.sum()}): start p50 {np.median(us(cta[:C][sel,0])):.2f} data p50 "
+              f"{np.median(us(cta[:C][sel,4])):.2f} cons done p10/50/90 {pc(us(cta[:C][sel,5]))}")
+        for k in range(min(nst, 32)):
+            ok = sel & (iss[:, k] > 0) & (rdy[:, k] > 0)
+            if not ok.any():
+                continue
+            print(f"  stage {k:2d}: issue {pc(us(iss[ok, k]))}  ready {pc(us(rdy[ok, k]))}  lat {pc((rdy[ok,k]-iss[ok,k])/1e3)}")
     del pool
