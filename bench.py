@@ -73,6 +73,7 @@ LOCAL = int(os.environ.get("LOCAL_RANK", "0"))
 HQ, HKV, D = 32, 8, 128
 DT_NAMES = {0: "fp16", 1: "fp8_e4m3", 2: "int8", 3: "int4"}
 C4_WAVE = (64, 8)
+DEBUG = bool(os.environ.get("BENCH_DEBUG"))
 C4_SLAB = 64 << 20
 C4_TRIGGER = 0.25
 
@@ -164,9 +165,13 @@ def config_dict(wl, batch, ctx, extra=None):
 # Phase schedules shared by both arms
 # ======================================================================
 def c4_phase_targets(warmup, steps, phase_steps):
-    """Batch per model for every step: warm-up at the wave's high value, then
-    the timed steps alternate low / high every phase_steps steps."""
-    out = [C4_WAVE[0]] * warmup
+    """Batch per model for every step: the warm-up runs one low / high cycle
+    (so the first shrink, compaction, slab scrub and admission -- lazy module
+    loads, first-touch costs: up to 35 ms once on a fresh box -- happen before
+    the timed region) and ends high; the timed steps then alternate low / high
+    every phase_steps steps."""
+    lo = warmup // 2 if warmup >= 3 else 0
+    out = [C4_WAVE[1]] * lo + [C4_WAVE[0]] * (warmup - lo)
     for k in range(steps):
         out.append(C4_WAVE[(k // max(1, phase_steps) + 1) % 2])
     return out
@@ -638,6 +643,8 @@ class Group:
             self.src = torch.randn(2, max_prompt_tokens, hkv, D, dtype=torch.float16, device=dev)
             n = len(self.fmts)
             self.tok_host = torch.zeros(n, 2, max_prompt_tokens, dtype=torch.int32).pin_memory()
+            self.tok_host_np = self.tok_host.numpy()  # same (pinned) memory
+            self.arange_np = np.arange(max_prompt_tokens, dtype=np.int32)
             self.tok_dev = torch.zeros(n, 2, max_prompt_tokens, dtype=torch.int32, device=dev)
             self.tok_ev = [torch.cuda.Event() for _ in range(n)]
             for e in self.tok_ev:
@@ -736,11 +743,15 @@ class Group:
     def admit_rows(self, mi, rows, prompts, src_fn=None, stream=None):
         """Prefill claim (simulator.cpp:500-526) + K1 append of the prompts'
         K/V for every layer (src_fn(T, mi): the e2e leg's copy of the T prompt
-        tokens' K/V from host memory).  The K1 launches go to `stream` (the
-        model's own: co-located engines prefill side by side, as they decode)
-        after the claim's table upload on the main stream.  Returns the K1
-        algorithmic bytes."""
-        torch, kv = self.torch, self.kv
+        tokens' K/V from host memory).  Returns the K1 algorithmic bytes."""
+        T = self.prepare_admission(mi, rows, prompts)
+        return self.launch_admission(mi, T, src_fn, stream)
+
+    def prepare_admission(self, mi, rows, prompts):
+        """Host half of an admission: the claims, the table delta upload and
+        the token -> (row, position) lists (pinned staging buffer, reused once
+        its previous upload finished), all on the main stream.  Returns T."""
+        torch = self.torch
         m = self.models[mi]
         main = torch.cuda.current_stream(self.dev)
         for s, p in zip(rows, prompts):
@@ -751,14 +762,30 @@ class Group:
         if T == 0:
             return 0
         assert T <= self.max_prompt_tokens
-        # token -> (row, position) lists through this model's pinned staging
-        # buffer (reused once its previous upload finished), no host sync
         self.tok_ev[mi].synchronize()
-        self.tok_host[mi, 0, :T] = torch.from_numpy(np.repeat(np.asarray(rows, np.int32), np.asarray(prompts)))
-        self.tok_host[mi, 1, :T] = torch.from_numpy(np.concatenate([np.arange(p, dtype=np.int32) for p in prompts]))
+        # numpy writes into the pinned buffer (one memcpy on this thread: a
+        # torch slice copy went through the intra-op thread pool and was
+        # measured stalling 4-7 ms at a time)
+        hv = self.tok_host_np[mi]
+        hv[0, :T] = np.repeat(np.asarray(rows, np.int32), np.asarray(prompts))
+        o = 0
+        for p in prompts:
+            hv[1, o:o + p] = self.arange_np[:p]
+            o += p
         for j in range(2):  # contiguous pinned rows: asynchronous DMA
             self.tok_dev[mi, j, :T].copy_(self.tok_host[mi, j, :T], non_blocking=True)
         self.tok_ev[mi].record(main)
+        return T
+
+    def launch_admission(self, mi, T, src_fn=None, stream=None):
+        """Device half: the K1 launches of every layer on `stream` (the
+        model's own: co-located engines prefill side by side, as they decode),
+        ordered after the main stream's uploads."""
+        if T == 0:
+            return 0
+        torch, kv = self.torch, self.kv
+        m = self.models[mi]
+        main = torch.cuda.current_stream(self.dev)
         ts, tp = self.tok_dev[mi, 0, :T], self.tok_dev[mi, 1, :T]
         src = self.src if src_fn is None else src_fn(T, mi)
         st = main if stream is None else stream
@@ -793,9 +820,26 @@ class Group:
                         m.release(s)
                 m.condense(keep)
             else:
+                # model by model, so the device runs model i's K1 while the
+                # host prepares model i+1 (preparing all four first left the
+                # GPU idle for the whole host half: measured 0.5-5 ms per grow)
                 rows = list(range(self.B, target))
                 prompts = self.rng.integers(512, 2049, size=len(rows)).tolist()
-                k1 += self.admit_rows(mi, rows, prompts, src_fn, stream=self.streams[mi])
+                if DEBUG:
+                    sc0 = self.kv.scrubbed_bytes(self.pool)
+                    e_a = self.torch.cuda.Event(enable_timing=True)
+                    e_a.record(main)
+                T = self.prepare_admission(mi, rows, prompts)
+                if DEBUG:
+                    e_b = self.torch.cuda.Event(enable_timing=True)
+                    e_b.record(main)
+                k1 += self.launch_admission(mi, T, src_fn, stream=self.streams[mi])
+                if DEBUG:
+                    e_c = self.torch.cuda.Event(enable_timing=True)
+                    e_c.record(self.streams[mi])
+                    e_c.synchronize()
+                    print(f"[debug] grow model {mi}: T {T} scrub {(self.kv.scrubbed_bytes(self.pool)-sc0)/1e9:.2f} GB "
+                          f"prep(dev) {e_a.elapsed_time(e_b):.3f} K1(dev) {e_b.elapsed_time(e_c):.3f} ms", file=sys.stderr)
         for st in self.streams:  # every model's admission K1 done before compaction / the step
             main.wait_stream(st)
         self.B = target
@@ -1024,6 +1068,7 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
         adm = sum(e[0].elapsed_time(e[1]) for _, _, e in reb)
         cmp_ = sum(e[1].elapsed_time(e[2]) for _, _, e in reb)
         bd["admission_ms"] = round(adm, 3)
+        bd["phase_change_ms_each"] = [round(e[0].elapsed_time(e[1]), 3) for _, _, e in reb]
         bd["admission_k1_gbs"] = round(sum(k for k, _, _ in reb) / max(adm, 1e-9) / 1e6, 1)
         bd["compaction_ms"] = round(cmp_, 3)
         k3b = sum(k for _, k, _ in reb)
@@ -1114,6 +1159,12 @@ def measure(name, dev, clocks_index, with_e2e=True, tune=True):
     shares = shares or None
     warm, timed = targets[:ARGS.warmup], targets[ARGS.warmup:]
     time_steps(grp, warm)
+    # the serving loop's long-lived objects out of the cyclic collector: a
+    # full collection inside a host-side admission was measured stalling the
+    # device 4-6 ms (gc.freeze, as serving engines do)
+    import gc
+    gc.collect()
+    gc.freeze()
     if WORLD > 1:
         import torch.distributed as dist
         dist.barrier()

@@ -58,5 +58,7 @@ def test_c4_phase_schedule():
     finally:
         sys.argv = argv
     t = mod.c4_phase_targets(5, 20, 5)
-    assert t == [64] * 5 + [8] * 5 + [64] * 5 + [8] * 5 + [64] * 5
+    # warm-up: one low / high cycle ending high; timed: 8, 64, 8, 64 (5 steps each)
+    assert t == [8] * 2 + [64] * 3 + [8] * 5 + [64] * 5 + [8] * 5 + [64] * 5
+    assert mod.c4_phase_targets(2, 4, 2) == [64] * 2 + [8] * 2 + [64] * 2
     assert mod.WL is mod.WORKLOADS["c4"]
