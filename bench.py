@@ -73,7 +73,6 @@ LOCAL = int(os.environ.get("LOCAL_RANK", "0"))
 HQ, HKV, D = 32, 8, 128
 DT_NAMES = {0: "fp16", 1: "fp8_e4m3", 2: "int8", 3: "int4"}
 C4_WAVE = (64, 8)
-DEBUG = bool(os.environ.get("BENCH_DEBUG"))
 C4_SLAB = 64 << 20
 C4_TRIGGER = 0.25
 
@@ -640,7 +639,12 @@ class Group:
         # K1 prompt source (admissions): fp16 K and V rows, larger than L2
         self.max_prompt_tokens = max_prompt_tokens
         if max_prompt_tokens:
-            self.src = torch.randn(2, max_prompt_tokens, hkv, D, dtype=torch.float16, device=dev)
+            # one prompt K/V source per model: co-located engines' prefills are
+            # distinct data (a shared source let the four models' concurrent
+            # K1 reads hit each other's L2 lines)
+            self.src_m = [torch.randn(2, max_prompt_tokens, hkv, D, dtype=torch.float16, device=dev)
+                          for _ in self.fmts]
+            self.src = self.src_m[0]
             n = len(self.fmts)
             self.tok_host = torch.zeros(n, 2, max_prompt_tokens, dtype=torch.int32).pin_memory()
             self.tok_host_np = self.tok_host.numpy()  # same (pinned) memory
@@ -652,6 +656,8 @@ class Group:
         self.compactions, self.moves, self.slabs_freed = 0, 0, 0
         self.stranded_trace, self.frag_trace = [], []
         self.reb_marks = []  # (K1 bytes, K3 bytes, events) per phase change
+        self.pending_prompts = None  # e2e: prompts of the next admission, drawn ahead
+        self.step_ms_est = {}  # device ms per step by batch (+ "grow"), from the timed leg
 
     # ---- step buffers ----
     def buffers(self, B):
@@ -787,7 +793,7 @@ class Group:
         m = self.models[mi]
         main = torch.cuda.current_stream(self.dev)
         ts, tp = self.tok_dev[mi, 0, :T], self.tok_dev[mi, 1, :T]
-        src = self.src if src_fn is None else src_fn(T, mi)
+        src = self.src_m[mi] if src_fn is None else src_fn(T, mi)
         st = main if stream is None else stream
         if st is not main:
             st.wait_stream(main)
@@ -824,22 +830,17 @@ class Group:
                 # host prepares model i+1 (preparing all four first left the
                 # GPU idle for the whole host half: measured 0.5-5 ms per grow)
                 rows = list(range(self.B, target))
-                prompts = self.rng.integers(512, 2049, size=len(rows)).tolist()
-                if DEBUG:
-                    sc0 = self.kv.scrubbed_bytes(self.pool)
-                    e_a = self.torch.cuda.Event(enable_timing=True)
-                    e_a.record(main)
+                if self.pending_prompts is not None:  # e2e: drawn (and copied) ahead
+                    prompts = self.pending_prompts[mi]
+                    assert len(prompts) == len(rows)
+                else:
+                    prompts = self.rng.integers(512, 2049, size=len(rows)).tolist()
                 T = self.prepare_admission(mi, rows, prompts)
-                if DEBUG:
-                    e_b = self.torch.cuda.Event(enable_timing=True)
-                    e_b.record(main)
                 k1 += self.launch_admission(mi, T, src_fn, stream=self.streams[mi])
-                if DEBUG:
-                    e_c = self.torch.cuda.Event(enable_timing=True)
-                    e_c.record(self.streams[mi])
-                    e_c.synchronize()
-                    print(f"[debug] grow model {mi}: T {T} scrub {(self.kv.scrubbed_bytes(self.pool)-sc0)/1e9:.2f} GB "
-                          f"prep(dev) {e_a.elapsed_time(e_b):.3f} K1(dev) {e_b.elapsed_time(e_c):.3f} ms", file=sys.stderr)
+        # the phase change's small host->device uploads (tables, token lists)
+        # are all issued: bulk copies on other streams may go after this
+        self.uploads_done = self.torch.cuda.Event()
+        self.uploads_done.record(main)
         for st in self.streams:  # every model's admission K1 done before compaction / the step
             main.wait_stream(st)
         self.B = target
@@ -1007,6 +1008,56 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
     if e2e:
         up, down = e2e["up"], e2e["down"]
     e0.record(main)
+    # e2e: the admitted prompts' K/V come from host memory too.  They are
+    # pipelined like the step inputs: two device staging slots per model
+    # (alternate admissions), the next admission's prompts drawn right after
+    # the previous one and their K/V copied in chunks issued on the copy
+    # stream right after each step's own input copy -- sized to the PCIe time
+    # the step's compute leaves (about 50 GB/s x the step's device time,
+    # less the next step's inputs) -- so the copies overlap the steps instead
+    # of stalling the admission.  The step waits only for its own inputs.
+    pf = None
+    n_models = len(grp.models)
+    tok_bytes = grp.hkv * D * 2  # one token's K (or V) rows, fp16
+    pcie = 50e9  # bytes/s budget per second of device time (H2D measured 55 GB/s)
+    est_ms = {b: grp.step_ms_est.get(b, 4.3 * b / 64) for b in set(targets)}
+    est_ms["grow"] = grp.step_ms_est.get("grow", 10.0)
+
+    def next_grow(k):
+        return next((j for j in range(k, len(targets)) if targets[j] > (targets[j - 1] if j else grp.B)), None)
+
+    def plan_prefetch(k):
+        """Prompts for the next admission at or after step k, and their copy queue."""
+        g = next_grow(k)
+        if g is None:
+            return None
+        before = targets[g - 1] if g else grp.B
+        prompts = {mi: grp.rng.integers(512, 2049, size=targets[g] - before).tolist() for mi in range(n_models)}
+        slot = e2e["slot"]
+        queue = [[mi, i, 0, int(sum(prompts[mi]))] for mi in range(n_models) for i in range(2)]
+        return {"g": g, "prompts": prompts, "queue": queue, "slot": slot, "waited": set(),
+                "ready": [torch.cuda.Event() for _ in range(n_models)]}
+
+    def pump(limit_bytes):
+        """Issue up to `limit_bytes` of the pending prompt copies on `up`."""
+        nonlocal h2d
+        limit = int(limit_bytes // tok_bytes)
+        while pf["queue"] and limit > 0:
+            q = pf["queue"][0]
+            mi, i, lo, hi = q
+            if mi not in pf["waited"]:  # the admission before last is done with this slot
+                up.wait_event(e2e["src_free"][pf["slot"]][mi])
+                pf["waited"].add(mi)
+            n = min(hi - lo, limit)
+            e2e["src_dev"][pf["slot"]][mi][i][lo:lo + n].copy_(e2e["src_host"][i][lo:lo + n], non_blocking=True)
+            h2d += n * tok_bytes
+            q[2] += n
+            limit -= n
+            if q[2] == hi:
+                pf["queue"].pop(0)
+                if i == 1:
+                    pf["ready"][mi].record(up)
+
     for k, B in enumerate(targets):
         X = k & 1
         src_fn = None
@@ -1014,26 +1065,36 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
             hin, hout, free_ev = e2e["host"](B)
             bs = grp.buffers(B)[X]
             with torch.cuda.stream(up):
+                if pf is not None and k == pf["g"]:
+                    pump(1 << 62)  # whatever did not fit in the earlier steps
                 up.wait_event(free_ev[X])
                 bs["inbuf"].copy_(hin[X], non_blocking=True)
                 h2d += bs["inbuf"].numel() * 2
-            main.wait_stream(up)
+                in_ready = torch.cuda.Event()
+                in_ready.record(up)
+            main.wait_event(in_ready)
 
-            def src_fn(T, mi):  # admitted prompts' K/V come from the host too (copy stream)
-                nonlocal h2d
-                dst = e2e["src_dev"][mi]  # per model: the models' K1 run concurrently
-                with torch.cuda.stream(up):
-                    up.wait_stream(main)
-                    for i in range(2):  # K, V: contiguous pinned rows -> device
-                        dst[i][:T].copy_(e2e["src_host"][i][:T], non_blocking=True)
-                main.wait_stream(up)
-                h2d += 2 * T * grp.hkv * D * 2
-                return dst
+            if pf is not None and k == pf["g"]:
+                grp.pending_prompts = pf["prompts"]
+                src_slot, src_ready = pf["slot"], pf["ready"]
+
+                def src_fn(T, mi):  # this admission's prompts, copied ahead
+                    grp.streams[mi].wait_event(src_ready[mi])
+                    return e2e["src_dev"][src_slot][mi]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(main)
+        grew = phase_changed = False
         if B != grp.B:
+            phase_changed = True
+            grew = B > grp.B
             k1, k3 = grp.rebalance(B, src_fn)
             nbytes += k1 + k3
+            if src_fn is not None:  # this slot is free again after these K1
+                for mi, st in enumerate(grp.streams):
+                    e2e["src_free"][src_slot][mi].record(st)
+                grp.pending_prompts = None
+                e2e["slot"] ^= 1
+                pf = None
         ev[1].record(main)
         marks.append((B, ev))
         nbytes += grp.host_step()
@@ -1044,6 +1105,23 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
             grp.graph(B, X if e2e else 0).replay()
             graph_launches += grp.n_launch_graph[(B, X if e2e else 0)]
         ev[2].record(main)
+        if e2e and grp.max_prompt_tokens:
+            # the next admission's prompts ride in the PCIe time this step's
+            # compute leaves (after its own inputs, before the next step's)
+            if pf is None:
+                pf = plan_prefetch(k + 1)
+            if pf is not None and k + 1 < pf["g"]:
+                nxt = targets[k + 1]
+                # (half the admission's time: copies beside the four models'
+                # K1 were measured slowing it; 0 / 0.5 / 1 gave 3.94 / 4.07 / 4.0 TB/s)
+                budget = pcie * (est_ms[B] + (0.5 * est_ms["grow"] if grew else 0.0)) / 1e3 \
+                    - grp.buffers(nxt)[0]["inbuf"].numel() * 2
+                with torch.cuda.stream(up):
+                    if phase_changed:
+                        # a bulk copy queued ahead of the phase change's small
+                        # uploads on the copy engine stalled the admission 13 ms
+                        up.wait_event(grp.uploads_done)
+                    pump(max(0.0, budget))
         if e2e:
             done = torch.cuda.Event()
             done.record(main)
@@ -1101,7 +1179,14 @@ def make_e2e(grp):
     e2e = {"host": host, "up": torch.cuda.Stream(grp.dev), "down": torch.cuda.Stream(grp.dev)}
     if grp.max_prompt_tokens:
         e2e["src_host"] = [grp.src[i].cpu().pin_memory() for i in range(2)]
-        e2e["src_dev"] = [torch.empty_like(grp.src) for _ in grp.models]
+        # two staging slots per model: admissions alternate, so the next one's
+        # prompts can be copied while the last one's K1 still reads its slot
+        e2e["src_dev"] = [[torch.zeros_like(grp.src) for _ in grp.models] for _ in range(2)]
+        e2e["src_free"] = [[torch.cuda.Event() for _ in grp.models] for _ in range(2)]
+        for sl in e2e["src_free"]:
+            for e in sl:
+                e.record()
+        e2e["slot"] = 0
     return e2e
 
 
@@ -1123,7 +1208,11 @@ def build_group(name, dev, seed):
     """The GPU arm's Group for a workload and its step schedule."""
     wl = WORKLOADS[name]
     total = ARGS.warmup + ARGS.steps
-    e2e_steps = max(4, ARGS.steps)
+    # the e2e leg runs two of the timed schedule back to back: its prompt
+    # copies are pipelined one admission ahead, and the leg's first admission
+    # (nothing before it to overlap with) would otherwise weigh as much as a
+    # steady-state one
+    e2e_steps = max(8, 2 * ARGS.steps)
     if name == "c4":
         max_ctx = 2048 + 3 * (total + e2e_steps) + 16
         grp = Group(dev, wl["dts"], C4_WAVE[0], max_ctx, ARGS.layers, slab=C4_SLAB, seed=seed,
@@ -1171,6 +1260,10 @@ def measure(name, dev, clocks_index, with_e2e=True, tune=True):
     c0, m0, s0 = grp.compactions, grp.moves, grp.slabs_freed
     st0 = len(grp.stranded_trace)
     ms, nbytes, tokens, launches, _, _, clk = time_steps(grp, timed, clocks_index=clocks_index)
+    bd = time_steps.breakdown
+    grp.step_ms_est = {b: bd[f"step_ms_B{b}"] for b in set(timed) if f"step_ms_B{b}" in bd}
+    if bd.get("phase_change_ms_each"):
+        grp.step_ms_est["grow"] = max(bd["phase_change_ms_each"])
     res = dict(ms=ms, bytes=nbytes, tokens=tokens, launches=launches, clocks=clk, shares=shares,
                breakdown=time_steps.breakdown,
                compactions=grp.compactions - c0, moves=grp.moves - m0, slabs_freed=grp.slabs_freed - s0,
@@ -1180,7 +1273,8 @@ def measure(name, dev, clocks_index, with_e2e=True, tune=True):
         for B in set(e2e_targets):  # pinned host buffers before the timed region
             e2e["host"](B)
         r = time_steps(grp, e2e_targets, e2e=e2e)
-        res["e2e"] = dict(ms=r[0], bytes=r[1], h2d=r[4] / len(e2e_targets), d2h=r[5] / len(e2e_targets))
+        res["e2e"] = dict(ms=r[0], bytes=r[1], h2d=r[4] / len(e2e_targets), d2h=r[5] / len(e2e_targets),
+                          breakdown=time_steps.breakdown, steps=len(e2e_targets))
         r = time_steps(grp, e2e_targets, e2e=e2e, eager=True)
         res["e2e_eager"] = dict(ms=r[0], bytes=r[1], h2d=r[4] / len(e2e_targets), d2h=r[5] / len(e2e_targets))
     if max(targets) != grp.B:  # the kernels at the workload's largest batch
@@ -1244,6 +1338,7 @@ def summarise(name, r, peak, peak_kind, world):
         out["e2e"] = {"value": round(eb / (ems / 1e3) / 1e9, 2), "unit": "GB/s",
                       "h2d_bytes_per_step": int(e["h2d"]), "d2h_bytes_per_step": int(e["d2h"]),
                       "mode": "CUDA-graph replay of each step; inputs from pinned host memory, outputs back",
+                      "steps": e.get("steps"), "ms": round(ems, 3), "breakdown": e.get("breakdown"),
                       "eager": {"value": round(xb / (xms / 1e3) / 1e9, 2), "unit": "GB/s",
                                 "mode": "per-layer ks_paged_decode_append calls from Python (ctypes), no graph"}}
     if name == "c4":
