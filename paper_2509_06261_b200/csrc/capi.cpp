@@ -172,6 +172,12 @@ struct ks_pool {
   void destroy_device() {
     if (device >= 0) {
       DeviceGuard g(device);
+      // A pool may be destroyed (e.g. by a garbage collector) while another
+      // stream of this thread is being captured into a graph; in the default
+      // global capture mode cudaFree / cudaEventSynchronize would invalidate
+      // that capture.  Relaxed mode for this thread while we tear down.
+      cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+      const bool swapped = cudaThreadExchangeStreamCaptureMode(&mode) == cudaSuccess;
       if (fence) cudaEventSynchronize(fence), cudaEventDestroy(fence);
       for (int i = 0; i < kSlots; ++i)
         if (slot_ev[i]) cudaEventSynchronize(slot_ev[i]), cudaEventDestroy(slot_ev[i]);
@@ -179,6 +185,7 @@ struct ks_pool {
       cudaFree(d_slab_table);
       cudaFree(d_stage);
       cudaFreeHost(h_stage);
+      if (swapped) cudaThreadExchangeStreamCaptureMode(&mode);
     }
   }
   // Next staging slot, waiting for its previous consumer if still running.

@@ -567,3 +567,32 @@ def test_block_table_remap_beyond_one_staging_slot():
     got = table.cpu().numpy()
     assert (got[:n] == dst).all() and (got[n:2 * n] == dst).all()
     assert got[-2] == 6 and got[-1] == 10**6
+
+
+def test_pool_destroyed_during_another_capture():
+    """A pool torn down (here: close(); in practice a garbage collector) while
+    another pool's decode is being captured into a CUDA graph must not
+    invalidate that capture (the teardown's cudaFree / event syncs run in
+    relaxed capture mode)."""
+    fmt = KvFormat(KvDtype.FP8_E4M3, 8, 32, num_layers=1)
+    w = make_world(fmt, [40, 300], seed=21, churn=False,
+                   fp8_scale=np.ones(16, np.float32))
+    append_gpu(w, fmt, 0)
+    doomed = ks.SlabPool(ks.SlabPoolConfig(8 * fmt.key * 4, fmt.key * 4, [fmt.key]), device=0)
+    kv.kv_tensor(doomed).zero_()
+    q = dev(np.random.default_rng(3).standard_normal((2, 32, 128)).astype(np.float16))
+    table, ctx, sc = dev(w["table"]), dev(w["ctx"]), dev(w["scales"])
+    ws = kv.DecodeWorkspace(w["pool"], fmt, 2)
+    out = kv.paged_decode(w["pool"], fmt, 0, q, table, ctx, kv_scales=sc, workspace=ws)
+    torch.cuda.synchronize()
+    ref = out.clone()
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            kv.paged_decode(w["pool"], fmt, 0, q, table, ctx, out=out, kv_scales=sc, workspace=ws)
+            doomed.close()  # teardown in the middle of the capture
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
