@@ -946,6 +946,12 @@ class Group:
                     w0 = [ww[0] * skew] + ww[1:]
                     cands.add(tuple(max(8, min(tot - 8, int(tot * x / sum(w0)))) for x in w0))
         cands.add(tuple([nsm] * n))  # no partition: every model's grid spans the GPU
+        # the consumer-bound INT4 model fenced into k SMs, the HBM-bound
+        # models sharing the rest without a partition among themselves
+        if any(int(f.kv_dtype) == 3 for f in self.fmts) and n > 1:
+            for k4 in (24, 30, 37, 44, 52):
+                for rest in (nsm - k4, nsm - k4 + 12, nsm):
+                    cands.add(tuple(k4 if int(f.kv_dtype) == 3 else min(nsm, rest) for f in self.fmts))
         bs = self.buffers(B)[0]
         main = torch.cuda.current_stream(self.dev)
         times = {}
