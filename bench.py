@@ -952,6 +952,11 @@ class Group:
             for k4 in (24, 30, 37, 44, 52):
                 for rest in (nsm - k4, nsm - k4 + 12, nsm):
                     cands.add(tuple(k4 if int(f.kv_dtype) == 3 else min(nsm, rest) for f in self.fmts))
+        if n > 2:  # proportional splits that overlap (caps summing past the SM count)
+            ww = [wbytes[int(f.kv_dtype)] * (2.0 if int(f.kv_dtype) == 3 else 1.0) for f in self.fmts]
+            for over in (1.1, 1.2, 1.35, 1.5):
+                tot = nsm * over
+                cands.add(tuple(max(8, min(nsm, int(tot * x / sum(ww)))) for x in ww))
         bs = self.buffers(B)[0]
         main = torch.cuda.current_stream(self.dev)
         times = {}
@@ -980,12 +985,14 @@ class Group:
             g.replay()
             torch.cuda.synchronize(self.dev)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(main)
-            for _ in range(3):
+            reps = []
+            for _ in range(5):  # best of 5 timed replays (single replays are noisy)
+                a.record(main)
                 g.replay()
-            b.record(main)
-            torch.cuda.synchronize(self.dev)
-            times[c] = a.elapsed_time(b) / 3
+                b.record(main)
+                torch.cuda.synchronize(self.dev)
+                reps.append(a.elapsed_time(b))
+            times[c] = min(reps)
             del g
         pick = min(times, key=times.get)
         for m, sh in zip(self.models, pick):
