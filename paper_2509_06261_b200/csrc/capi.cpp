@@ -114,6 +114,8 @@ Tuning Tuning::from_env() {
   t.merge_dc = static_cast<uint32_t>(num("KVSLAB_MERGE_DC", 0));
   t.decode_pack = static_cast<uint32_t>(num("KVSLAB_DECODE_PACK", 0));
   t.pdl = num("KVSLAB_NO_PDL", 0) ? 0 : 1;
+  t.append_per_sm = static_cast<uint32_t>(num("KVSLAB_APPEND_PER_SM", 0));
+  t.decode_min_blocks = static_cast<uint32_t>(num("KVSLAB_DECODE_MIN_BLOCKS", 0));
   t.prefill_nt = static_cast<uint32_t>(num("KVSLAB_PREFILL_NT", 0));
   t.prefill_tc = static_cast<int>(num("KVSLAB_PREFILL_TC", 2));
   t.prefill_expand = static_cast<int>(num("KVSLAB_PREFILL_EXPAND", -1));
@@ -809,6 +811,7 @@ ks_status ks_kv_append(ks_pool* pool, const ks_kv_format* fmt, uint32_t layer, c
     p.block_table = d_block_table;
     p.bt_stride = bt_stride;
     p.kv_scales = d_kv_scales;
+    p.ctas_per_sm = pool->tuning.append_per_sm;
     cudaError_t fe = prepare(pool, static_cast<cudaStream_t>(stream));
     if (fe != cudaSuccess) return cuda_fail(fe, "launch prologue (fence / slab scrub)");
     cudaError_t e = kvslab::launch_kv_append(p, static_cast<int>(fmt->kv_dtype),
@@ -886,6 +889,7 @@ static ks_status decode_impl(ks_pool* pool, const ks_kv_format* fmt, uint32_t la
     p.pack_mode = tu.decode_pack;
     p.debug = tu.decode_debug;
     p.pdl = tu.pdl;
+    p.min_blocks = tu.decode_min_blocks;
     p.trace = tu.decode_trace;  // probe builds only (Tuning::from_env)
     cudaError_t fe = prepare(pool, static_cast<cudaStream_t>(stream));
     if (fe != cudaSuccess) return cuda_fail(fe, "launch prologue (fence / slab scrub)");

@@ -95,8 +95,10 @@ constexpr uint32_t kMinBlocksPerCta = 4;
 // with very short contexts (a few blocks per unit) four units serialised on
 // one CTA -- a Q load, the fused append and an epilogue each -- cost more
 // than the blocks (FP8 B8 ctx 16: 9.3 us per launch against 3.7 us at B1).
-__device__ __forceinline__ uint32_t effective_ctas(uint32_t total, uint32_t grid, uint32_t units) {
-  const uint32_t want = max((total + kMinBlocksPerCta - 1) / kMinBlocksPerCta, min(units, total));
+__device__ __forceinline__ uint32_t effective_ctas(uint32_t total, uint32_t grid, uint32_t units,
+                                                   uint32_t min_blocks) {
+  const uint32_t mb = min_blocks ? min_blocks : kMinBlocksPerCta;
+  const uint32_t want = max((total + mb - 1) / mb, min(units, total));
   return max(1u, min(grid, want));
 }
 
@@ -159,7 +161,7 @@ __global__ void __maxnreg__(56) merge_kernel(const DecodeParams p, uint32_t WS, 
   const uint32_t nblk = (static_cast<uint32_t>(ctx_s) + kTPB - 1) / kTPB;
   const uint32_t total = all * NG;
   const uint32_t U0 = before * NG + grp * nblk;
-  const CtaSplit sp = make_split(total, effective_ctas(total, grid, p.batch * NG));
+  const CtaSplit sp = make_split(total, effective_ctas(total, grid, p.batch * NG, p.min_blocks));
   const uint32_t ca = cta_of(U0, sp), cb = cta_of(U0 + nblk - 1, sp);
   if (ca == cb) {  // whole unit: the decode kernel wrote it
     if (blockIdx.x == 0) pdl_wait();
@@ -400,7 +402,7 @@ __global__ void __maxnreg__(NT == 1 ? 152 : 255) paged_decode_kernel(const Decod
 
   // small launches use fewer CTAs (>= kMinBlocksPerCta blocks each) so a unit
   // is not cut into more partials than the work justifies
-  const uint32_t C = effective_ctas(total, gridDim.x, p.batch * NG);
+  const uint32_t C = effective_ctas(total, gridDim.x, p.batch * NG, p.min_blocks);
   if (blockIdx.x >= C) return;  // uniform across the CTA
   const CtaSplit sp = make_split(total, C);
   const uint32_t cs = cta_start(blockIdx.x, sp), ce = cta_start(blockIdx.x + 1, sp);

@@ -33,6 +33,8 @@ struct Tuning {
   int decode_debug = 0;            // KVSLAB_DECODE_DEBUG (probe builds only)
   unsigned long long* decode_trace = nullptr;  // KVSLAB_DECODE_TRACE (probe builds only)
   int pdl = 1;                     // KVSLAB_NO_PDL=1 -> 0
+  uint32_t append_per_sm = 0;      // KVSLAB_APPEND_PER_SM (K1 CTAs per SM, 0 = occupancy)
+  uint32_t decode_min_blocks = 0;  // KVSLAB_DECODE_MIN_BLOCKS (K2 blocks per CTA floor, 0 = default)
   uint32_t prefill_nt = 0;         // KVSLAB_PREFILL_NT
   int prefill_tc = 2;              // KVSLAB_PREFILL_TC
   int prefill_debug = 0;           // KVSLAB_PREFILL_DEBUG (probe builds only)
@@ -70,6 +72,7 @@ struct DecodeParams {
   uint32_t pack_mode;     // packed G<=4 step: 0 = auto, 1 = off, 2-4 A/B forms (decode.cu)
   int debug;     // bit0: skip math, bit1: skip partial merge (probes only)
   int pdl;       // launch with programmatic stream serialization
+  uint32_t min_blocks;    // >= this many blocks per CTA (0 = kMinBlocksPerCta)
   unsigned long long* trace;  // probes: per-warp globaltimer stamps (nullable)
 };
 
@@ -113,6 +116,7 @@ struct AppendParams {
   const int32_t* block_table;
   uint32_t bt_stride;
   const float* kv_scales;
+  uint32_t ctas_per_sm;  // 0 = every resident slot (occupancy); else at most this many per SM
 };
 
 struct CompactParams {

@@ -62,3 +62,30 @@ def test_c4_phase_schedule():
     assert t == [8] * 2 + [64] * 3 + [8] * 5 + [64] * 5 + [8] * 5 + [64] * 5
     assert mod.c4_phase_targets(2, 4, 2) == [64] * 2 + [8] * 2 + [64] * 2
     assert mod.WL is mod.WORKLOADS["c4"]
+
+
+@pytest.mark.gpu
+def test_bench_line_contract():
+    """One short c4 run prints ONE JSON line with the contract's keys: the
+    BASELINE metric, device value, roofline (with ncu traffic), e2e through
+    host buffers with its copy bytes, clocks, our own kernel launches, and
+    the CPU baseline."""
+    p = _run(["--steps", "4", "--warmup", "3", "--phase-steps", "2", "--no-sweep", "--no-c3"])
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    base = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+    assert d["metric"] == "slab paged-decode attention HBM GB/s" and d["unit"] == "GB/s"
+    assert d["n_gpus"] == 1 and d["steps"] == 4 and d["warmup"] == 3 and d["higher_is_better"]
+    assert d["config"]["workload"].startswith("c4")
+    assert d["value"] > 0 and d["gpu_launches"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and 0 < r["frac"] <= 1.2 and r["peak"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["value"] < d["value"] * 1.05  # through PCIe: not faster than the device leg
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    cb = d["cpu_baseline"]
+    assert cb["value"] > 0 and cb["kind"] == "port" and cb["cores"] >= 1
+    assert base  # BASELINE.json readable next to the bench
