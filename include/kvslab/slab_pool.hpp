@@ -163,6 +163,7 @@ class SlabPool {
   // stale bytes must be cleared before a kernel reads a block slot past a
   // sequence's context (a foreign format's bytes can be NaN patterns).
   void drain_scrub_slabs(std::vector<std::uint32_t>* out);
+  bool has_scrub_slabs() const noexcept { return !scrub_.empty(); }
 
  private:
   int key_index(Bytes key) const;  // -1 if unregistered

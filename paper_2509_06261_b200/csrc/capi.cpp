@@ -251,6 +251,7 @@ cudaError_t wait_fence(ks_pool* p, cudaStream_t s) {
 // last call (SlabPool::drain_scrub_slabs), on `s`, ahead of the launch that
 // follows.  Not while `s` is being captured: a graph must not replay it.
 cudaError_t scrub_slabs(ks_pool* p, cudaStream_t s) {
+  if (!p->pool->has_scrub_slabs()) return cudaSuccess;  // the common case: no runtime call
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaError_t e = cudaStreamIsCapturing(s, &cs);
   if (e != cudaSuccess || cs != cudaStreamCaptureStatusNone) return e;

@@ -79,6 +79,17 @@ class KvFormat:
         return L.ks_kv_format(int(self.kv_dtype), self.num_kv_heads, self.num_q_heads,
                               self.head_dim, self.num_layers, self.tokens_per_block, self.qparams)
 
+    def c_ref(self):
+        """byref of this format's C struct, built once per format (the C side
+        only reads it during the call): the per-layer hot paths skip the
+        struct construction."""
+        r = self.__dict__.get("_c_ref")
+        if r is None:
+            c = self.to_c()
+            r = (c, C.byref(c))
+            object.__setattr__(self, "_c_ref", r)
+        return r[1]
+
     def shard(self, tp: int) -> "KvFormat":
         """Format of one tensor-parallel shard: KV and Q
         heads split over `tp` GPUs, each shard an ordinary pool over its heads.
@@ -197,8 +208,7 @@ def kv_append(pool: SlabPool, fmt: KvFormat, layer: int, k: torch.Tensor, v: tor
     """K1: quantise + write n tokens' K/V ([n, Hkv, d] fp16) into their slab blocks."""
     assert k.dtype == torch.float16 and v.dtype == torch.float16
     assert k.is_contiguous() and v.is_contiguous() and block_table.dtype == torch.int32
-    f = fmt.to_c()
-    check(L.lib.ks_kv_append(pool.handle, C.byref(f), layer, _ptr(k), _ptr(v), k.shape[0],
+    check(L.lib.ks_kv_append(pool.handle, fmt.c_ref(), layer, _ptr(k), _ptr(v), k.shape[0],
                              _ptr(tok_seq), _ptr(tok_pos), _ptr(block_table),
                              block_table.stride(0), _ptr(kv_scales), _stream(stream)))
 
@@ -266,16 +276,16 @@ def paged_decode(pool: SlabPool, fmt: KvFormat, layer: int, q: torch.Tensor,
         out = torch.empty_like(q)
     if workspace is None:
         workspace = _default_decode_ws(pool, fmt, B, stream)
-    f = fmt.to_c()
+    f = fmt.c_ref()
     scale = 0.0 if sm_scale is None else float(sm_scale)
     if k_new is None:
-        check(L.lib.ks_paged_decode(pool.handle, C.byref(f), layer, _ptr(q), _ptr(out), _ptr(lse),
+        check(L.lib.ks_paged_decode(pool.handle, f, layer, _ptr(q), _ptr(out), _ptr(lse),
                                     _ptr(block_table), block_table.stride(0), _ptr(ctx_lens), B,
                                     scale, _ptr(kv_scales), _ptr(workspace.buf), workspace.nbytes,
                                     _stream(stream)))
     else:
         assert k_new.dtype == torch.float16 and k_new.is_contiguous() and v_new.is_contiguous()
-        check(L.lib.ks_paged_decode_append(pool.handle, C.byref(f), layer, _ptr(q), _ptr(k_new),
+        check(L.lib.ks_paged_decode_append(pool.handle, f, layer, _ptr(q), _ptr(k_new),
                                            _ptr(v_new), _ptr(out), _ptr(lse), _ptr(block_table),
                                            block_table.stride(0), _ptr(ctx_lens), B, scale,
                                            _ptr(kv_scales), _ptr(workspace.buf), workspace.nbytes,
