@@ -617,3 +617,31 @@ def test_pool_destroyed_during_another_capture():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("dt", FORMATS, ids=[d.name for d in FORMATS])
+@pytest.mark.parametrize("sms", [1, 7, 37, 111])
+def test_decode_under_sm_share(dt, sms):
+    """A model's SM share (ks_set_decode_sm_share, the co-location fence the
+    bench autotunes -- e.g. INT4 in 37 SMs) changes the grid and so every
+    unit's CTA split and merge: the outputs must still match the oracle, from
+    one CTA (no split) to most of the GPU."""
+    fmt = KvFormat(dt, 8, 32, num_layers=2)
+    ctx = [1300, 17, 2048, 1, 700, 64, 0, 333]
+    sc = list(np.linspace(0.5, 2.0, 16)) if dt == KvDtype.FP8_E4M3 else None
+    w = make_world(fmt, ctx, seed=sms + int(dt), fp8_scale=sc)
+    append_gpu(w, fmt, 0)
+    kv.set_decode_sm_share(w["pool"], fmt.key, sms)
+    img = kv.kv_tensor(w["pool"]).cpu().numpy()
+    q = w["rng"].standard_normal((len(ctx), 32, 128)).astype(np.float16)
+    out = kv.paged_decode(w["pool"], fmt, 0, dev(q), dev(w["table"]), dev(w["ctx"]),
+                          kv_scales=None if w["scales"] is None else dev(w["scales"]))
+    torch.cuda.synchronize()
+    f = oracle.fmt(int(dt), 8, 32, 128, 2, 16, fmt.qparams)
+    ref, _ = oracle.paged_decode(img, w["pool"].slab_size(), w["pool"].blocks_per_slab(fmt.key), f, 0,
+                                 q.view(np.uint16), w["table"], w["ctx"], 1 / math.sqrt(128), w["scales"],
+                                 nthreads=oracle.NPROC)
+    o = out.cpu().numpy()
+    live = w["ctx"] > 0
+    assert rel_err(o[live], ref[live]) <= TOL[dt]
+    assert (o[~live] == 0).all()
