@@ -13,14 +13,17 @@ compaction on every key when the stranded free-block bytes exceed 25 % of the
 bytes in formatted slabs.  A decode step = host growth rule
 (kvslab::SeqTable, simulator.cpp:561-578) + table delta upload, then one CUDA
 graph: per layer and model one fused K1+K2 launch, the models on their own
-streams.
+streams with SM shares autotuned per batch size (the consumer-bound INT4
+model fenced into a few dozen SMs at B = 64).  The warm-up runs one low /
+high cycle; the timed steps then alternate 8, 64, 8, 64 (--phase-steps each).
 
 value  = algorithmic HBM bytes (K2 decode + K1 appends + K3 moves, SURVEY.md
          8d) / device time of exactly --steps steps (phase changes included),
          whole job over all ranks (max-over-ranks time).
-e2e    = the same stream of steps through the public API with every step's
+e2e    = the same schedule (twice) through the public API with every step's
          inputs (Q, new K/V, admitted prompts' K/V) copied in from pinned host
-         memory and O copied back; graph replay, plus an eager variant.
+         memory and O copied back (prompt K/V pipelined one admission ahead);
+         graph replay, plus an eager variant.
 roofline = the FP16 K2 launch (dominant kernel) timed live by CUDA events.
 c3     = BASELINE configs[2] (FP16 + INT4 co-located, B8, ctx 8k), same
          contract, nested in the line (N=1).
