@@ -1081,6 +1081,8 @@ def time_steps(grp, targets, clocks_index=None, e2e=None, eager=False):
             hin, hout, free_ev = e2e["host"](B)
             bs = grp.buffers(B)[X]
             with torch.cuda.stream(up):
+                if pf is None and grp.max_prompt_tokens and B > grp.B:
+                    pf = plan_prefetch(k)  # an admission nothing was copied ahead for
                 if pf is not None and k == pf["g"]:
                     pump(1 << 62)  # whatever did not fit in the earlier steps
                 up.wait_event(free_ev[X])
