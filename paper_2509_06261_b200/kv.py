@@ -31,6 +31,9 @@ class KvDtype(enum.IntEnum):
 _BITS = {KvDtype.FP16: 16, KvDtype.FP8_E4M3: 8, KvDtype.INT8: 8, KvDtype.INT4: 4}
 
 
+_C_FMT_CACHE: dict = {}
+
+
 @dataclass(frozen=True)
 class KvFormat:
     """Per-model KV format (ks_kv_format).  quant_param_bytes_per_block=None
@@ -80,14 +83,14 @@ class KvFormat:
                               self.head_dim, self.num_layers, self.tokens_per_block, self.qparams)
 
     def c_ref(self):
-        """byref of this format's C struct, built once per format (the C side
-        only reads it during the call): the per-layer hot paths skip the
-        struct construction."""
-        r = self.__dict__.get("_c_ref")
+        """byref of this format's C struct, built once per distinct format
+        (the C side only reads it during the call): the per-layer hot paths
+        skip the struct construction.  Cached by value outside the instance,
+        so formats stay plain picklable dataclasses."""
+        r = _C_FMT_CACHE.get(self)
         if r is None:
             c = self.to_c()
-            r = (c, C.byref(c))
-            object.__setattr__(self, "_c_ref", r)
+            r = _C_FMT_CACHE[self] = (c, C.byref(c))
         return r[1]
 
     def shard(self, tp: int) -> "KvFormat":
